@@ -1,0 +1,136 @@
+/*
+ * sptrsv_b200 — C ABI of the B200-native synchronization-free sparse lower
+ * triangular solver (fp64, L x = b). Plain pointers and sizes only: no torch,
+ * no C++ types, no exceptions cross this boundary.
+ *
+ * The reference package has no FFI; its operator API is the Python function
+ * set re-exported from /root/reference/pkg/src/sptrsv/__init__.py:10-48. Each
+ * entry point below names the reference function whose contract it serves, so
+ * a binding (ctypes here) can sit exactly where the
+ * reference's Python engine sits today (cli.py:149-150 `_run_engine`).
+ *
+ * Threading: a plan is not re-entrant; distinct plans may be used concurrently
+ * (SPEC.md:451). Every call is synchronous unless its name ends in _async.
+ */
+#ifndef SPTRSV_B200_H
+#define SPTRSV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python shim maps them 1:1 onto the reference exception
+ * classes of errors.py (ZeroDiagonal, MissingDiagonal, MatrixStructureError,
+ * DimensionMismatch, SolveTimeout, InvalidPeCount). */
+enum {
+  SPTRSV_OK = 0,
+  SPTRSV_E_DIMENSION = 1,        /* DimensionMismatch        errors.py:62   */
+  SPTRSV_E_ZERO_DIAGONAL = 2,    /* ZeroDiagonal(col)        errors.py:52   */
+  SPTRSV_E_MISSING_DIAGONAL = 3, /* MissingDiagonal(col)     errors.py:46   */
+  SPTRSV_E_STRUCTURE = 4,        /* MatrixStructureError     errors.py:42   */
+  SPTRSV_E_TIMEOUT = 5,          /* SolveTimeout             errors.py:82   */
+  SPTRSV_E_INVALID_PE = 6,       /* InvalidPeCount           errors.py:68   */
+  SPTRSV_E_CUDA = 7,             /* CUDA runtime failure (no reference class) */
+  SPTRSV_E_ARGUMENT = 8,         /* ValueError                               */
+  SPTRSV_E_UNSUPPORTED = 9
+};
+
+/* Arithmetic of the solve. EXACT reproduces solve_serial (reference.py:20-35)
+ * bit for bit; FAST pre-scales rows by 1/l_ii and uses FMA (max relative
+ * error vs the oracle ~1e-15, contract 1e-12). */
+enum { SPTRSV_PRECISION_EXACT = 0, SPTRSV_PRECISION_FAST = 1 };
+
+/* Which device executor runs the solve. ROWS: sync-free component pool over
+ * a level-ordered ticket queue (paper Alg. 3). CHAINS: lane-chain lockstep
+ * warps over contiguous row tasks. AUTO picks by the analysis statistics. */
+enum { SPTRSV_EXECUTOR_AUTO = 0, SPTRSV_EXECUTOR_ROWS = 1, SPTRSV_EXECUTOR_CHAINS = 2 };
+
+/* plan flags */
+enum {
+  SPTRSV_PLAN_STRUCTURE_ONLY = 1 /* analysis only: diagonal may be missing/zero, values may be NULL */
+};
+
+typedef struct sptrsv_options {
+  int32_t precision;      /* SPTRSV_PRECISION_* */
+  int32_t executor;       /* SPTRSV_EXECUTOR_* */
+  int32_t device;         /* CUDA ordinal */
+  int32_t flags;          /* SPTRSV_PLAN_* */
+  double timeout_s;       /* device watchdog, SolverConfig.timeout (engine.py:75) */
+  int32_t spin_initial;   /* Backoff.initial_pause (engine.py:61-66) */
+  int32_t spin_max_ns;    /* Backoff.max_pause, as nanoseconds of __nanosleep */
+  int32_t chain_lanes;    /* chains executor: lanes per warp task (<=32); 0 = 32 */
+  int32_t reserved[7];
+} sptrsv_options;
+
+typedef struct sptrsv_stats {
+  double setup_ms;        /* plan creation (upload, K1, transpose, levels, schedule) */
+  double solve_ms;        /* device time of the last solve (CUDA events) */
+  double h2d_ms, d2h_ms;  /* host<->device copies of the last host-buffer solve */
+  int64_t spins;          /* polls that found a dependency unsolved (lock_wait_spins) */
+  int64_t remote_reads;   /* dependency loads from another PE's segment */
+  int64_t launches;       /* kernels launched by the last solve */
+  int32_t executor;       /* executor that ran */
+  int32_t n_levels;
+} sptrsv_stats;
+
+typedef struct sptrsv_plan sptrsv_plan;
+
+/* Fill defaults (exact, auto, device 0, 60 s, Backoff(16, 512)). */
+void sptrsv_default_options(sptrsv_options* opt);
+
+/* Upload a CSC lower-triangular L (the CscMatrix arrays, matrix.py:35-57) and
+ * run validation + in-degree + transpose + level analysis on the device.
+ * Replaces: column_lists + ensure_lower_triangular + Phase-1 counting of
+ * solve_partitioned (engine.py:442-490) and compute_level_schedule
+ * (analysis.py:43-64). On a lower-triangular violation returns
+ * SPTRSV_E_{MISSING,ZERO}_DIAGONAL / STRUCTURE and stores the column in
+ * *bad_col (the reference's first violation by (col, kind), matrix.py:150). */
+int sptrsv_plan_create(const int64_t* col_ptr, const int64_t* row_idx, const double* values, int64_t n,
+                       const sptrsv_options* opt, sptrsv_plan** out, int64_t* bad_col);
+
+/* compute_in_degrees (analysis.py:19-27): int64[n], bit-exact. */
+int sptrsv_plan_in_degrees(const sptrsv_plan* plan, int64_t* out);
+
+/* compute_level_schedule (analysis.py:43-64): level_of int64[n]; components
+ * grouped by level ascending (order int64[n], level_ptr int64[n_levels+1]). */
+int sptrsv_plan_levels(const sptrsv_plan* plan, int64_t* level_of, int64_t* order, int64_t* level_ptr,
+                       int64_t* n_levels);
+
+/* Structure-only conveniences on raw CSC arrays (no plan kept). in_degree
+ * accepts any structurally valid square CSC, like the reference. */
+int sptrsv_in_degrees(const int64_t* col_ptr, const int64_t* row_idx, int64_t n, int32_t device, int64_t* out);
+
+/* solve (engine.py:585-589) on host buffers: copies b in, solves, copies x
+ * out. b and x are float64[n]. */
+int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* stats);
+
+/* Device-resident solve: d_b/d_x are device pointers on the plan's device,
+ * `stream` a cudaStream_t (0 = the plan's stream). Asynchronous. */
+int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x, void* stream);
+
+/* Wait for the plan's work and report the device status of the last solve
+ * (SPTRSV_E_TIMEOUT if the watchdog tripped). */
+int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats);
+
+int sptrsv_plan_destroy(sptrsv_plan* plan);
+
+/* Last error message of this thread (empty string when none). */
+const char* sptrsv_last_error(void);
+
+/* Number of visible CUDA devices (0 without a GPU; no CUDA context is kept). */
+int sptrsv_device_count(void);
+
+int sptrsv_abi_version(void);
+
+/* sizeof(sptrsv_options) / sizeof(sptrsv_stats) as compiled, so bindings can
+ * assert their struct mirrors. */
+int sptrsv_sizeof_options(void);
+int sptrsv_sizeof_stats(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPTRSV_B200_H */

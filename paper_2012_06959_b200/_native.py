@@ -1,0 +1,255 @@
+"""ctypes binding of the C ABI in ``include/sptrsv_b200.h``.
+
+This is the only module that talks to the CUDA library. There is no CPU
+fallback anywhere in the package: if ``libsptrsv_b200.so`` is missing or no
+CUDA device is visible, every compute entry point raises
+:class:`~paper_2012_06959_b200.errors.NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+import weakref
+from pathlib import Path
+
+import numpy as np
+
+from .errors import NativeUnavailable, raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "libsptrsv_b200.so"
+
+PRECISION = {"exact": 0, "fast": 1}
+EXECUTOR = {"auto": 0, "rows": 1, "chains": 2}
+EXECUTOR_NAME = {v: k for k, v in EXECUTOR.items()}
+PLAN_STRUCTURE_ONLY = 1
+
+
+class Options(C.Structure):
+    _fields_ = [
+        ("precision", C.c_int32),
+        ("executor", C.c_int32),
+        ("device", C.c_int32),
+        ("flags", C.c_int32),
+        ("timeout_s", C.c_double),
+        ("spin_initial", C.c_int32),
+        ("spin_max_ns", C.c_int32),
+        ("chain_lanes", C.c_int32),
+        ("reserved", C.c_int32 * 7),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("setup_ms", C.c_double),
+        ("solve_ms", C.c_double),
+        ("h2d_ms", C.c_double),
+        ("d2h_ms", C.c_double),
+        ("spins", C.c_int64),
+        ("remote_reads", C.c_int64),
+        ("launches", C.c_int64),
+        ("executor", C.c_int32),
+        ("n_levels", C.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_P64 = C.POINTER(C.c_int64)
+_PD = C.POINTER(C.c_double)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def library_path() -> Path:
+    return LIB_PATH
+
+
+def _bind(lib: C.CDLL) -> None:
+    lib.sptrsv_default_options.argtypes = [C.POINTER(Options)]
+    lib.sptrsv_default_options.restype = None
+    lib.sptrsv_plan_create.argtypes = [_P64, _P64, _PD, C.c_int64, C.POINTER(Options), C.POINTER(C.c_void_p), _P64]
+    lib.sptrsv_plan_create.restype = C.c_int
+    lib.sptrsv_plan_in_degrees.argtypes = [C.c_void_p, _P64]
+    lib.sptrsv_plan_in_degrees.restype = C.c_int
+    lib.sptrsv_plan_levels.argtypes = [C.c_void_p, _P64, _P64, _P64, _P64]
+    lib.sptrsv_plan_levels.restype = C.c_int
+    lib.sptrsv_in_degrees.argtypes = [_P64, _P64, C.c_int64, C.c_int32, _P64]
+    lib.sptrsv_in_degrees.restype = C.c_int
+    lib.sptrsv_solve.argtypes = [C.c_void_p, _PD, _PD, C.POINTER(Stats)]
+    lib.sptrsv_solve.restype = C.c_int
+    lib.sptrsv_solve_device_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.sptrsv_solve_device_async.restype = C.c_int
+    lib.sptrsv_synchronize.argtypes = [C.c_void_p, C.POINTER(Stats)]
+    lib.sptrsv_synchronize.restype = C.c_int
+    lib.sptrsv_plan_destroy.argtypes = [C.c_void_p]
+    lib.sptrsv_plan_destroy.restype = C.c_int
+    lib.sptrsv_last_error.argtypes = []
+    lib.sptrsv_last_error.restype = C.c_char_p
+    lib.sptrsv_device_count.argtypes = []
+    lib.sptrsv_device_count.restype = C.c_int
+    lib.sptrsv_abi_version.argtypes = []
+    lib.sptrsv_abi_version.restype = C.c_int
+
+
+def load_library() -> C.CDLL:
+    """Load (once) the in-tree CUDA library; raises if it is absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise NativeUnavailable(
+                    f"{LIB_PATH} is missing: run `python -m paper_2012_06959_b200.build` (there is no CPU fallback)"
+                )
+            lib = C.CDLL(str(LIB_PATH))
+            _bind(lib)
+            _lib = lib
+        return _lib
+
+
+def require_gpu() -> C.CDLL:
+    lib = load_library()
+    if lib.sptrsv_device_count() < 1:
+        raise NativeUnavailable("no CUDA device visible: this solver runs on the GPU only")
+    return lib
+
+
+def _err(lib) -> str:
+    msg = lib.sptrsv_last_error()
+    return msg.decode() if msg else ""
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def default_options() -> Options:
+    opt = Options()
+    load_library().sptrsv_default_options(C.byref(opt))
+    return opt
+
+
+class NativePlan:
+    """A device-resident plan for one matrix (C handle ``sptrsv_plan*``)."""
+
+    def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
+                 timeout=60.0, spin_initial=16, spin_max_ns=512, structure_only=False, chain_lanes=32):
+        lib = require_gpu()
+        self._lib = lib
+        self.n = int(n)
+        cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
+        ri = np.ascontiguousarray(row_idx, dtype=np.int64)
+        va = None if values is None else np.ascontiguousarray(values, dtype=np.float64)
+        opt = default_options()
+        opt.precision = PRECISION[precision]
+        opt.executor = EXECUTOR[executor]
+        opt.device = int(device)
+        opt.flags = PLAN_STRUCTURE_ONLY if structure_only else 0
+        opt.timeout_s = float(timeout)
+        opt.spin_initial = int(spin_initial)
+        opt.spin_max_ns = int(spin_max_ns)
+        opt.chain_lanes = int(chain_lanes)
+        handle = C.c_void_p()
+        bad = C.c_int64(-1)
+        rc = lib.sptrsv_plan_create(_ptr(cp, C.c_int64), _ptr(ri, C.c_int64),
+                                    None if va is None else _ptr(va, C.c_double), self.n, C.byref(opt),
+                                    C.byref(handle), C.byref(bad))
+        raise_for_status(rc, _err(lib), bad.value)
+        self._h = handle
+        self.precision = precision
+        self.device = int(device)
+        self._finalizer = weakref.finalize(self, lib.sptrsv_plan_destroy, handle)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def close(self) -> None:
+        self._finalizer()
+
+    def in_degrees(self) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.int64)
+        rc = self._lib.sptrsv_plan_in_degrees(self._h, _ptr(out, C.c_int64))
+        raise_for_status(rc, _err(self._lib))
+        return out
+
+    def levels(self) -> tuple[np.ndarray, np.ndarray, np.ndarray, int]:
+        n_levels = C.c_int64(0)
+        rc = self._lib.sptrsv_plan_levels(self._h, None, None, None, C.byref(n_levels))
+        raise_for_status(rc, _err(self._lib))
+        level_of = np.empty(self.n, dtype=np.int64)
+        order = np.empty(self.n, dtype=np.int64)
+        level_ptr = np.empty(n_levels.value + 1, dtype=np.int64)
+        rc = self._lib.sptrsv_plan_levels(self._h, _ptr(level_of, C.c_int64), _ptr(order, C.c_int64),
+                                          _ptr(level_ptr, C.c_int64), C.byref(n_levels))
+        raise_for_status(rc, _err(self._lib))
+        return level_of, order, level_ptr, int(n_levels.value)
+
+    def solve(self, b: np.ndarray, out: np.ndarray | None = None) -> tuple[np.ndarray, dict]:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = out if out is not None else np.empty(self.n, dtype=np.float64)
+        st = Stats()
+        rc = self._lib.sptrsv_solve(self._h, _ptr(b, C.c_double), _ptr(x, C.c_double), C.byref(st))
+        raise_for_status(rc, _err(self._lib))
+        d = st.as_dict()
+        d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
+        return x, d
+
+    def solve_device_async(self, d_b: int, d_x: int, stream: int = 0) -> None:
+        rc = self._lib.sptrsv_solve_device_async(self._h, C.c_void_p(d_b), C.c_void_p(d_x), C.c_void_p(stream))
+        raise_for_status(rc, _err(self._lib))
+
+    def synchronize(self) -> dict:
+        st = Stats()
+        rc = self._lib.sptrsv_synchronize(self._h, C.byref(st))
+        raise_for_status(rc, _err(self._lib))
+        d = st.as_dict()
+        d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
+        return d
+
+
+def in_degrees_raw(col_ptr, row_idx, n: int, device: int = 0) -> np.ndarray:
+    lib = require_gpu()
+    cp = np.ascontiguousarray(col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(row_idx, dtype=np.int64)
+    out = np.empty(n, dtype=np.int64)
+    rc = lib.sptrsv_in_degrees(_ptr(cp, C.c_int64), _ptr(ri, C.c_int64), n, device, _ptr(out, C.c_int64))
+    raise_for_status(rc, _err(lib))
+    return out
+
+
+# --- plan cache -------------------------------------------------------------
+# CscMatrix is immutable (frozen arrays), so a device plan stays valid for the
+# matrix object's lifetime; repeated solve() calls with the same L reuse it.
+_cache: dict[int, dict] = {}
+_cache_lock = threading.Lock()
+
+
+def _evict(ident: int) -> None:
+    with _cache_lock:
+        _cache.pop(ident, None)
+
+
+def plan_for(l, **kw) -> NativePlan:
+    """Device plan of matrix ``l`` (identity-keyed; dropped with the matrix)."""
+    key = tuple(sorted(kw.items()))
+    ident = id(l)
+    with _cache_lock:
+        per = _cache.get(ident)
+        if per is None:
+            per = {}
+            _cache[ident] = per
+            weakref.finalize(l, _evict, ident)
+        plan = per.get(key)
+    if plan is None:
+        plan = NativePlan(l.col_ptr, l.row_idx, None if kw.get("structure_only") else l.values, l.n, **kw)
+        with _cache_lock:
+            per[key] = plan
+    return plan
+
+
+def env_device() -> int:
+    return int(os.environ.get("SPTRSV_DEVICE", "0"))

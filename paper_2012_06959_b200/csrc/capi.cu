@@ -1,0 +1,391 @@
+// C ABI (include/sptrsv_b200.h): plan lifetime, preprocessing pipeline and the
+// solve entry points. Host-side runtime in C++; all compute is device kernels.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <chrono>
+#include <algorithm>
+#include "../../include/sptrsv_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "plan.hpp"
+
+using namespace sptrsv;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+}  // namespace
+
+namespace sptrsv {
+int plan_fail(int code, const char* msg) { return fail(code, msg); }
+}  // namespace sptrsv
+
+namespace {
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) return fail(SPTRSV_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+namespace sptrsv {
+
+void DevicePlan::release() {
+  cudaSetDevice(device);
+  void* ptrs[] = {rp, ci, cv, wv, dg, rdg, indeg, level, by_level, level_ptr, order, xbuf, bbuf, ticket, status,
+                  abort_flag, xseg_dev, lseg_dev};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  chains.release();
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+int DevicePlan::run_levels() {
+  // K6: level_i = 1 + max(level_j) over dependencies, 0 without any; the
+  // component pool in (max,+1) arithmetic over the natural (topological) order.
+  CUDA_TRY(cudaMemsetAsync(level, 0xFF, sizeof(int) * (size_t)n, stream));
+  CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(int), stream));
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(DeviceStatus), stream));
+  CUDA_TRY(cudaMemsetAsync(abort_flag, 0, sizeof(int), stream));
+  RowsArgs a{};
+  a.n = (int)n;
+  a.rp = rp;
+  a.ci = ci;
+  a.lseg = lseg_dev;
+  a.xseg = xseg_dev;
+  a.order = nullptr;
+  a.order_len = n;
+  a.ticket = ticket;
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.spin_initial = opt.spin_initial;
+  a.spin_max_ns = opt.spin_max_ns;
+  a.coop_long = 0;
+  a.long_deps = 1 << 30;
+  CUDA_TRY(launch_rows(kModeLevel, a, rows_grid(kModeLevel), stream));
+  DeviceStatus hs{};
+  CUDA_TRY(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  if (hs.code == SPTRSV_E_TIMEOUT) return fail(SPTRSV_E_TIMEOUT, "level analysis exceeded the timeout");
+
+  // group components by level: stable sort (level, row) -> ascending rows per level
+  int *iota = nullptr, *keys_out = nullptr, *cnt = nullptr, *tick = nullptr, *tb = nullptr;
+  CUDA_TRY(dalloc(&iota, n));
+  CUDA_TRY(dalloc(&keys_out, n));
+  CUDA_TRY(launch_iota(iota, (int)n, stream));
+  CUDA_TRY(sort_pairs_stable(level, keys_out, iota, by_level, n, (int)n, stream));
+  int last = 0;
+  if (n > 0) CUDA_TRY(cudaMemcpyAsync(&last, keys_out + n - 1, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  n_levels = n > 0 ? last + 1 : 0;
+  CUDA_TRY(dalloc(&level_ptr, n_levels + 1));
+  CUDA_TRY(dalloc(&cnt, n_levels + 1));
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (n_levels + 1), stream));
+  CUDA_TRY(launch_level_hist(level, (int)n, cnt, stream));
+  CUDA_TRY(scan_exclusive(cnt, level_ptr, n_levels + 1, stream));
+  // ticket layout for the component pool: single-level tickets when the
+  // padding costs < 2x, which enables warp-wide long rows
+  CUDA_TRY(dalloc(&tick, n_levels + 1));
+  CUDA_TRY(dalloc(&tb, n_levels + 1));
+  CUDA_TRY(cudaMemsetAsync(tick, 0, sizeof(int) * (n_levels + 1), stream));
+  CUDA_TRY(launch_tickets_per_level(cnt, n_levels, tick, stream));
+  CUDA_TRY(scan_exclusive(tick, tb, n_levels + 1, stream));
+  int total_tickets = 0;
+  CUDA_TRY(cudaMemcpyAsync(&total_tickets, tb + n_levels, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  long long padded = 32ll * total_tickets;
+  if (n > 0 && padded <= 2 * n) {
+    CUDA_TRY(dalloc(&order, padded));
+    CUDA_TRY(cudaMemsetAsync(order, 0xFF, sizeof(int) * padded, stream));
+    CUDA_TRY(launch_pad_order(by_level, level, level_ptr, tb, (int)n, order, stream));
+    order_len = padded;
+    coop_long = 1;
+  } else {
+    CUDA_TRY(dalloc(&order, n));
+    CUDA_TRY(cudaMemcpyAsync(order, by_level, sizeof(int) * n, cudaMemcpyDeviceToDevice, stream));
+    order_len = n;
+    coop_long = 0;
+  }
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  cudaFree(iota);
+  cudaFree(keys_out);
+  cudaFree(cnt);
+  cudaFree(tick);
+  cudaFree(tb);
+  return SPTRSV_OK;
+}
+
+int DevicePlan::rows_grid(int mode) const {
+  int per_sm = rows_blocks_per_sm(mode);
+  if (per_sm < 1) per_sm = 1;
+  long long want = (order_len + 255) / 256;
+  long long cap = (long long)num_sms * per_sm;
+  if (want < 1) want = 1;
+  return (int)std::min(want, cap);
+}
+
+int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
+  const int mode = opt.precision == SPTRSV_PRECISION_FAST ? kModeFast : kModeExact;
+  CUDA_TRY(cudaMemsetAsync(d_x, 0xFF, sizeof(double) * (size_t)n, s));
+  CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(int), s));
+  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s));
+  CUDA_TRY(cudaMemsetAsync(abort_flag, 0, sizeof(int), s));
+  unsigned long long* xs = reinterpret_cast<unsigned long long*>(d_x);
+  CUDA_TRY(cudaMemcpyAsync(xseg_dev, &xs, sizeof(xs), cudaMemcpyHostToDevice, s));
+  RowsArgs a{};
+  a.n = (int)n;
+  a.rp = rp;
+  a.ci = ci;
+  a.val = mode == kModeFast ? wv : cv;
+  a.dg = dg;
+  a.rdg = rdg;
+  a.b = d_b;
+  a.xseg = xseg_dev;
+  a.lseg = lseg_dev;
+  a.order = order;
+  a.order_len = order_len;
+  a.ticket = ticket;
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.spin_initial = opt.spin_initial;
+  a.spin_max_ns = opt.spin_max_ns;
+  a.coop_long = coop_long;
+  a.long_deps = 32;
+  CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
+  launches = 5;
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
+  if (structure_only) return fail(SPTRSV_E_ARGUMENT, "plan was created structure-only; it cannot solve");
+  int rc;
+  CUDA_TRY(cudaEventRecord(ev0, s));
+  if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
+  else rc = solve_rows(d_b, d_x, s);
+  if (rc != SPTRSV_OK) return rc;
+  CUDA_TRY(cudaEventRecord(ev1, s));
+  pending = true;
+  return SPTRSV_OK;
+}
+
+int DevicePlan::finish(sptrsv_stats* st) {
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  DeviceStatus hs{};
+  CUDA_TRY(cudaMemcpy(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  if (pending) CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+  pending = false;
+  last_solve_ms = ms;
+  if (st) {
+    st->setup_ms = setup_ms;
+    st->solve_ms = ms;
+    st->spins = (int64_t)hs.spins;
+    st->remote_reads = (int64_t)hs.remote_reads;
+    st->launches = launches;
+    st->executor = executor_used;
+    st->n_levels = n_levels;
+  }
+  if (hs.code == SPTRSV_E_TIMEOUT)
+    return fail(SPTRSV_E_TIMEOUT, "solve exceeded " + std::to_string(opt.timeout_s) + "s (device watchdog)");
+  return SPTRSV_OK;
+}
+
+}  // namespace sptrsv
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+void sptrsv_default_options(sptrsv_options* opt) {
+  std::memset(opt, 0, sizeof(*opt));
+  opt->precision = SPTRSV_PRECISION_EXACT;
+  opt->executor = SPTRSV_EXECUTOR_AUTO;
+  opt->device = 0;
+  opt->timeout_s = 60.0;
+  opt->spin_initial = 16;
+  opt->spin_max_ns = 512;
+  opt->chain_lanes = 32;
+}
+
+int sptrsv_abi_version(void) { return 1; }
+int sptrsv_sizeof_options(void) { return (int)sizeof(sptrsv_options); }
+int sptrsv_sizeof_stats(void) { return (int)sizeof(sptrsv_stats); }
+
+const char* sptrsv_last_error(void) { return g_err.c_str(); }
+
+int sptrsv_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return c;
+}
+
+int sptrsv_plan_create(const int64_t* col_ptr, const int64_t* row_idx, const double* values, int64_t n,
+                       const sptrsv_options* opt_in, sptrsv_plan** out, int64_t* bad_col) {
+  g_err.clear();
+  if (!out || !col_ptr || (n > 0 && !row_idx)) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (bad_col) *bad_col = -1;
+  sptrsv_options opt;
+  if (opt_in) opt = *opt_in;
+  else sptrsv_default_options(&opt);
+  if (opt.chain_lanes <= 0 || opt.chain_lanes > 32) opt.chain_lanes = 32;
+  const bool structure_only = (opt.flags & SPTRSV_PLAN_STRUCTURE_ONLY) != 0;
+  if (!structure_only && n > 0 && !values) return fail(SPTRSV_E_ARGUMENT, "values required");
+  if (n < 0) return fail(SPTRSV_E_STRUCTURE, "negative dimension");
+  const long long nnz = col_ptr[n];
+  if (col_ptr[0] != 0 || nnz < 0) return fail(SPTRSV_E_STRUCTURE, "malformed col_ptr");
+  if (n >= (1ll << 31) - 1 || nnz >= (1ll << 31) - 1)
+    return fail(SPTRSV_E_UNSUPPORTED, "n and nnz must be < 2^31 (int32 device indices)");
+  for (long long j = 0; j < n; ++j)
+    if (col_ptr[j + 1] < col_ptr[j]) return fail(SPTRSV_E_STRUCTURE, "col_ptr is not non-decreasing");
+
+  auto t0 = std::chrono::steady_clock::now();
+  auto* p = new DevicePlan();
+  p->opt = opt;
+  p->n = n;
+  p->nnz = nnz;
+  p->device = opt.device;
+  p->structure_only = structure_only;
+  int rc = p->build(col_ptr, row_idx, values, bad_col);
+  if (rc != SPTRSV_OK) {
+    std::string keep = g_err;
+    p->release();
+    delete p;
+    g_err = keep;
+    return rc;
+  }
+  p->setup_ms = ms_since(t0);
+  *out = reinterpret_cast<sptrsv_plan*>(p);
+  return SPTRSV_OK;
+}
+
+int sptrsv_plan_in_degrees(const sptrsv_plan* plan, int64_t* out) {
+  g_err.clear();
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p || !out) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  CUDA_TRY(cudaSetDevice(p->device));
+  long long* tmp = nullptr;
+  CUDA_TRY(dalloc(&tmp, p->n));
+  CUDA_TRY(launch_widen(p->indeg, tmp, p->n, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(out, tmp, sizeof(long long) * p->n, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  cudaFree(tmp);
+  return SPTRSV_OK;
+}
+
+int sptrsv_plan_levels(const sptrsv_plan* plan, int64_t* level_of, int64_t* order, int64_t* level_ptr,
+                       int64_t* n_levels) {
+  g_err.clear();
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p) return fail(SPTRSV_E_ARGUMENT, "null plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (n_levels) *n_levels = p->n_levels;
+  long long* tmp = nullptr;
+  CUDA_TRY(dalloc(&tmp, p->n + 1));
+  if (level_of) {
+    CUDA_TRY(launch_widen(p->level, tmp, p->n, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(level_of, tmp, sizeof(long long) * p->n, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+  }
+  if (order) {
+    CUDA_TRY(launch_widen(p->by_level, tmp, p->n, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(order, tmp, sizeof(long long) * p->n, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+  }
+  if (level_ptr) {
+    CUDA_TRY(launch_widen(p->level_ptr, tmp, p->n_levels + 1, p->stream));
+    CUDA_TRY(cudaMemcpyAsync(level_ptr, tmp, sizeof(long long) * (p->n_levels + 1), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+  }
+  cudaFree(tmp);
+  return SPTRSV_OK;
+}
+
+int sptrsv_in_degrees(const int64_t* col_ptr, const int64_t* row_idx, int64_t n, int32_t device, int64_t* out) {
+  sptrsv_options opt;
+  sptrsv_default_options(&opt);
+  opt.device = device;
+  opt.flags = SPTRSV_PLAN_STRUCTURE_ONLY | 2 /* in-degree only */;
+  sptrsv_plan* plan = nullptr;
+  int rc = sptrsv_plan_create(col_ptr, row_idx, nullptr, n, &opt, &plan, nullptr);
+  if (rc != SPTRSV_OK) return rc;
+  rc = sptrsv_plan_in_degrees(plan, out);
+  sptrsv_plan_destroy(plan);
+  return rc;
+}
+
+int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* stats) {
+  g_err.clear();
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || (p->n > 0 && (!b || !x))) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (p->n == 0) return p->finish(stats);
+  auto t0 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaMemcpyAsync(p->bbuf, b, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  double h2d = ms_since(t0);
+  int rc = p->solve_device(p->bbuf, p->xbuf, p->stream);
+  if (rc != SPTRSV_OK) return rc;
+  rc = p->finish(stats);
+  if (rc != SPTRSV_OK) return rc;
+  auto t1 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaMemcpyAsync(x, p->xbuf, sizeof(double) * p->n, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (stats) {
+    stats->h2d_ms = h2d;
+    stats->d2h_ms = ms_since(t1);
+  }
+  return SPTRSV_OK;
+}
+
+int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x, void* stream) {
+  g_err.clear();
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p) return fail(SPTRSV_E_ARGUMENT, "null plan");
+  if (p->n == 0) return SPTRSV_OK;
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = stream ? reinterpret_cast<cudaStream_t>(stream) : p->stream;
+  return p->solve_device(d_b, d_x, s);
+}
+
+int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats) {
+  g_err.clear();
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p) return fail(SPTRSV_E_ARGUMENT, "null plan");
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return p->finish(stats);
+}
+
+int sptrsv_plan_destroy(sptrsv_plan* plan) {
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p) return SPTRSV_OK;
+  p->release();
+  delete p;
+  return SPTRSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Device plan: everything resident in HBM for one matrix. One plan per
+// (matrix, device); reused by every solve of that matrix.
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/sptrsv_b200.h"
+#include "common.cuh"
+#include "chains.hpp"
+
+namespace sptrsv {
+
+struct DevicePlan {
+  sptrsv_options opt{};
+  long long n = 0, nnz = 0, noff = 0;
+  int device = 0;
+  int num_sms = 148;
+  bool structure_only = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // CSR of off-diagonals + diagonal (preprocess.cu)
+  int* rp = nullptr;
+  int* ci = nullptr;
+  double* cv = nullptr;
+  double* wv = nullptr;
+  double* dg = nullptr;
+  double* rdg = nullptr;
+  int* indeg = nullptr;
+
+  // level analysis (K6) and the component-pool ticket order
+  int* level = nullptr;
+  int* by_level = nullptr;
+  int* level_ptr = nullptr;
+  int n_levels = 0;
+  int* order = nullptr;
+  long long order_len = 0;
+  int coop_long = 0;
+
+  // solve scratch
+  double* xbuf = nullptr;
+  double* bbuf = nullptr;
+  int* ticket = nullptr;
+  DeviceStatus* status = nullptr;
+  int* abort_flag = nullptr;
+  unsigned long long** xseg_dev = nullptr;  // [1] for a single-PE plan
+  int** lseg_dev = nullptr;
+
+  ChainPlan chains;
+  int executor_used = SPTRSV_EXECUTOR_ROWS;
+
+  double setup_ms = 0.0;
+  double last_solve_ms = 0.0;
+  long long launches = 0;
+  bool pending = false;
+
+  int build(const int64_t* col_ptr, const int64_t* row_idx, const double* values, int64_t* bad_col);
+  int run_levels();
+  int rows_grid(int mode) const;
+  int solve_rows(const double* d_b, double* d_x, cudaStream_t s);
+  int solve_chains(const double* d_b, double* d_x, cudaStream_t s);
+  int build_chains();
+  bool chains_preferred() const;
+  int solve_device(const double* d_b, double* d_x, cudaStream_t s);
+  int finish(sptrsv_stats* st);
+  void release();
+};
+
+}  // namespace sptrsv

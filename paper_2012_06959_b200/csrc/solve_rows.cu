@@ -1,0 +1,318 @@
+// Sync-free component pool: the paper's warp-per-component solve (Alg. 3,
+// /root/reference/PAPER.md:339-399) restated for B200 as a pull kernel.
+//
+// * A persistent grid; each warp takes tickets of 32 consecutive slots of a
+//   topological order (`order`) from one atomic counter — the "malleable task
+//   pool". Tickets are handed out in ascending order, so the
+//   earliest unsolved component always belongs to a running warp: the
+//   reference's progress argument (engine.py:30-35) carries over.
+// * Thread-per-component for short rows: each lane gathers its row's x_j with
+//   relaxed 8-byte loads; a slot still equal to kNotReady means "not solved
+//   yet" and is re-polled (lock-wait, engine.py:497-521). Loads are issued four
+//   at a time so independent dependencies overlap.
+// * Rows with many dependencies are solved by the whole warp when tickets are
+//   single-level (coop_long): lanes poll disjoint chunks, and the partial sums
+//   are folded in ascending column order (exact mode) or by a shuffle tree (fast).
+// * Exact mode reproduces solve_serial bit for bit: left_sum accumulates
+//   v*x_j in ascending column order with separate IEEE mul/add, then
+//   x_i = (b_i - left_sum) / l_ii (reference.py:30-34).
+// * Level mode runs the same dataflow over (max, +1): level_i = 1 + max level_j,
+//   which is the reference's canonical earliest level (analysis.py:43-64).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sptrsv {
+
+namespace {
+
+struct Poller {
+  const RowsArgs& a;
+  unsigned long long spins = 0;
+  unsigned long long remote = 0;
+  unsigned long long deadline = 0;
+  __device__ explicit Poller(const RowsArgs& args) : a(args) {
+    if (a.timeout_ns) deadline = globaltimer_ns() + a.timeout_ns;
+  }
+
+  // Wait for one slot; returns false when the launch is being aborted.
+  __device__ __forceinline__ bool wait_u64(const unsigned long long* p, bool sys, unsigned long long& u) {
+    int polls = 0;
+    int sleep_ns = 32;
+    while (u == kNotReady) {
+      ++spins;
+      ++polls;
+      if (polls > a.spin_initial) {
+        if ((polls & 63) == 0) {
+          if (ld_relaxed_s32(a.abort_flag)) return false;
+          if (deadline && globaltimer_ns() > deadline) {
+            atomicExch(&a.status->code, 5);
+            atomicExch(a.abort_flag, 1);
+            return false;
+          }
+        }
+        __nanosleep(sleep_ns);
+        if (sleep_ns < a.spin_max_ns) sleep_ns <<= 1;
+      }
+      u = sys ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p);
+    }
+    return true;
+  }
+  __device__ __forceinline__ bool wait_s32(const int* p, int& v) {
+    int polls = 0;
+    int sleep_ns = 32;
+    while (v < 0) {
+      ++spins;
+      ++polls;
+      if (polls > a.spin_initial) {
+        if ((polls & 63) == 0) {
+          if (ld_relaxed_s32(a.abort_flag)) return false;
+          if (deadline && globaltimer_ns() > deadline) {
+            atomicExch(&a.status->code, 5);
+            atomicExch(a.abort_flag, 1);
+            return false;
+          }
+        }
+        __nanosleep(sleep_ns);
+        if (sleep_ns < a.spin_max_ns) sleep_ns <<= 1;
+      }
+      v = ld_relaxed_s32(p);
+    }
+    return true;
+  }
+};
+
+template <int MODE>
+struct Acc;
+
+template <>
+struct Acc<kModeExact> {
+  double s = 0.0;
+  __device__ void init(const RowsArgs&, int) { s = 0.0; }
+  __device__ void add(double v, double xj) { s = __dadd_rn(s, __dmul_rn(v, xj)); }
+  __device__ double finish(const RowsArgs& a, int i) const {
+    return div_exact(__dsub_rn(a.b[i], s), a.dg[i], a.rdg[i]);
+  }
+};
+
+template <>
+struct Acc<kModeFast> {
+  double s = 0.0;
+  __device__ void init(const RowsArgs& a, int i) { s = __dmul_rn(a.b[i], a.rdg[i]); }
+  __device__ void add(double w, double xj) { s = __fma_rn(w, xj, s); }
+  __device__ double finish(const RowsArgs&, int) const { return s; }
+};
+
+template <int MODE>
+__device__ __forceinline__ const unsigned long long* slot_u64(const RowsArgs& a, int j, bool& remote) {
+  if (a.owner == nullptr) {
+    remote = false;
+    return a.xseg[0] + j;
+  }
+  int p = a.owner[j];
+  remote = p != a.my_pe;
+  return a.xseg[p] + j;
+}
+
+__device__ __forceinline__ const int* slot_s32(const RowsArgs& a, int j, bool& remote) {
+  if (a.owner == nullptr) {
+    remote = false;
+    return a.lseg[0] + j;
+  }
+  int p = a.owner[j];
+  remote = p != a.my_pe;
+  return a.lseg[p] + j;
+}
+
+__device__ __forceinline__ void publish_u64(const RowsArgs& a, int i, double v) {
+  unsigned long long* p = a.xseg[a.owner ? a.my_pe : 0] + i;
+  if (a.owner) st_relaxed_sys_u64(p, publishable(v));
+  else st_relaxed_u64(p, publishable(v));
+}
+
+// One lane, one row, floating point.
+template <int MODE>
+__device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
+  Acc<MODE> acc;
+  acc.init(a, i);
+  int k = a.rp[i];
+  const int end = a.rp[i + 1];
+  const bool multi = a.owner != nullptr;
+  for (; k < end; k += 4) {
+    int j[4];
+    double v[4];
+    unsigned long long u[4];
+    const unsigned long long* p[4];
+    bool rem[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (k + q < end) {
+        j[q] = __ldg(a.ci + k + q);
+        v[q] = __ldg(a.val + k + q);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (k + q < end) {
+        p[q] = slot_u64<MODE>(a, j[q], rem[q]);
+        u[q] = rem[q] ? ld_relaxed_sys_u64(p[q]) : ld_relaxed_u64(p[q]);
+        if (multi && rem[q]) ++poll.remote;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (k + q < end) {
+        if (!poll.wait_u64(p[q], rem[q], u[q])) return false;
+        acc.add(v[q], as_f64(u[q]));
+      }
+    }
+  }
+  publish_u64(a, i, acc.finish(a, i));
+  return true;
+}
+
+__device__ bool level_row_thread(const RowsArgs& a, Poller& poll, int i) {
+  int lv = 0;
+  const int end = a.rp[i + 1];
+  for (int k = a.rp[i]; k < end; k += 4) {
+    int vals[4];
+    const int* p[4];
+    bool rem[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k + q < end) {
+        p[q] = slot_s32(a, __ldg(a.ci + k + q), rem[q]);
+        vals[q] = ld_relaxed_s32(p[q]);
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k + q < end) {
+        if (!poll.wait_s32(p[q], vals[q])) return false;
+        lv = max(lv, vals[q] + 1);
+      }
+  }
+  st_relaxed_s32(a.lseg[a.owner ? a.my_pe : 0] + i, lv);
+  return true;
+}
+
+// Whole warp, one long row. Exact mode keeps the ascending-column fold by
+// letting lane 0 add the 32 products of each chunk in order.
+template <int MODE>
+__device__ bool solve_row_warp(const RowsArgs& a, Poller& poll, int i, int lane) {
+  const int beg = a.rp[i], end = a.rp[i + 1];
+  double s = (MODE == kModeFast) ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
+  double part = 0.0;  // fast mode: per-lane partial
+  for (int base = beg; base < end; base += kWarp) {
+    int k = base + lane;
+    double prod = 0.0;
+    bool ok = true;
+    if (k < end) {
+      int j = __ldg(a.ci + k);
+      double v = __ldg(a.val + k);
+      bool rem;
+      const unsigned long long* p = slot_u64<MODE>(a, j, rem);
+      unsigned long long u = rem ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p);
+      if (rem) ++poll.remote;
+      ok = poll.wait_u64(p, rem, u);
+      if (MODE == kModeExact) prod = __dmul_rn(v, as_f64(u));
+      else part = __fma_rn(v, as_f64(u), part);
+    }
+    if (__any_sync(0xffffffffu, !ok)) return false;
+    if (MODE == kModeExact) {
+      int cnt = min(kWarp, end - base);
+      for (int q = 0; q < cnt; ++q) {
+        double pq = __shfl_sync(0xffffffffu, prod, q);
+        s = __dadd_rn(s, pq);
+      }
+    }
+  }
+  double xi;
+  if (MODE == kModeExact) {
+    xi = div_exact(__dsub_rn(a.b[i], s), a.dg[i], a.rdg[i]);
+  } else {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    xi = s + part;
+  }
+  if (lane == 0) publish_u64(a, i, xi);
+  return true;
+}
+
+__device__ bool level_row_warp(const RowsArgs& a, Poller& poll, int i, int lane) {
+  const int beg = a.rp[i], end = a.rp[i + 1];
+  int lv = 0;
+  for (int k = beg + lane; k < end; k += kWarp) {
+    bool rem;
+    const int* p = slot_s32(a, __ldg(a.ci + k), rem);
+    int v = ld_relaxed_s32(p);
+    if (!poll.wait_s32(p, v)) { lv = -1 << 30; break; }
+    lv = max(lv, v + 1);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, off));
+  if (lv < 0) return false;
+  if (lane == 0) st_relaxed_s32(a.lseg[a.owner ? a.my_pe : 0] + i, lv);
+  return true;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_rows(RowsArgs a) {
+  const int lane = threadIdx.x & 31;
+  Poller poll(a);
+  while (true) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    long long slot = (long long)t * kWarp + lane;
+    if ((long long)t * kWarp >= a.order_len) break;
+    int i = -1;
+    if (slot < a.order_len) i = a.order ? a.order[slot] : (int)slot;
+    bool is_long = false;
+    if (i >= 0 && a.coop_long) is_long = (a.rp[i + 1] - a.rp[i]) > a.long_deps;
+    bool ok = true;
+    if (i >= 0 && !is_long) {
+      if constexpr (MODE == kModeLevel) ok = level_row_thread(a, poll, i);
+      else ok = solve_row_thread<MODE>(a, poll, i);
+    }
+    unsigned longs = __ballot_sync(0xffffffffu, is_long);
+    while (longs && __all_sync(0xffffffffu, ok)) {
+      int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      int r = __shfl_sync(0xffffffffu, i, src);
+      bool wok;
+      if constexpr (MODE == kModeLevel) wok = level_row_warp(a, poll, r, lane);
+      else wok = solve_row_warp<MODE>(a, poll, r, lane);
+      ok = ok && wok;
+    }
+    if (!__all_sync(0xffffffffu, ok)) break;
+  }
+  // fold per-thread counters
+  unsigned long long sp = poll.spins, rm = poll.remote;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    sp += __shfl_xor_sync(0xffffffffu, sp, off);
+    rm += __shfl_xor_sync(0xffffffffu, rm, off);
+  }
+  if (lane == 0 && (sp | rm)) {
+    atomicAdd(&a.status->spins, sp);
+    atomicAdd(&a.status->remote_reads, rm);
+  }
+}
+
+}  // namespace
+
+int rows_blocks_per_sm(int mode) {
+  int nb = 0;
+  if (mode == kModeExact) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows<kModeExact>, 256, 0);
+  else if (mode == kModeFast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows<kModeFast>, 256, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rows<kModeLevel>, 256, 0);
+  return nb;
+}
+
+cudaError_t launch_rows(int mode, const RowsArgs& a, int blocks, cudaStream_t s) {
+  if (mode == kModeExact) k_rows<kModeExact><<<blocks, 256, 0, s>>>(a);
+  else if (mode == kModeFast) k_rows<kModeFast><<<blocks, 256, 0, s>>>(a);
+  else k_rows<kModeLevel><<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sptrsv

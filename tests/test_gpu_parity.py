@@ -1,0 +1,182 @@
+"""GPU parity: the CUDA path against the reference goldens and the C oracle.
+
+Bars (BASELINE.json north star): in-degrees and levels bit-exact; x bit-exact
+in ``precision="exact"`` (the serial oracle's arithmetic) and within max
+relative error 1e-12 in ``precision="fast"``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2012_06959_b200 as sp
+from paper_2012_06959_b200 import _native, synth
+from paper_2012_06959_b200.errors import (
+    DimensionMismatch,
+    MatrixStructureError,
+    MissingDiagonal,
+    SolveTimeout,
+    ZeroDiagonal,
+)
+from conftest import GOLDEN, REFERENCE_CASES, case_matrix
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-12
+EXECUTORS = ["rows", "chains"]
+
+
+def _solve(l, b, precision="exact", executor="auto", **kw):
+    plan = _native.plan_for(l, precision=precision, executor=executor, device=0, **kw)
+    x, st = plan.solve(b)
+    return x, st
+
+
+@pytest.mark.parametrize("name", sorted(REFERENCE_CASES))
+def test_in_degrees_and_levels_bit_exact(name):
+    c = REFERENCE_CASES[name]
+    l = case_matrix(c)
+    np.testing.assert_array_equal(sp.compute_in_degrees(l), c["in_degree"])
+    sched = sp.compute_level_schedule(l)
+    np.testing.assert_array_equal(sched.level_of, c["level_of"])
+    assert sched.n_levels == int(c["n_levels"])
+    # levels[k] lists the level-k components in ascending order (analysis.py:36-37)
+    for k, comps in enumerate(sched.levels):
+        assert comps == sorted(np.flatnonzero(c["level_of"] == k).tolist())
+
+
+@pytest.mark.parametrize("executor", EXECUTORS)
+@pytest.mark.parametrize("name", sorted(n for n in REFERENCE_CASES if "x" in REFERENCE_CASES[n]))
+def test_exact_solve_bitwise_equals_reference(name, executor):
+    c = REFERENCE_CASES[name]
+    l = case_matrix(c)
+    x, st = _solve(l, c["b"], "exact", executor)
+    assert x.tobytes() == c["x"].tobytes(), sp.compare_solutions(x, c["x"], 1e-300)
+
+
+@pytest.mark.parametrize("executor", EXECUTORS)
+@pytest.mark.parametrize("name", sorted(n for n in REFERENCE_CASES if "x" in REFERENCE_CASES[n]))
+def test_fast_solve_within_1e12(name, executor):
+    c = REFERENCE_CASES[name]
+    l = case_matrix(c)
+    x, _ = _solve(l, c["b"], "fast", executor)
+    cmp = sp.compare_solutions(x, c["x"], FAST_TOL)
+    assert cmp.within_tol, cmp
+
+
+def test_solve_serial_dropin_lap2d_256():
+    z = np.load(GOLDEN / "lap2d_256.npz")
+    l = synth.lap2d(256)
+    assert sp.solve_serial(l, np.ones(l.n)).tobytes() == z["x_ones"].tobytes()
+    assert sp.solve_serial(l, z["b_rand"]).tobytes() == z["x_rand"].tobytes()
+    np.testing.assert_array_equal(sp.compute_in_degrees(l), z["in_degree"])
+    sched = sp.compute_level_schedule(l)
+    np.testing.assert_array_equal(sched.level_of, z["level_of"])
+    assert sched.n_levels == 511
+
+
+MID_SIZE = {
+    "lap2d-128": lambda: synth.lap2d(128),
+    "lap3d-24": lambda: synth.lap3d(24),
+    "banded-20k": lambda: synth.banded(20_000, 64, 0.5, 3),
+    "rmat-14": lambda: synth.rmat(14, 8, 1),
+    "random-3000": lambda: synth.random_lower(3000, 0.01, 5, dominant=True),
+    "blockdiag-64": lambda: synth.block_diagonal(8192, 64, 2),
+}
+
+
+@pytest.mark.parametrize("executor", EXECUTORS)
+@pytest.mark.parametrize("name", sorted(MID_SIZE))
+def test_mid_size_against_c_oracle(name, executor):
+    l = MID_SIZE[name]()
+    rng = np.random.default_rng(7)
+    b = rng.uniform(-1.0, 1.0, size=l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    x, _ = _solve(l, b, "exact", executor)
+    assert x.tobytes() == ref.tobytes()
+    xf, _ = _solve(l, b, "fast", executor)
+    assert sp.compare_solutions(xf, ref, FAST_TOL).within_tol
+    lv, nl = oracle.levels(l.col_ptr, l.row_idx)
+    sched_lv, _, _, n_levels = _native.plan_for(l, structure_only=True, device=0).levels()
+    np.testing.assert_array_equal(sched_lv, lv)
+    assert n_levels == nl
+    np.testing.assert_array_equal(sp.compute_in_degrees(l), oracle.in_degrees(l.col_ptr, l.row_idx))
+
+
+def test_repeat_solves_reuse_plan_and_agree():
+    l = synth.lap2d(64)
+    plan = _native.plan_for(l, precision="exact", executor="auto", device=0)
+    first, _ = plan.solve(np.ones(l.n))
+    for seed in range(3):
+        b = np.random.default_rng(seed).uniform(-1, 1, l.n)
+        x, _ = plan.solve(b)
+        assert x.tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b).tobytes()
+    again, _ = plan.solve(np.ones(l.n))
+    assert again.tobytes() == first.tobytes()
+
+
+def test_edge_cases_tiny():
+    one = sp.CscMatrix(n=1, col_ptr=[0, 1], row_idx=[0], values=[-2.5])
+    assert sp.solve_serial(one, np.array([5.0]))[0] == -2.0
+    eye = synth.diagonal(33)
+    b = np.linspace(-1, 1, 33)
+    assert sp.solve_serial(eye, b).tobytes() == b.tobytes()
+    empty = sp.CscMatrix(n=0, col_ptr=[0], row_idx=[], values=[])
+    assert sp.solve_serial(empty, np.zeros(0)).shape == (0,)
+
+
+def test_special_values_propagate_like_ieee():
+    l = sp.CscMatrix.from_entries(4, {(0, 0): 1e-310, (1, 0): 1e300, (1, 1): 3.0, (2, 1): 1.0, (2, 2): 1e-300,
+                                      (3, 2): -1.0, (3, 3): 7.0})
+    for b in ([1e-300, 1.0, 2.0, 3.0], [0.0, -0.0, np.inf, 1.0], [np.nan, 1.0, 1.0, 1.0]):
+        b = np.array(b)
+        x = sp.solve_serial(l, b)
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        np.testing.assert_array_equal(np.isnan(x), np.isnan(ref))
+        ok = ~np.isnan(ref)
+        assert x[ok].tobytes() == ref[ok].tobytes()
+
+
+def test_errors_raised_before_solving():
+    zero = sp.CscMatrix.from_entries(2, {(0, 0): 0.0, (1, 1): 1.0})
+    with pytest.raises(ZeroDiagonal) as e:
+        sp.solve_serial(zero, np.ones(2))
+    assert e.value.col == 0
+    missing = sp.CscMatrix.from_entries(3, {(0, 0): 1.0, (2, 1): 1.0, (2, 2): 1.0})
+    with pytest.raises(MissingDiagonal) as e:
+        sp.solve_serial(missing, np.ones(3))
+    assert e.value.col == 1
+    upper = sp.CscMatrix.from_entries(2, {(0, 0): 1.0, (0, 1): 2.0, (1, 1): 1.0})
+    with pytest.raises(MatrixStructureError):
+        sp.solve_serial(upper, np.ones(2))
+    with pytest.raises(DimensionMismatch):
+        sp.solve_serial(synth.diagonal(4), np.ones(5))
+    # first violation by (col, kind): column 1 misses its diagonal before column 2's zero
+    mixed = sp.CscMatrix.from_entries(3, {(0, 0): 1.0, (2, 1): 1.0, (2, 2): 0.0})
+    with pytest.raises(MissingDiagonal):
+        sp.solve_serial(mixed, np.ones(3))
+
+
+def test_watchdog_raises_solve_timeout():
+    l = synth.bidiagonal(400_000)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor="rows",
+                              timeout=2e-4, spin_initial=1, spin_max_ns=64)
+    with pytest.raises(SolveTimeout):
+        plan.solve(np.ones(l.n))
+    plan.close()
+
+
+def test_device_resident_solve_matches_host_path():
+    torch = pytest.importorskip("torch")
+    l = synth.lap3d(20)
+    b = np.random.default_rng(3).uniform(-1, 1, l.n)
+    plan = _native.plan_for(l, precision="fast", executor="auto", device=0)
+    db = torch.from_numpy(b).cuda()
+    dx = torch.empty_like(db)
+    plan.solve_device_async(db.data_ptr(), dx.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    plan.synchronize()
+    torch.cuda.synchronize()
+    x_host, _ = plan.solve(b)
+    assert dx.cpu().numpy().tobytes() == x_host.tobytes()
