@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 SpTRSV on B200 — µs/solve and GFLOP/s (2·nnz/t), % of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config lap2d-4096]
+                    [--precision fast|exact] [--executor auto|rows|chains]
+    python bench.py --impl reference ...      # the reference's CPU path (oracle port)
+
+One JSON line on stdout (rank 0). A "step" is one solve of L x = b for the
+configured matrix with b = ones (the reference CLI default, cli.py:139-140).
+
+* ``value``: GFLOP/s = 2·nnz / t, t = mean device time per solve over K
+  back-to-back solves with b and x resident in HBM (CUDA events, barrier +
+  synchronize on both sides, max over ranks).
+* ``e2e``: the same metric through the C-ABI host-buffer call
+  (``sptrsv_solve``: pinned b -> device, solve, device -> pinned x), wall clock.
+* ``roofline``: the solve kernel's algorithmic bytes (SURVEY.md §8d:
+  12·nnz + 4·(n+1) + 16·n) over its CUDA-event duration, against the measured
+  HBM copy bandwidth in MEASURED_PEAKS.json.
+* ``cpu_baseline``: the C port of the reference ``solve_serial`` (oracle/)
+  on one host core, full matrix.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpTRSV µs/solve and GFLOP/s (2·nnz/t) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "GFLOP/s"
+
+
+def algorithmic_bytes(n: int, nnz: int) -> int:
+    """int32 indices/pointers, f64 values, b and x."""
+    return 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n
+
+
+def measured_peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5,
+                ).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": reasons,
+            "samples": len(self.rows),
+        }
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_arm(args, l, b) -> dict:
+    """The reference's CPU solve (C port of solve_serial, reference.py:20-35), 1 core."""
+    import oracle
+
+    t_all = []
+    deadline = time.perf_counter() + max(10.0, 3.0 * args.steps)
+    reps = 0
+    x = None
+    for _ in range(args.warmup):
+        oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    while reps < args.steps or (time.perf_counter() < deadline and reps < 1):
+        t0 = time.perf_counter()
+        x = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        t_all.append(time.perf_counter() - t0)
+        reps += 1
+        if time.perf_counter() > deadline:
+            break
+    t = statistics.mean(t_all)
+    return {"seconds": t, "reps": reps, "x": x}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="lap2d-4096")
+    ap.add_argument("--precision", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--executor", choices=["auto", "rows", "chains"], default="auto")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    ws, rank, local = dist_env()
+    from paper_2012_06959_b200 import synth
+
+    t0 = time.perf_counter()
+    l = synth.config_matrix(args.config)
+    gen_s = time.perf_counter() - t0
+    n, nnz = l.n, l.nnz
+    flops = 2.0 * nnz
+    b = np.ones(n)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference_arm(args, l, b)
+        gflops = flops / r["seconds"] / 1e9
+        line = {
+            "metric": METRIC, "value": gflops, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": r["reps"], "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n": n, "nnz": nnz, "rhs": "ones"},
+            "cpu_baseline": {"value": gflops, "unit": UNIT, "cores": 1, "kind": "port",
+                             "sample": f"full {args.config} solve_serial (C port, -ffp-contract=off) x{r['reps']}"},
+            "e2e": {"value": gflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)
+    dev = local
+    torch.cuda.set_device(dev)
+    from paper_2012_06959_b200 import _native
+
+    ts = time.perf_counter()
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, n, precision=args.precision,
+                              executor=args.executor, device=dev)
+    setup_s = time.perf_counter() - ts
+    info = plan.info()
+
+    # ---- device-resident timing -------------------------------------------
+    db = torch.from_numpy(b).to(f"cuda:{dev}")
+    dx = torch.empty_like(db)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    for _ in range(args.warmup):
+        plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
+    plan.synchronize()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    kernel_ms = []
+    with ClockSampler(dev) as clocks:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        total_ms = e0.elapsed_time(e1)
+        # per-launch kernel durations (same stream, events around the kernel)
+        for _ in range(min(args.steps, 10)):
+            plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
+            st = plan.synchronize()
+            kernel_ms.append(st["kernel_ms"])
+    ms = total_ms / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    x_dev = dx.cpu().numpy()
+
+    # ---- end-to-end through the C ABI host-buffer call --------------------
+    hb = torch.from_numpy(b).pin_memory()
+    hx = torch.empty(n, dtype=torch.float64).pin_memory()
+    hb_np, hx_np = hb.numpy(), hx.numpy()
+    plan.solve(hb_np, out=hx_np)
+    t_e2e = []
+    for _ in range(args.e2e_steps):
+        t1 = time.perf_counter()
+        plan.solve(hb_np, out=hx_np)
+        t_e2e.append(time.perf_counter() - t1)
+    e2e_s = statistics.mean(t_e2e)
+    assert hx_np.tobytes() == x_dev.tobytes()
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---- correctness against the C oracle -----------------------------------
+    import oracle
+    from paper_2012_06959_b200 import compare_solutions, residual_norm, residual_norm_2
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_reference_arm(argparse.Namespace(steps=1, warmup=0), l, b)
+        x_ref = cpu["x"]
+    else:
+        x_ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    cmp = compare_solutions(x_dev, x_ref, 1e-12)
+    res_inf = residual_norm(l, x_dev, b)[1]
+    res_2 = residual_norm_2(l, x_dev, b)
+
+    kern = statistics.mean(kernel_ms) if kernel_ms else ms
+    peak, peak_kind = measured_peaks()
+    alg = algorithmic_bytes(n, nnz)
+    achieved = alg / (kern * 1e-3) / 1e9
+    traffic = None
+    tr = ROOT / "profiles" / "traffic.json"
+    if tr.exists():
+        try:
+            traffic = json.loads(tr.read_text()).get(f"{args.config}/{args.precision}/{info['executor']}")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": flops / (ms * 1e-3) / 1e9,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "us_per_solve": ms * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {
+            "workload": args.config,
+            "n": n,
+            "nnz": nnz,
+            "n_levels": info["n_levels"],
+            "rhs": "ones",
+            "precision": args.precision,
+            "executor": info["executor"],
+            "parallelism": f"column-block x{ws}" if ws > 1 else "single GPU",
+            "l2": f"no flush: solve inputs {alg / 1e6:.0f} MB vs 126 MB L2" if alg > 256e6
+            else "inputs fit L2 (warm-L2 figure)",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": traffic,
+            "peak_kind": peak_kind,
+            "algorithmic_bytes": alg,
+            "kernel_ms": kern,
+        },
+        "e2e": {
+            "value": flops / e2e_s / 1e9,
+            "unit": UNIT,
+            "h2d_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": 8 * n,
+            "ms_per_step": e2e_s * 1e3,
+            "path": "sptrsv_solve (C ABI, pinned host b/x)",
+        },
+        "cpu_baseline": None if cpu is None else {
+            "value": flops / cpu["seconds"] / 1e9,
+            "unit": UNIT,
+            "cores": 1,
+            "kind": "port",
+            "sample": f"full {args.config} solve_serial (C port of reference.py:20-35), 1 rep",
+            "seconds": cpu["seconds"],
+        },
+        "gpu_launches": args.steps,
+        "clocks": clocks.summary(),
+        "correctness": {
+            "max_rel_err_vs_oracle": cmp.max_rel_error,
+            "bitwise_equal_oracle": bool(x_dev.tobytes() == x_ref.tobytes()),
+            "residual_inf_rel": res_inf,
+            "residual_2_rel": res_2,
+        },
+        "setup_ms": setup_s * 1e3,
+        "plan": {k: info[k] for k in ("chain_tasks", "chain_slices", "chain_stream_bytes", "chain_mailboxes",
+                                     "chain_max_width", "deps_total", "deps_register", "deps_ring",
+                                     "deps_mailbox", "chain_max_task_steps", "schedule_ms")},
+        "generate_s": gen_s,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

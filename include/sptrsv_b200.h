@@ -68,6 +68,7 @@ typedef struct sptrsv_stats {
   double setup_ms;        /* plan creation (upload, K1, transpose, levels, schedule) */
   double solve_ms;        /* device time of the last solve (CUDA events) */
   double h2d_ms, d2h_ms;  /* host<->device copies of the last host-buffer solve */
+  double kernel_ms;       /* the solve kernel alone (CUDA events around its launch) */
   int64_t spins;          /* polls that found a dependency unsolved (lock_wait_spins) */
   int64_t remote_reads;   /* dependency loads from another PE's segment */
   int64_t launches;       /* kernels launched by the last solve */
@@ -75,7 +76,25 @@ typedef struct sptrsv_stats {
   int32_t n_levels;
 } sptrsv_stats;
 
+typedef struct sptrsv_plan_info {
+  int64_t n, nnz, n_offdiag;
+  int32_t n_levels;
+  int32_t executor;            /* executor the plan will run */
+  double setup_ms;
+  /* lane-chain schedule (valid when chains_ready) */
+  int32_t chains_ready;
+  int32_t chain_tasks;
+  int64_t chain_slices, chain_stream_bytes, chain_mailboxes;
+  int32_t chain_max_width, chain_lanes;
+  int64_t deps_total, deps_in_task, deps_register, deps_ring, deps_mailbox;
+  int64_t chain_max_task_steps;
+  double schedule_ms;
+} sptrsv_plan_info;
+
 typedef struct sptrsv_plan sptrsv_plan;
+
+/* Plan statistics (sizes, executor, schedule shape) for reports. */
+int sptrsv_plan_get_info(const sptrsv_plan* plan, sptrsv_plan_info* info);
 
 /* Fill defaults (exact, auto, device 0, 60 s, Backoff(16, 512)). */
 void sptrsv_default_options(sptrsv_options* opt);

@@ -46,6 +46,7 @@ class Stats(C.Structure):
         ("solve_ms", C.c_double),
         ("h2d_ms", C.c_double),
         ("d2h_ms", C.c_double),
+        ("kernel_ms", C.c_double),
         ("spins", C.c_int64),
         ("remote_reads", C.c_int64),
         ("launches", C.c_int64),
@@ -55,6 +56,36 @@ class Stats(C.Structure):
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("nnz", C.c_int64),
+        ("n_offdiag", C.c_int64),
+        ("n_levels", C.c_int32),
+        ("executor", C.c_int32),
+        ("setup_ms", C.c_double),
+        ("chains_ready", C.c_int32),
+        ("chain_tasks", C.c_int32),
+        ("chain_slices", C.c_int64),
+        ("chain_stream_bytes", C.c_int64),
+        ("chain_mailboxes", C.c_int64),
+        ("chain_max_width", C.c_int32),
+        ("chain_lanes", C.c_int32),
+        ("deps_total", C.c_int64),
+        ("deps_in_task", C.c_int64),
+        ("deps_register", C.c_int64),
+        ("deps_ring", C.c_int64),
+        ("deps_mailbox", C.c_int64),
+        ("chain_max_task_steps", C.c_int64),
+        ("schedule_ms", C.c_double),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {name: getattr(self, name) for name, _ in self._fields_}
+        d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
+        return d
 
 
 _P64 = C.POINTER(C.c_int64)
@@ -93,6 +124,8 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_device_count.restype = C.c_int
     lib.sptrsv_abi_version.argtypes = []
     lib.sptrsv_abi_version.restype = C.c_int
+    lib.sptrsv_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
+    lib.sptrsv_plan_get_info.restype = C.c_int
 
 
 def load_library() -> C.CDLL:
@@ -169,6 +202,12 @@ class NativePlan:
 
     def close(self) -> None:
         self._finalizer()
+
+    def info(self) -> dict:
+        inf = PlanInfo()
+        rc = self._lib.sptrsv_plan_get_info(self._h, C.byref(inf))
+        raise_for_status(rc, _err(self._lib))
+        return inf.as_dict()
 
     def in_degrees(self) -> np.ndarray:
         out = np.empty(self.n, dtype=np.int64)

@@ -55,6 +55,8 @@ void DevicePlan::release() {
   chains.release();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
+  if (evk0) cudaEventDestroy(evk0);
+  if (evk1) cudaEventDestroy(evk1);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -76,7 +78,7 @@ int DevicePlan::run_levels() {
   a.ticket = ticket;
   a.status = status;
   a.abort_flag = abort_flag;
-  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.timeout_ns = (unsigned long long)(std::max(opt.timeout_s, 600.0) * 1e9);  // analysis is not under the solve watchdog
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = 0;
@@ -171,8 +173,10 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = coop_long;
   a.long_deps = 32;
+  CUDA_TRY(cudaEventRecord(evk0, s));
   CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
-  launches = 5;
+  CUDA_TRY(cudaEventRecord(evk1, s));
+  launches = 1;
   return SPTRSV_OK;
 }
 
@@ -192,13 +196,17 @@ int DevicePlan::finish(sptrsv_stats* st) {
   CUDA_TRY(cudaStreamSynchronize(stream));
   DeviceStatus hs{};
   CUDA_TRY(cudaMemcpy(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost));
-  float ms = 0.f;
-  if (pending) CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+  float ms = 0.f, kms = 0.f;
+  if (pending) {
+    CUDA_TRY(cudaEventElapsedTime(&ms, ev0, ev1));
+    CUDA_TRY(cudaEventElapsedTime(&kms, evk0, evk1));
+  }
   pending = false;
   last_solve_ms = ms;
   if (st) {
     st->setup_ms = setup_ms;
     st->solve_ms = ms;
+    st->kernel_ms = kms;
     st->spins = (int64_t)hs.spins;
     st->remote_reads = (int64_t)hs.remote_reads;
     st->launches = launches;
@@ -378,6 +386,35 @@ int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats) {
   CUDA_TRY(cudaSetDevice(p->device));
   CUDA_TRY(cudaDeviceSynchronize());
   return p->finish(stats);
+}
+
+int sptrsv_plan_get_info(const sptrsv_plan* plan, sptrsv_plan_info* info) {
+  g_err.clear();
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p || !info) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  info->n = p->n;
+  info->nnz = p->nnz;
+  info->n_offdiag = p->noff;
+  info->n_levels = p->n_levels;
+  info->executor = p->executor_used;
+  info->setup_ms = p->setup_ms;
+  const ChainPlan& c = p->chains;
+  info->chains_ready = c.ready ? 1 : 0;
+  info->chain_tasks = c.n_tasks;
+  info->chain_slices = c.n_slices;
+  info->chain_stream_bytes = c.stream_bytes;
+  info->chain_mailboxes = c.n_mbox;
+  info->chain_max_width = c.max_width;
+  info->chain_lanes = c.lanes;
+  info->deps_total = c.deps_total;
+  info->deps_in_task = c.deps_in_task;
+  info->deps_register = c.deps_reg;
+  info->deps_ring = c.deps_ring;
+  info->deps_mailbox = c.deps_mbox;
+  info->chain_max_task_steps = c.max_task_steps;
+  info->schedule_ms = c.schedule_ms;
+  return SPTRSV_OK;
 }
 
 int sptrsv_plan_destroy(sptrsv_plan* plan) {

@@ -28,6 +28,8 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   P_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   P_TRY(cudaEventCreate(&ev0));
   P_TRY(cudaEventCreate(&ev1));
+  P_TRY(cudaEventCreate(&evk0));
+  P_TRY(cudaEventCreate(&evk1));
   const bool indeg_only = (opt.flags & 2) != 0;
 
   long long *d_cp = nullptr, *d_ri64 = nullptr;

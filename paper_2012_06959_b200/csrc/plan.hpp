@@ -17,7 +17,8 @@ struct DevicePlan {
   int num_sms = 148;
   bool structure_only = false;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;    // whole solve (resets + kernel)
+  cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // the solve kernel alone
 
   // CSR of off-diagonals + diagonal (preprocess.cu)
   int* rp = nullptr;
