@@ -194,7 +194,9 @@ def main():
     # ---- device-resident timing -------------------------------------------
     db = torch.from_numpy(b).to(f"cuda:{dev}")
     dx = torch.empty_like(db)
-    stream = torch.cuda.current_stream(dev)
+    torch.cuda.synchronize(dev)
+    # a dedicated (non-default) stream: the solves and the timing events share it
+    stream = torch.cuda.Stream(dev)
     sh = stream.cuda_stream
     for _ in range(args.warmup):
         plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)

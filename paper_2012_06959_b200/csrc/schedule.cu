@@ -6,11 +6,14 @@
 //    otherwise it opens a new chain = a new lane. A task closes when it
 //    would need more lanes than a warp has, or reaches max_rows.
 // 2. Steps: ASAP lockstep list schedule, step(i) = max(step(prev in lane) + 1,
-//    step(j) + 1 over in-task deps j).
+//    step(j) + 1 over in-task deps j). Every task starts with kPrefetch empty
+//    steps whose only job is to launch the first prefetches.
 // 3. Sources: a dependency is read from a register (chain predecessor), the
-//    smem ring (same task, < kRingSteps steps old) or a mailbox (older, or
-//    produced by an earlier task). Mailboxes are value-is-flag slots.
-// 4. Emit slices (one per task step) packed into <= kChunkBytes chunks.
+//    smem ring (same task, < kRingSteps steps old), the inbox (a value of an
+//    earlier task prefetched kPrefetch steps ahead; first kMaxInbox per row)
+//    or a direct mailbox poll (anything else). Mailboxes are value-is-flag.
+// 4. Emit slices (one per step) packed into <= kChunkBytes chunks; rows with
+//    more than kInlineDeps dependencies continue in an overflow list.
 //
 // Deadlock freedom: tasks are dealt in ascending order by a ticket counter and
 // only wait on earlier tasks (mailboxes of rows < a) or on earlier steps of
@@ -44,34 +47,45 @@ struct ScheduleOutput {
   std::vector<long long> chunk_off;
   std::vector<int> chunk_steps;
   std::vector<int> task_chunk;
+  std::vector<int> ovf_src;
+  std::vector<double> ovf_val;
   long long n_mbox = 0;
   int max_width = 0;
-  long long deps_total = 0, deps_in_task = 0, deps_ring = 0, deps_reg = 0, deps_mbox = 0;
+  int n_inbox = 0;
+  long long deps_total = 0, deps_in_task = 0, deps_ring = 0, deps_reg = 0, deps_mbox = 0, deps_inbox = 0;
   long long n_slices = 0, max_task_steps = 0;
   bool ok = true;
 };
+
+// Dependency d of a row with nd dependencies is stored inline in its slice
+// (else in the overflow list, whose mailbox reads are always direct polls).
+static inline bool inline_dep(int d, int nd) { return nd <= kInlineDeps || d < kInlineDeps - 1; }
 
 static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
   const int n = in.n;
   const int* rp = in.rp;
   const int* ci = in.ci;
   const int L = in.lanes;
+  const int P = kPrefetch;
   std::vector<int> lane_of(n), step_of(n), task_start;
   task_start.reserve(1024);
 
-  // pass 1: tasks, lanes, steps
+  // pass 1: tasks, lanes, steps (steps start at P: the first P are prefetch-only)
   {
     int a = 0, nl = 0;
     int tail[32], last_step[32];
-    for (int q = 0; q < 32; ++q) tail[q] = -1, last_step[q] = -1;
+    auto reset = [&]() {
+      nl = 0;
+      for (int q = 0; q < 32; ++q) tail[q] = -1, last_step[q] = P - 1;
+    };
+    reset();
     task_start.push_back(0);
     int i = 0;
     while (i < n) {
       const int lo = rp[i], hi = rp[i + 1];
       if (i - a >= in.max_rows) {
         a = i;
-        nl = 0;
-        for (int q = 0; q < 32; ++q) tail[q] = -1, last_step[q] = -1;
+        reset();
         task_start.push_back(a);
       }
       int p = (hi > lo && ci[hi - 1] >= a) ? ci[hi - 1] : -1;
@@ -79,10 +93,9 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       if (p >= 0 && tail[lane_of[p]] == p) {
         lane = lane_of[p];
       } else {
-        if (nl == L) {  // needs a 33rd chain: close the task before row i
+        if (nl == L) {  // needs one chain more than a warp has: close the task before row i
           a = i;
-          nl = 0;
-          for (int q = 0; q < 32; ++q) tail[q] = -1, last_step[q] = -1;
+          reset();
           task_start.push_back(a);
           continue;
         }
@@ -103,8 +116,10 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
   }
   const int n_tasks = (int)task_start.size() - 1;
 
-  // pass 2: classify dependencies, assign mailboxes to rows read from one
+  // pass 2: classify dependencies; mailboxes for rows read across tasks or
+  // from too far back in the same task; inbox width of the plan
   std::vector<int> mbox_of(n, -1);
+  int max_inbox = 0;
   {
     std::vector<int> prev_in_lane(32);
     for (int t = 0; t < n_tasks; ++t) {
@@ -112,11 +127,13 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       std::fill(prev_in_lane.begin(), prev_in_lane.end(), -1);
       for (int i = a; i < b; ++i) {
         const int li = lane_of[i];
+        int inbox = 0;
         for (int k = rp[i]; k < rp[i + 1]; ++k) {
           const int j = ci[k];
           ++out.deps_total;
           if (j < a) {
             ++out.deps_mbox;
+            if (inbox < kMaxInbox && inline_dep(k - rp[i], rp[i + 1] - rp[i])) ++inbox;
             if (mbox_of[j] < 0) mbox_of[j] = (int)out.n_mbox++;
             continue;
           }
@@ -130,10 +147,13 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
             if (mbox_of[j] < 0) mbox_of[j] = (int)out.n_mbox++;
           }
         }
+        max_inbox = std::max(max_inbox, inbox);
         prev_in_lane[li] = i;
       }
     }
   }
+  const int M = max_inbox;
+  out.n_inbox = M;
 
   // pass 3: emit slices and chunks
   out.task_chunk.reserve(n_tasks + 1);
@@ -141,7 +161,7 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
   std::vector<int> count, first, rows_by_step;
   std::vector<int> prev_in_lane(32);
   auto& st = out.stream;
-  st.reserve((size_t)n * 48 + (size_t)rp[n] * 12 + 4096);
+  st.reserve((size_t)n * 52 + (size_t)rp[n] * 12 + 4096);
   for (int t = 0; t < n_tasks; ++t) {
     const int a = task_start[t], b = task_start[t + 1];
     out.task_chunk.push_back((int)out.chunk_steps.size());
@@ -153,25 +173,25 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
     for (int s = 0; s < nsteps; ++s) count[s + 1] += count[s];
     first = count;
     rows_by_step.assign(b - a, 0);
-    for (int i = a; i < b; ++i) rows_by_step[first[step_of[i]]++] = i;  // ascending rows per step
+    for (int i = a; i < b; ++i) rows_by_step[first[step_of[i]]++] = i;
+    auto rows_at = [&](int s, int* row) {
+      for (int q = 0; q < 32; ++q) row[q] = -1;
+      if (s >= nsteps) return;
+      for (int r = count[s]; r < count[s + 1]; ++r) row[lane_of[rows_by_step[r]]] = rows_by_step[r];
+    };
     std::fill(prev_in_lane.begin(), prev_in_lane.end(), -1);
     size_t chunk_begin = st.size();
     int chunk_steps = 0;
+    int row[32], pf[32];
     for (int s = 0; s < nsteps; ++s) {
-      int row[32], width = 0;
-      for (int q = 0; q < 32; ++q) row[q] = -1;
-      for (int r = count[s]; r < count[s + 1]; ++r) {
-        const int i = rows_by_step[r];
-        row[lane_of[i]] = i;
-        width = std::max(width, rp[i + 1] - rp[i]);
-      }
+      rows_at(s, row);
+      rows_at(s + P, pf);
+      int width = 0;
+      for (int q = 0; q < 32; ++q)
+        if (row[q] >= 0) width = std::max(width, std::min(rp[row[q] + 1] - rp[row[q]], kInlineDeps));
       out.max_width = std::max(out.max_width, width);
-      const int bytes = slice_bytes(width, in.exact);
-      if (bytes > kChunkBytes) {
-        out.ok = false;
-        return;
-      }
-      if ((st.size() - chunk_begin) + bytes > (size_t)kChunkBytes || chunk_steps == kMaxChunkSteps) {
+      const int bytes = slice_bytes(width, M, in.exact);
+      if ((st.size() - chunk_begin) + bytes > (size_t)kChunkBytes) {
         out.chunk_steps.push_back(chunk_steps);
         out.chunk_off.push_back((long long)st.size());
         chunk_begin = st.size();
@@ -183,6 +203,7 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       std::memset(p, 0, bytes);
       int32_t* hdr = reinterpret_cast<int32_t*>(p);
       hdr[0] = width;
+      hdr[1] = M;
       int32_t* srow = reinterpret_cast<int32_t*>(p + 16);
       int32_t* smbo = reinterpret_cast<int32_t*>(p + 144);
       double* srdg = reinterpret_cast<double*>(p + 272);
@@ -190,7 +211,20 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       const size_t deps_off = 528 + (in.exact ? 256 : 0);
       int32_t* ssrc = reinterpret_cast<int32_t*>(p + deps_off);
       double* sval = reinterpret_cast<double*>(p + deps_off + 128 * (size_t)width);
+      int32_t* spf = reinterpret_cast<int32_t*>(p + deps_off + 384 * (size_t)width);
+      int32_t* spfm = spf + 32;
       for (int q = 0; q < 32; ++q) {
+        // prefetch fields for step s + P
+        const int f = pf[q];
+        spf[q] = f;
+        int m = 0;
+        if (f >= 0) {
+          const int fnd = rp[f + 1] - rp[f];
+          for (int k = rp[f]; k < rp[f + 1] && m < M; ++k)
+            if (ci[k] < a && inline_dep(k - rp[f], fnd)) spfm[m++ * 32 + q] = mbox_of[ci[k]];
+        }
+        for (; m < M; ++m) spfm[m * 32 + q] = -1;
+
         const int i = row[q];
         srow[q] = i;
         for (int d = 0; d < width; ++d) ssrc[d * 32 + q] = kSrcSkip;
@@ -201,16 +235,43 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
         smbo[q] = mbox_of[i];
         srdg[q] = in.rdg ? in.rdg[i] : 0.0;
         if (in.exact) sdg[q] = in.dg ? in.dg[i] : 0.0;
-        int d = 0;
-        for (int k = rp[i]; k < rp[i + 1]; ++k, ++d) {
+        const int nd = rp[i + 1] - rp[i];
+        const bool spill = nd > kInlineDeps;
+        int inbox = 0;
+        for (int d = 0; d < nd; ++d) {
+          const int k = rp[i] + d;
           const int j = ci[k];
           int code;
-          if (j < a) code = -2 - mbox_of[j];
-          else if (j == prev_in_lane[q]) code = kSrcPrev;
-          else if (s - step_of[j] < kRingSteps) code = lane_of[j] * kRingSteps + (step_of[j] % kRingSteps);
-          else code = -2 - mbox_of[j];
-          ssrc[d * 32 + q] = code;
-          sval[d * 32 + q] = in.val ? in.val[k] : 0.0;
+          if (j < a) {
+            if (inline_dep(d, nd) && inbox < M) {
+              code = kSrcInbox0 - inbox;
+              ++inbox;
+              ++out.deps_inbox;
+            } else {
+              code = kSrcDirect - mbox_of[j];
+            }
+          } else if (j == prev_in_lane[q]) {
+            code = kSrcPrev;
+          } else if (s - step_of[j] < kRingSteps) {
+            code = lane_of[j] * kRingSteps + (step_of[j] % kRingSteps);
+          } else {
+            code = kSrcDirect - mbox_of[j];
+          }
+          if (spill && d >= kInlineDeps - 1) {
+            if (d == kInlineDeps - 1) {
+              // slot kInlineDeps-1 points at the overflow list holding deps d..nd-1
+              const long long start = (long long)out.ovf_src.size();
+              const long long cnt = nd - d;
+              ssrc[d * 32 + q] = kSrcOverflow;
+              const long long packed = (start << 24) | cnt;
+              std::memcpy(&sval[d * 32 + q], &packed, 8);
+            }
+            out.ovf_src.push_back(code);
+            out.ovf_val.push_back(in.val ? in.val[k] : 0.0);
+          } else {
+            ssrc[d * 32 + q] = code;
+            sval[d * 32 + q] = in.val ? in.val[k] : 0.0;
+          }
         }
         prev_in_lane[q] = i;
       }
@@ -247,11 +308,13 @@ int DevicePlan::build_chains() {
   ScheduleOutput out;
   build_schedule(in, out);
   chains.max_width = out.max_width;
+  chains.n_inbox = out.n_inbox;
   chains.deps_total = out.deps_total;
   chains.deps_in_task = out.deps_in_task;
   chains.deps_ring = out.deps_ring;
   chains.deps_reg = out.deps_reg;
   chains.deps_mbox = out.deps_mbox;
+  chains.deps_inbox = out.deps_inbox;
   if (!out.ok) {
     chains.ready = false;
     return SPTRSV_OK;
@@ -260,6 +323,7 @@ int DevicePlan::build_chains() {
   chains.n_chunks = (long long)out.chunk_steps.size();
   chains.n_slices = out.n_slices;
   chains.n_mbox = out.n_mbox;
+  chains.n_overflow = (long long)out.ovf_src.size();
   chains.stream_bytes = (long long)out.stream.size();
   chains.max_task_steps = out.max_task_steps;
   auto al = [](void** p, size_t bytes) { return cudaMalloc(p, bytes < 16 ? 16 : bytes); };
@@ -267,12 +331,18 @@ int DevicePlan::build_chains() {
       (e = al((void**)&chains.chunk_off, sizeof(long long) * out.chunk_off.size())) != cudaSuccess ||
       (e = al((void**)&chains.chunk_steps, sizeof(int) * out.chunk_steps.size())) != cudaSuccess ||
       (e = al((void**)&chains.task_chunk, sizeof(int) * out.task_chunk.size())) != cudaSuccess ||
-      (e = al((void**)&chains.mbox, sizeof(unsigned long long) * out.n_mbox)) != cudaSuccess ||
+      (e = al((void**)&chains.mbox, 16 * (size_t)out.n_mbox)) != cudaSuccess ||  // 16-byte slots
+      (e = al((void**)&chains.ovf_src, sizeof(int) * out.ovf_src.size())) != cudaSuccess ||
+      (e = al((void**)&chains.ovf_val, sizeof(double) * out.ovf_val.size())) != cudaSuccess ||
       (e = al((void**)&chains.ticket, sizeof(int))) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   cudaMemcpy(chains.stream, out.stream.data(), out.stream.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(chains.chunk_off, out.chunk_off.data(), sizeof(long long) * out.chunk_off.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(chains.chunk_steps, out.chunk_steps.data(), sizeof(int) * out.chunk_steps.size(), cudaMemcpyHostToDevice);
+  if (!out.ovf_src.empty()) {
+    cudaMemcpy(chains.ovf_src, out.ovf_src.data(), sizeof(int) * out.ovf_src.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(chains.ovf_val, out.ovf_val.data(), sizeof(double) * out.ovf_val.size(), cudaMemcpyHostToDevice);
+  }
   if ((e = cudaMemcpy(chains.task_chunk, out.task_chunk.data(), sizeof(int) * out.task_chunk.size(),
                       cudaMemcpyHostToDevice)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));

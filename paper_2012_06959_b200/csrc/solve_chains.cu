@@ -1,26 +1,28 @@
 // Lane-chain lockstep executor ("chains").
 //
-// Why: on B200 a dependency handed between SMs through L2 costs ~800 cycles
-// one way (tools/microbench: volatile ping-pong 1556 cycles round trip), a
-// warp-synchronous hand-off through shared memory ~35 cycles, a register 0.
-// The sync-free component pool (solve_rows.cu) pays the L2 price on every
-// level; on a 2D Laplacian in natural order that is 8191 levels.
+// Why: on B200 a value handed between SMs through L2 costs ~800 cycles one
+// way (tools/microbench/latency.cu: volatile ping-pong 1556 cycles round
+// trip), a warp-synchronous hand-off through shared memory ~35 cycles, a
+// register nothing. The sync-free component pool (solve_rows.cu) pays the L2
+// price on every level; a 2D Laplacian in natural order has 8191 of them.
 //
 // How: the host scheduler (schedule.cu) cuts the rows into contiguous tasks
 // of <= 32 dependency chains, gives each chain a lane and each row a lockstep
 // step. One warp runs one task: at every step each lane solves its row,
 // reading the chain predecessor from a register, same-task values from a
 // shared-memory ring written in earlier steps, and values of earlier tasks
-// from value-is-flag mailboxes in global memory (polled like the component
-// pool). Tasks are dealt by an ascending ticket counter to persistent warps.
+// from value-is-flag mailboxes in global memory. Tasks are dealt to
+// persistent warps by an ascending ticket counter.
 //
-// Data movement: the task's schedule is a byte stream of slices (chains.hpp)
-// read exactly once; lane 0 streams it into shared memory with
-// cp.async.bulk (TMA bulk copies, mbarrier completion) kChunkBuffers chunks
-// ahead, and every lane gathers its b values for the next chunks with
-// cp.async (LDGSTS), so the lockstep loop only touches shared memory and
-// registers. The next step's slice record is loaded into registers while the
-// current step computes.
+// Latency hiding: every slice also names the row each lane will solve
+// kPrefetch steps later and that row's cross-task mailbox slots; the lane
+// issues cp.async (LDGSTS) copies of b and of those mailboxes into shared
+// memory right away, so by the time the row is solved its inputs sit in
+// shared memory. A copied mailbox that still held "not ready" is re-polled
+// from global memory (the slow path). The schedule stream itself is read
+// exactly once: lane 0 keeps kChunkBuffers chunks in flight with
+// cp.async.bulk (TMA bulk copies completing on mbarriers), and the next
+// step's record is loaded into registers while the current step computes.
 #include "plan.hpp"
 #include "kernels.cuh"
 
@@ -34,7 +36,10 @@ struct ChainArgs {
   const int* chunk_steps;
   const int* task_chunk;
   int n_tasks;
+  int n_inbox;
   unsigned long long* mbox;
+  const int* ovf_src;
+  const double* ovf_val;
   int* ticket;
   const double* b;
   double* x;
@@ -48,9 +53,11 @@ struct ChainArgs {
 namespace {
 
 constexpr int kSmemChunks = kChunkBuffers * kChunkBytes;
-constexpr int kSmemB = kChunkBuffers * kMaxChunkSteps * 32 * 8;
 constexpr int kSmemRing = 32 * kRingSteps * 8;
-constexpr int kSmemTotal = kSmemChunks + kSmemB + kSmemRing + 64;
+constexpr int kSmemB = kPrefetch * 32 * 8;
+constexpr int kSmemInbox = kMaxInbox * kPrefetch * 32 * 16;  // 16-byte slots (cp.async.cg granularity)
+constexpr int kSmemSlot = kMaxInbox * kPrefetch * 32 * 4;
+constexpr int kSmemTotal = kSmemChunks + kSmemRing + kSmemB + kSmemInbox + kSmemSlot + 64;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -75,71 +82,58 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// b is read-only: an L1-allocating 8-byte async copy is fine.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// Mailboxes are written during the kernel: copy them L2-only (.cg, 16 bytes),
+// never from a stale L1 line. Mailbox slots are 16 bytes apart for this reason.
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+constexpr int kMboxStride = 2;  // u64 words per mailbox slot
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-struct Layout {
-  int width;
-  const int* row;
-  const int* mbo;
-  const double* rdg;
-  const double* dg;
-  const int* src;
-  const double* val;
-  int bytes;
-};
-
-template <bool EXACT>
-__device__ __forceinline__ Layout slice_at(const unsigned char* p) {
-  Layout s;
-  s.width = *reinterpret_cast<const int*>(p);
-  s.row = reinterpret_cast<const int*>(p + 16);
-  s.mbo = reinterpret_cast<const int*>(p + 144);
-  s.rdg = reinterpret_cast<const double*>(p + 272);
-  s.dg = reinterpret_cast<const double*>(p + 528);
-  const int deps = 528 + (EXACT ? 256 : 0);
-  s.src = reinterpret_cast<const int*>(p + deps);
-  s.val = reinterpret_cast<const double*>(p + deps + 128 * s.width);
-  s.bytes = slice_bytes(s.width, EXACT);
-  return s;
-}
-
-// One lane's view of one step, held in registers one step ahead (W > 0), or
-// just the fixed part with deps read in the loop (W == 0).
-template <int W>
-struct Rec {
-  int row, mbo, width;
-  double rdg, dg, b;
-  int code[W > 0 ? W : 1];
-  double val[W > 0 ? W : 1];
-};
-
+// One lane's view of one slice, loaded a step ahead into registers.
 template <bool EXACT, int W>
-__device__ __forceinline__ void load_rec(Rec<W>& r, const Layout& s, const double* bslot, int lane) {
-  r.width = s.width;
-  r.row = s.row[lane];
-  r.mbo = s.mbo[lane];
-  r.rdg = s.rdg[lane];
-  if (EXACT) r.dg = s.dg[lane];
-  r.b = bslot[lane];
-  if constexpr (W > 0) {
+struct Rec {
+  int bytes;
+  int row, mbo, pf_row;
+  int pf_mbox[kMaxInbox];
+  double rdg, dg;
+  int code[W];
+  double val[W];
+
+  __device__ __forceinline__ void load(const unsigned char* p, int lane, int n_inbox) {
+    // clamped: the look-ahead load past a chunk's last slice reads padding
+    const int width = min(max(*reinterpret_cast<const int*>(p), 0), W);
+    bytes = slice_bytes(width, n_inbox, EXACT);
+    row = reinterpret_cast<const int*>(p + 16)[lane];
+    mbo = reinterpret_cast<const int*>(p + 144)[lane];
+    rdg = reinterpret_cast<const double*>(p + 272)[lane];
+    if (EXACT) dg = reinterpret_cast<const double*>(p + 528)[lane];
+    const unsigned char* deps = p + 528 + (EXACT ? 256 : 0);
+    const int* src = reinterpret_cast<const int*>(deps);
+    const double* vals = reinterpret_cast<const double*>(deps + 128 * width);
 #pragma unroll
     for (int d = 0; d < W; ++d) {
-      if (d < s.width) {
-        r.code[d] = s.src[d * 32 + lane];
-        r.val[d] = s.val[d * 32 + lane];
+      if (d < width) {
+        code[d] = src[d * 32 + lane];
+        val[d] = vals[d * 32 + lane];
       } else {
-        r.code[d] = kSrcSkip;
+        code[d] = kSrcSkip;
       }
     }
+    const int* pf = reinterpret_cast<const int*>(deps + 384 * width);
+    pf_row = pf[lane];
+#pragma unroll
+    for (int m = 0; m < kMaxInbox; ++m) pf_mbox[m] = m < n_inbox ? pf[32 + m * 32 + lane] : -1;
   }
-}
+};
 
 struct Waiter {
   const ChainArgs& a;
@@ -148,9 +142,8 @@ struct Waiter {
   __device__ explicit Waiter(const ChainArgs& args) : a(args) {
     if (a.timeout_ns) deadline = globaltimer_ns() + a.timeout_ns;
   }
-  // Returns false when the launch aborts (watchdog or another warp's abort).
-  __device__ __forceinline__ bool mailbox(const unsigned long long* p, double& out) {
-    unsigned long long u = ld_relaxed_u64(p);
+  // Poll a mailbox until solved; false when the launch aborts.
+  __device__ __forceinline__ bool mailbox(const unsigned long long* p, unsigned long long u, double& out) {
     int polls = 0, sleep_ns = 32;
     while (u == kNotReady) {
       ++spins;
@@ -180,28 +173,18 @@ __device__ __forceinline__ double fold(double acc, double v, double xj) {
   return __fma_rn(v, xj, acc);
 }
 
-// Issue the b gathers (cp.async) for every step of a chunk already in smem.
-template <bool EXACT>
-__device__ __forceinline__ void gather_b(const unsigned char* buf, int steps, double* barea, const double* b,
-                                         int lane) {
-  const unsigned char* p = buf;
-  for (int s = 0; s < steps; ++s) {
-    Layout sl = slice_at<EXACT>(p);
-    int row = sl.row[lane];
-    if (row >= 0) cp_async8(barea + s * 32 + lane, b + row);
-    p += sl.bytes;
-  }
-  cp_async_commit();
-}
-
 template <bool EXACT, int W>
 __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* chunks = smem;
-  double* barea = reinterpret_cast<double*>(smem + kSmemChunks);
-  double* ring = reinterpret_cast<double*>(smem + kSmemChunks + kSmemB);
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kSmemChunks + kSmemB + kSmemRing);
+  double* ring = reinterpret_cast<double*>(smem + kSmemChunks);
+  double* bring = reinterpret_cast<double*>(smem + kSmemChunks + kSmemRing);
+  unsigned long long* mring = reinterpret_cast<unsigned long long*>(smem + kSmemChunks + kSmemRing + kSmemB);
+  int* mslot = reinterpret_cast<int*>(smem + kSmemChunks + kSmemRing + kSmemB + kSmemInbox);
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(smem + kSmemChunks + kSmemRing + kSmemB + kSmemInbox + kSmemSlot);
   const int lane = threadIdx.x;
+  const int M = a.n_inbox;
   if (lane == 0) {
     for (int k = 0; k < kChunkBuffers; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -217,17 +200,16 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= a.n_tasks) break;
     const int c0 = a.task_chunk[t], c1 = a.task_chunk[t + 1];
-    auto buf_of = [&](int c) { return chunks + (size_t)((c - c0) % kChunkBuffers) * kChunkBytes; };
-    auto bar_of = [&](int c) { return &bars[(c - c0) % kChunkBuffers]; };
-    auto barea_of = [&](int c) { return barea + (size_t)((c - c0) % kChunkBuffers) * kMaxChunkSteps * 32; };
     int issued_hi = c0 - 1, awaited_hi = c0 - 1;
+    auto buf_of = [&](int c) { return chunks + (size_t)((c - c0) % kChunkBuffers) * kChunkBytes; };
     auto issue = [&](int c) {
       issued_hi = c;
       if (lane == 0) {
+        unsigned long long* bar = &bars[(c - c0) % kChunkBuffers];
         const unsigned bytes = (unsigned)(a.chunk_off[c + 1] - a.chunk_off[c]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar_of(c), bytes);
-        bulk_g2s(buf_of(c), a.stream + a.chunk_off[c], bytes, bar_of(c));
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(buf_of(c), a.stream + a.chunk_off[c], bytes, bar);
       }
     };
     auto await = [&](int c) {
@@ -239,88 +221,101 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
       awaited_hi = c;
     };
     for (int c = c0; c < c1 && c < c0 + kChunkBuffers; ++c) issue(c);
-    await(c0);
-    gather_b<EXACT>(buf_of(c0), a.chunk_steps[c0], barea_of(c0), a.b, lane);
-    if (c0 + 1 < c1) {
-      await(c0 + 1);
-      gather_b<EXACT>(buf_of(c0 + 1), a.chunk_steps[c0 + 1], barea_of(c0 + 1), a.b, lane);
-    }
+
     double xprev = 0.0;
     int step = 0;
-    for (int c = c0; c < c1; ++c) {
-      if (c + 1 < c1) cp_async_wait<1>();
-      else cp_async_wait<0>();
+    Rec<EXACT, W> cur, nxt;
+    for (int c = c0; c < c1 && alive; ++c) {
+      await(c);
       const unsigned char* p = buf_of(c);
-      const double* bslot = barea_of(c);
       const int steps = a.chunk_steps[c];
-      Layout cur_sl = slice_at<EXACT>(p);
-      Rec<W> cur;
-      load_rec<EXACT, W>(cur, cur_sl, bslot, lane);
-      for (int s = 0; s < steps; ++s) {
-        // prefetch next step's record (stream data is immutable in this chunk)
-        Layout nxt_sl;
-        Rec<W> nxt;
+      cur.load(p, lane, M);
+      for (int s = 0; s < steps; ++s, ++step) {
         const bool more = s + 1 < steps;
-        if (more) {
-          nxt_sl = slice_at<EXACT>(p + cur_sl.bytes);
-          load_rec<EXACT, W>(nxt, nxt_sl, bslot + (s + 1) * 32, lane);
-        }
+        nxt.load(p + cur.bytes, lane, M);  // unconditional: keeps Rec in registers
+        const int pslot = step % kPrefetch;
+        // the copies for this step were issued kPrefetch steps ago
+        cp_async_wait<kPrefetch - 1>();
         if (cur.row >= 0) {
-          double acc = EXACT ? 0.0 : __dmul_rn(cur.b, cur.rdg);
+          const double bi = bring[pslot * 32 + lane];
+          double acc = EXACT ? 0.0 : __dmul_rn(bi, cur.rdg);
           bool ok = true;
-          if constexpr (W > 0) {
 #pragma unroll
-            for (int d = 0; d < W; ++d) {
-              const int code = cur.code[d];
-              if (code == kSrcSkip) break;
+          for (int d = 0; d < W; ++d) {
+            const int code = cur.code[d];
+            if (code != kSrcSkip && code != kSrcOverflow) {
               double xj;
-              if (code >= 0) xj = ring[code];
-              else if (code == kSrcPrev) xj = xprev;
-              else ok = ok && wait.mailbox(a.mbox + (-2 - code), xj);
+              if (code >= 0) {
+                xj = ring[code];
+              } else if (code == kSrcPrev) {
+                xj = xprev;
+              } else if (code >= kSrcInbox0 - (kMaxInbox - 1)) {
+                const int m = kSrcInbox0 - code;
+                const unsigned long long u = mring[((m * kPrefetch + pslot) * 32 + lane) * 2];
+                xj = as_f64(u);
+                if (u == kNotReady) {
+                  const unsigned long long* src = a.mbox + kMboxStride * mslot[(m * kPrefetch + pslot) * 32 + lane];
+                  ok = ok && wait.mailbox(src, ld_relaxed_u64(src), xj);
+                }
+              } else {
+                const unsigned long long* src = a.mbox + kMboxStride * (kSrcDirect - code);
+                ok = ok && wait.mailbox(src, ld_relaxed_u64(src), xj);
+              }
               acc = fold<EXACT>(acc, cur.val[d], xj);
             }
-          } else {
-            for (int d = 0; d < cur_sl.width; ++d) {
-              const int code = cur_sl.src[d * 32 + lane];
-              if (code == kSrcSkip) break;
-              const double v = cur_sl.val[d * 32 + lane];
-              double xj;
-              if (code >= 0) xj = ring[code];
-              else if (code == kSrcPrev) xj = xprev;
-              else ok = ok && wait.mailbox(a.mbox + (-2 - code), xj);
-              acc = fold<EXACT>(acc, v, xj);
+          }
+          if constexpr (W == kInlineDeps) {
+            // a row wider than kInlineDeps continues in the overflow list
+            if (cur.code[W - 1] == kSrcOverflow) {
+              const long long packed = __double_as_longlong(cur.val[W - 1]);
+              const long long start = packed >> 24, cnt = packed & 0xFFFFFF;
+              for (long long o = start; o < start + cnt; ++o) {
+                const int oc = __ldg(a.ovf_src + o);
+                const double ov = __ldg(a.ovf_val + o);
+                double oj;
+                if (oc >= 0) oj = ring[oc];
+                else if (oc == kSrcPrev) oj = xprev;
+                else {
+                  const unsigned long long* src = a.mbox + kMboxStride * (kSrcDirect - oc);
+                  ok = ok && wait.mailbox(src, ld_relaxed_u64(src), oj);
+                }
+                acc = fold<EXACT>(acc, ov, oj);
+              }
             }
           }
           if (!ok) alive = false;
-          double xi = EXACT ? div_exact(__dsub_rn(cur.b, acc), cur.dg, cur.rdg) : acc;
+          double xi = EXACT ? div_exact(__dsub_rn(bi, acc), cur.dg, cur.rdg) : acc;
           const unsigned long long bits = publishable(xi);
           xi = as_f64(bits);
           ring[lane * kRingSteps + (step % kRingSteps)] = xi;
           xprev = xi;
           a.x[cur.row] = xi;
-          if (cur.mbo >= 0) st_relaxed_u64(a.mbox + cur.mbo, bits);
+          if (cur.mbo >= 0) st_relaxed_u64(a.mbox + kMboxStride * cur.mbo, bits);
         }
+        // launch the copies for step + kPrefetch into the slots just consumed
+        if (cur.pf_row >= 0) {
+          cp_async8(bring + pslot * 32 + lane, a.b + cur.pf_row);
+#pragma unroll
+          for (int m = 0; m < kMaxInbox; ++m) {
+            const int slot = cur.pf_mbox[m];
+            if (slot >= 0) {
+              cp_async16_cg(mring + ((m * kPrefetch + pslot) * 32 + lane) * 2, a.mbox + kMboxStride * slot);
+              mslot[(m * kPrefetch + pslot) * 32 + lane] = slot;
+            }
+          }
+        }
+        cp_async_commit();
         __syncwarp();
-        ++step;
         if (more) {
-          p += cur_sl.bytes;
-          cur_sl = nxt_sl;
+          p += cur.bytes;
           cur = nxt;
         }
       }
-      if (!__all_sync(0xffffffffu, alive)) {
-        alive = false;
-        break;
-      }
-      // buffer of chunk c is free: stream chunk c + kChunkBuffers into it,
-      // and gather b for chunk c + 2 (its stream landed long ago)
+      if (!__all_sync(0xffffffffu, alive)) alive = false;
       __syncwarp();
-      if (c + kChunkBuffers < c1) issue(c + kChunkBuffers);
-      if (c + 2 < c1) {
-        await(c + 2);
-        gather_b<EXACT>(buf_of(c + 2), a.chunk_steps[c + 2], barea_of(c + 2), a.b, lane);
-      }
+      if (alive && c + kChunkBuffers < c1) issue(c + kChunkBuffers);
     }
+    cp_async_wait<0>();
     if (!alive) {
       // drain the bulk copies still in flight into this CTA's shared memory
       for (int c = awaited_hi + 1; c <= issued_hi; ++c) await(c);
@@ -346,12 +341,19 @@ cudaError_t launch_variant(const ChainArgs& a, int blocks, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <bool EXACT>
+cudaError_t launch_width(int w, const ChainArgs& a, int blocks, cudaStream_t s) {
+  if (w <= 4) return launch_variant<EXACT, 4>(a, blocks, s);
+  if (w <= 8) return launch_variant<EXACT, 8>(a, blocks, s);
+  return launch_variant<EXACT, kInlineDeps>(a, blocks, s);
+}
+
 }  // namespace
 
 int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   if (!chains.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "chains schedule not built");
   cudaError_t e;
-  if ((e = cudaMemsetAsync(chains.mbox, 0xFF, sizeof(unsigned long long) * (size_t)std::max(chains.n_mbox, 1ll), s)) !=
+  if ((e = cudaMemsetAsync(chains.mbox, 0xFF, 16 * (size_t)std::max(chains.n_mbox, 1ll), s)) !=
           cudaSuccess ||
       (e = cudaMemsetAsync(chains.ticket, 0, sizeof(int), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
@@ -363,7 +365,10 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.chunk_steps = chains.chunk_steps;
   a.task_chunk = chains.task_chunk;
   a.n_tasks = chains.n_tasks;
+  a.n_inbox = chains.n_inbox;
   a.mbox = chains.mbox;
+  a.ovf_src = chains.ovf_src;
+  a.ovf_val = chains.ovf_val;
   a.ticket = chains.ticket;
   a.b = d_b;
   a.x = d_x;
@@ -372,17 +377,11 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
-  // one warp per CTA; at most 2 CTAs per SM fit the shared-memory budget
+  // one warp per CTA, at most 2 CTAs per SM (shared-memory budget)
   const int blocks = std::max(1, std::min(chains.n_tasks, num_sms * 2));
-  const int w = chains.max_width;
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  if (chains.exact) {
-    e = w <= 4 ? launch_variant<true, 4>(a, blocks, s)
-               : (w <= 8 ? launch_variant<true, 8>(a, blocks, s) : launch_variant<true, 0>(a, blocks, s));
-  } else {
-    e = w <= 4 ? launch_variant<false, 4>(a, blocks, s)
-               : (w <= 8 ? launch_variant<false, 8>(a, blocks, s) : launch_variant<false, 0>(a, blocks, s));
-  }
+  e = chains.exact ? launch_width<true>(chains.max_width, a, blocks, s)
+                   : launch_width<false>(chains.max_width, a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;
