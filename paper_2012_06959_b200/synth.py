@@ -71,8 +71,10 @@ def _stencil_lower(n: int, diag_value: float, offsets: list[tuple[int, np.ndarra
     return CscMatrix(n=n, col_ptr=col_ptr, row_idx=rows, values=vals)
 
 
-def lap2d(nx: int) -> CscMatrix:
-    n = nx * nx
+def lap2d(nx: int, ny: int | None = None) -> CscMatrix:
+    """5-point lower stencil on an nx-by-ny grid (ny defaults to nx)."""
+    ny = nx if ny is None else ny
+    n = nx * ny
     i = np.arange(n, dtype=np.int64)
     x = i % nx
     y = i // nx
