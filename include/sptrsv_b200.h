@@ -61,7 +61,8 @@ typedef struct sptrsv_options {
   int32_t spin_initial;   /* Backoff.initial_pause (engine.py:61-66) */
   int32_t spin_max_ns;    /* Backoff.max_pause, as nanoseconds of __nanosleep */
   int32_t chain_lanes;    /* chains executor: lanes per warp task (<=32); 0 = 32 */
-  int32_t reserved[7];
+  int32_t probe_flags;    /* diagnostics only (tools/chains_probe.py); 0 in production */
+  int32_t reserved[6];
 } sptrsv_options;
 
 typedef struct sptrsv_stats {
@@ -134,6 +135,10 @@ int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x,
 int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats);
 
 int sptrsv_plan_destroy(sptrsv_plan* plan);
+
+/* Diagnostics: copy up to `count` probe timestamps (clock64) recorded by the
+ * last solve when options.probe_flags asked for them. */
+int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count);
 
 /* Last error message of this thread (empty string when none). */
 const char* sptrsv_last_error(void);

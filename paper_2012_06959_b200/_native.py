@@ -36,7 +36,8 @@ class Options(C.Structure):
         ("spin_initial", C.c_int32),
         ("spin_max_ns", C.c_int32),
         ("chain_lanes", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("probe_flags", C.c_int32),
+        ("reserved", C.c_int32 * 6),
     ]
 
 
@@ -126,6 +127,8 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_abi_version.restype = C.c_int
     lib.sptrsv_plan_get_info.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
     lib.sptrsv_plan_get_info.restype = C.c_int
+    lib.sptrsv_plan_probe_read.argtypes = [C.c_void_p, _P64, C.c_int32]
+    lib.sptrsv_plan_probe_read.restype = C.c_int
 
 
 def load_library() -> C.CDLL:
@@ -169,7 +172,8 @@ class NativePlan:
     """A device-resident plan for one matrix (C handle ``sptrsv_plan*``)."""
 
     def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
-                 timeout=60.0, spin_initial=16, spin_max_ns=512, structure_only=False, chain_lanes=32):
+                 timeout=60.0, spin_initial=16, spin_max_ns=512, structure_only=False, chain_lanes=32,
+                 probe_flags=0):
         lib = require_gpu()
         self._lib = lib
         self.n = int(n)
@@ -185,6 +189,7 @@ class NativePlan:
         opt.spin_initial = int(spin_initial)
         opt.spin_max_ns = int(spin_max_ns)
         opt.chain_lanes = int(chain_lanes)
+        opt.probe_flags = int(probe_flags)
         handle = C.c_void_p()
         bad = C.c_int64(-1)
         rc = lib.sptrsv_plan_create(_ptr(cp, C.c_int64), _ptr(ri, C.c_int64),
@@ -208,6 +213,12 @@ class NativePlan:
         rc = self._lib.sptrsv_plan_get_info(self._h, C.byref(inf))
         raise_for_status(rc, _err(self._lib))
         return inf.as_dict()
+
+    def probe_stamps(self) -> np.ndarray:
+        out = np.zeros(5 * 64, dtype=np.int64)
+        rc = self._lib.sptrsv_plan_probe_read(self._h, _ptr(out, C.c_int64), out.size)
+        raise_for_status(rc, _err(self._lib))
+        return out.reshape(64, 5)
 
     def in_degrees(self) -> np.ndarray:
         out = np.empty(self.n, dtype=np.int64)

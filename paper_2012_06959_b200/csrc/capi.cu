@@ -49,7 +49,7 @@ namespace sptrsv {
 void DevicePlan::release() {
   cudaSetDevice(device);
   void* ptrs[] = {rp, ci, cv, wv, dg, rdg, indeg, level, by_level, level_ptr, order, xbuf, bbuf, ticket, status,
-                  abort_flag, xseg_dev, lseg_dev};
+                  abort_flag, xseg_dev, lseg_dev, probe_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   chains.release();
@@ -414,6 +414,16 @@ int sptrsv_plan_get_info(const sptrsv_plan* plan, sptrsv_plan_info* info) {
   info->deps_mailbox = c.deps_mbox;
   info->chain_max_task_steps = c.max_task_steps;
   info->schedule_ms = c.schedule_ms;
+  return SPTRSV_OK;
+}
+
+int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count) {
+  g_err.clear();
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p || !out) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (!p->probe_buf) return fail(SPTRSV_E_ARGUMENT, "no probe data: set options.probe_flags");
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(cudaMemcpy(out, p->probe_buf, sizeof(long long) * std::min(count, 5 * 64), cudaMemcpyDeviceToHost));
   return SPTRSV_OK;
 }
 

@@ -62,18 +62,20 @@ struct ChainPlan {
   unsigned char* stream = nullptr;     // slices, chunked
   long long* chunk_off = nullptr;      // [n_chunks+1] byte offsets into stream
   int* chunk_steps = nullptr;          // [n_chunks] slices per chunk
+  int* chunk_width = nullptr;          // [n_chunks] dependency slots per slice (uniform in a chunk)
   int* task_chunk = nullptr;           // [n_tasks+1] first chunk of each task
-  unsigned long long* mbox = nullptr;  // [n_mbox] cross-task mailboxes (value-is-flag)
+  unsigned long long* mbox = nullptr;  // [n_mbox] cross-task mailboxes (value-is-flag, 16-byte slots)
   int* ovf_src = nullptr;              // overflow dependency lists (rows wider than kInlineDeps)
   double* ovf_val = nullptr;
   int* ticket = nullptr;
   void release() {
-    void* ptrs[] = {stream, chunk_off, chunk_steps, task_chunk, mbox, ovf_src, ovf_val, ticket};
+    void* ptrs[] = {stream, chunk_off, chunk_steps, chunk_width, task_chunk, mbox, ovf_src, ovf_val, ticket};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
     chunk_off = nullptr;
     chunk_steps = nullptr;
+    chunk_width = nullptr;
     task_chunk = nullptr;
     mbox = nullptr;
     ovf_src = nullptr;

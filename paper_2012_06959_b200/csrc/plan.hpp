@@ -48,6 +48,7 @@ struct DevicePlan {
   int** lseg_dev = nullptr;
 
   ChainPlan chains;
+  long long* probe_buf = nullptr;  // diagnostics (probe_flags)
   int executor_used = SPTRSV_EXECUTOR_ROWS;
 
   double setup_ms = 0.0;

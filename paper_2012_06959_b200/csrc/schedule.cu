@@ -46,6 +46,7 @@ struct ScheduleOutput {
   std::vector<unsigned char> stream;
   std::vector<long long> chunk_off;
   std::vector<int> chunk_steps;
+  std::vector<int> chunk_width;
   std::vector<int> task_chunk;
   std::vector<int> ovf_src;
   std::vector<double> ovf_val;
@@ -180,21 +181,37 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       for (int r = count[s]; r < count[s + 1]; ++r) row[lane_of[rows_by_step[r]]] = rows_by_step[r];
     };
     std::fill(prev_in_lane.begin(), prev_in_lane.end(), -1);
-    size_t chunk_begin = st.size();
+    // slice widths, then chunks of uniform width (the kernel computes slice
+    // addresses from the chunk's width instead of loading them)
+    std::vector<int> widths(nsteps, 0);
+    for (int s = 0; s < nsteps; ++s)
+      for (int r = count[s]; r < count[s + 1]; ++r) {
+        const int i = rows_by_step[r];
+        widths[s] = std::max(widths[s], std::min(rp[i + 1] - rp[i], kInlineDeps));
+      }
+    std::vector<int> chunk_of_step(nsteps), chunk_w;
+    for (int s = 0; s < nsteps;) {
+      int w = widths[s], cnt = 1;
+      while (s + cnt < nsteps && (cnt + 1) * slice_bytes(std::max(w, widths[s + cnt]), M, in.exact) <= kChunkBytes) {
+        w = std::max(w, widths[s + cnt]);
+        ++cnt;
+      }
+      for (int k = 0; k < cnt; ++k) chunk_of_step[s + k] = (int)chunk_w.size();
+      chunk_w.push_back(w);
+      s += cnt;
+    }
     int chunk_steps = 0;
     int row[32], pf[32];
     for (int s = 0; s < nsteps; ++s) {
       rows_at(s, row);
       rows_at(s + P, pf);
-      int width = 0;
-      for (int q = 0; q < 32; ++q)
-        if (row[q] >= 0) width = std::max(width, std::min(rp[row[q] + 1] - rp[row[q]], kInlineDeps));
+      const int width = chunk_w[chunk_of_step[s]];
       out.max_width = std::max(out.max_width, width);
       const int bytes = slice_bytes(width, M, in.exact);
-      if ((st.size() - chunk_begin) + bytes > (size_t)kChunkBytes) {
+      if (s > 0 && chunk_of_step[s] != chunk_of_step[s - 1]) {
         out.chunk_steps.push_back(chunk_steps);
+        out.chunk_width.push_back(chunk_w[chunk_of_step[s - 1]]);
         out.chunk_off.push_back((long long)st.size());
-        chunk_begin = st.size();
         chunk_steps = 0;
       }
       const size_t base = st.size();
@@ -253,7 +270,7 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
           } else if (j == prev_in_lane[q]) {
             code = kSrcPrev;
           } else if (s - step_of[j] < kRingSteps) {
-            code = lane_of[j] * kRingSteps + (step_of[j] % kRingSteps);
+            code = (step_of[j] % kRingSteps) * 32 + lane_of[j];  // [step][lane]: conflict-free
           } else {
             code = kSrcDirect - mbox_of[j];
           }
@@ -280,6 +297,7 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
     }
     if (chunk_steps > 0) {
       out.chunk_steps.push_back(chunk_steps);
+      out.chunk_width.push_back(chunk_w.back());
       out.chunk_off.push_back((long long)st.size());
     }
   }
@@ -330,6 +348,7 @@ int DevicePlan::build_chains() {
   if ((e = al((void**)&chains.stream, out.stream.size())) != cudaSuccess ||
       (e = al((void**)&chains.chunk_off, sizeof(long long) * out.chunk_off.size())) != cudaSuccess ||
       (e = al((void**)&chains.chunk_steps, sizeof(int) * out.chunk_steps.size())) != cudaSuccess ||
+      (e = al((void**)&chains.chunk_width, sizeof(int) * out.chunk_width.size())) != cudaSuccess ||
       (e = al((void**)&chains.task_chunk, sizeof(int) * out.task_chunk.size())) != cudaSuccess ||
       (e = al((void**)&chains.mbox, 16 * (size_t)out.n_mbox)) != cudaSuccess ||  // 16-byte slots
       (e = al((void**)&chains.ovf_src, sizeof(int) * out.ovf_src.size())) != cudaSuccess ||
@@ -339,6 +358,7 @@ int DevicePlan::build_chains() {
   cudaMemcpy(chains.stream, out.stream.data(), out.stream.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(chains.chunk_off, out.chunk_off.data(), sizeof(long long) * out.chunk_off.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(chains.chunk_steps, out.chunk_steps.data(), sizeof(int) * out.chunk_steps.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(chains.chunk_width, out.chunk_width.data(), sizeof(int) * out.chunk_width.size(), cudaMemcpyHostToDevice);
   if (!out.ovf_src.empty()) {
     cudaMemcpy(chains.ovf_src, out.ovf_src.data(), sizeof(int) * out.ovf_src.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(chains.ovf_val, out.ovf_val.data(), sizeof(double) * out.ovf_val.size(), cudaMemcpyHostToDevice);

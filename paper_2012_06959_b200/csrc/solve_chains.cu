@@ -34,6 +34,7 @@ struct ChainArgs {
   const unsigned char* stream;
   const long long* chunk_off;
   const int* chunk_steps;
+  const int* chunk_width;
   const int* task_chunk;
   int n_tasks;
   int n_inbox;
@@ -48,7 +49,14 @@ struct ChainArgs {
   unsigned long long timeout_ns;
   int spin_initial;
   int spin_max_ns;
+  int flags;            // probe variants (kProbe*), 0 in production
+  long long* dbg;       // probe timestamps, nullptr unless kProbeClock
 };
+
+// Probe variants (tools/chains_probe.py): switch parts of the step off to
+// attribute its cost, and record clock64 stamps of one warp's steps.
+constexpr int kProbeNoB = 1, kProbeNoStoreX = 2, kProbeNoWait = 4, kProbeClock = 16;
+constexpr int kProbeFirstStep = 1000, kProbeSteps = 64;
 
 namespace {
 
@@ -98,74 +106,73 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Byte offsets inside a slice of a chunk whose uniform width is w: computed
+// once per chunk, so loading the next step's record never waits on a load.
+struct Geom {
+  int sb, deps, vals, pf;
+  __device__ __forceinline__ Geom(int w, int n_inbox, bool exact) {
+    sb = slice_bytes(w, n_inbox, exact);
+    deps = 528 + (exact ? 256 : 0);
+    vals = deps + 128 * w;
+    pf = deps + 384 * w;
+  }
+};
+
 // One lane's view of one slice, loaded a step ahead into registers.
 template <bool EXACT, int W>
 struct Rec {
-  int bytes;
   int row, mbo, pf_row;
   int pf_mbox[kMaxInbox];
   double rdg, dg;
   int code[W];
   double val[W];
 
-  __device__ __forceinline__ void load(const unsigned char* p, int lane, int n_inbox) {
-    // clamped: the look-ahead load past a chunk's last slice reads padding
-    const int width = min(max(*reinterpret_cast<const int*>(p), 0), W);
-    bytes = slice_bytes(width, n_inbox, EXACT);
+  __device__ __forceinline__ void load(const unsigned char* p, const Geom& g, int w, int lane, int n_inbox) {
     row = reinterpret_cast<const int*>(p + 16)[lane];
     mbo = reinterpret_cast<const int*>(p + 144)[lane];
     rdg = reinterpret_cast<const double*>(p + 272)[lane];
     if (EXACT) dg = reinterpret_cast<const double*>(p + 528)[lane];
-    const unsigned char* deps = p + 528 + (EXACT ? 256 : 0);
-    const int* src = reinterpret_cast<const int*>(deps);
-    const double* vals = reinterpret_cast<const double*>(deps + 128 * width);
+    const int* src = reinterpret_cast<const int*>(p + g.deps);
+    const double* vals = reinterpret_cast<const double*>(p + g.vals);
 #pragma unroll
     for (int d = 0; d < W; ++d) {
-      if (d < width) {
-        code[d] = src[d * 32 + lane];
-        val[d] = vals[d * 32 + lane];
-      } else {
-        code[d] = kSrcSkip;
-      }
+      code[d] = d < w ? src[d * 32 + lane] : kSrcSkip;
+      val[d] = d < w ? vals[d * 32 + lane] : 0.0;
     }
-    const int* pf = reinterpret_cast<const int*>(deps + 384 * width);
+    const int* pf = reinterpret_cast<const int*>(p + g.pf);
     pf_row = pf[lane];
 #pragma unroll
     for (int m = 0; m < kMaxInbox; ++m) pf_mbox[m] = m < n_inbox ? pf[32 + m * 32 + lane] : -1;
   }
 };
 
-struct Waiter {
-  const ChainArgs& a;
-  unsigned long long spins = 0;
-  unsigned long long deadline = 0;
-  __device__ explicit Waiter(const ChainArgs& args) : a(args) {
-    if (a.timeout_ns) deadline = globaltimer_ns() + a.timeout_ns;
-  }
-  // Poll a mailbox until solved; false when the launch aborts.
-  __device__ __forceinline__ bool mailbox(const unsigned long long* p, unsigned long long u, double& out) {
-    int polls = 0, sleep_ns = 32;
-    while (u == kNotReady) {
-      ++spins;
-      ++polls;
-      if (polls > a.spin_initial) {
-        if ((polls & 63) == 0) {
-          if (ld_relaxed_s32(a.abort_flag)) return false;
-          if (deadline && globaltimer_ns() > deadline) {
-            atomicExch(&a.status->code, 5);
-            atomicExch(a.abort_flag, 1);
-            return false;
-          }
+// Slow path, kept out of line: poll a mailbox until it is solved. Returns its
+// bits, or kNotReady when the launch is aborting (watchdog or another warp).
+// Spins are added to the device status here, off the hot path.
+__device__ __noinline__ unsigned long long poll_mailbox(const unsigned long long* p, int* abort_flag,
+                                                        DeviceStatus* status, int spin_initial, int spin_max_ns,
+                                                        unsigned long long deadline) {
+  unsigned long long u = ld_relaxed_u64(p);
+  int polls = 0, sleep_ns = 32;
+  while (u == kNotReady) {
+    ++polls;
+    if (polls > spin_initial) {
+      if ((polls & 63) == 0) {
+        if (ld_relaxed_s32(abort_flag)) break;
+        if (deadline && globaltimer_ns() > deadline) {
+          atomicExch(&status->code, 5);
+          atomicExch(abort_flag, 1);
+          break;
         }
-        __nanosleep(sleep_ns);
-        if (sleep_ns < a.spin_max_ns) sleep_ns <<= 1;
       }
-      u = ld_relaxed_u64(p);
+      __nanosleep(sleep_ns);
+      if (sleep_ns < spin_max_ns) sleep_ns <<= 1;
     }
-    out = as_f64(u);
-    return true;
+    u = ld_relaxed_u64(p);
   }
-};
+  if (polls) atomicAdd(&status->spins, (unsigned long long)polls);
+  return u;
+}
 
 template <bool EXACT>
 __device__ __forceinline__ double fold(double acc, double v, double xj) {
@@ -191,7 +198,13 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
   }
   __syncwarp();
   unsigned phase_bits = 0;  // parity to wait for, per buffer
-  Waiter wait(a);
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  auto poll = [&](int slot, bool& ok) {
+    const unsigned long long u =
+        poll_mailbox(a.mbox + kMboxStride * slot, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+    ok = ok && u != kNotReady;
+    return as_f64(u);
+  };
   bool alive = true;
 
   while (alive) {
@@ -225,76 +238,90 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
     double xprev = 0.0;
     int step = 0;
     Rec<EXACT, W> cur, nxt;
+    int w_next = a.chunk_width[c0], steps_next = a.chunk_steps[c0];
     for (int c = c0; c < c1 && alive; ++c) {
+      const int w = w_next, steps = steps_next;
+      if (c + 1 < c1) {  // scalars of the next chunk, consumed a chunk later
+        w_next = a.chunk_width[c + 1];
+        steps_next = a.chunk_steps[c + 1];
+      }
+      const Geom g(w, M, EXACT);
       await(c);
       const unsigned char* p = buf_of(c);
-      const int steps = a.chunk_steps[c];
-      cur.load(p, lane, M);
+      cur.load(p, g, w, lane, M);
       for (int s = 0; s < steps; ++s, ++step) {
-        const bool more = s + 1 < steps;
-        nxt.load(p + cur.bytes, lane, M);  // unconditional: keeps Rec in registers
+        // next record: fixed offsets, issued before this step's dependencies
+        // (past the chunk's last slice it reads padding that is never used)
+        nxt.load(p + (s + 1) * g.sb, g, w, lane, M);
+        const bool probe = a.dbg && blockIdx.x == 0 && lane == 0 && step >= kProbeFirstStep &&
+                           step < kProbeFirstStep + kProbeSteps;
+        long long* stamp = probe ? a.dbg + 5 * (step - kProbeFirstStep) : nullptr;
+        if (probe) stamp[0] = clock64();
         const int pslot = step % kPrefetch;
         // the copies for this step were issued kPrefetch steps ago
-        cp_async_wait<kPrefetch - 1>();
-        if (cur.row >= 0) {
-          const double bi = bring[pslot * 32 + lane];
-          double acc = EXACT ? 0.0 : __dmul_rn(bi, cur.rdg);
-          bool ok = true;
+        if (!(a.flags & kProbeNoWait)) cp_async_wait<kPrefetch - 1>();
+        if (probe) stamp[1] = clock64();
+        // gather every dependency value branch-free (ring / register / inbox),
+        // flag the rare ones that must be polled from global memory
+        double xj[W];
+        unsigned slow = 0;
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+          const int code = cur.code[d];
+          const double rv = ring[code >= 0 ? code : 0];
+          const int m = kSrcInbox0 - code;
+          const bool inbox = m >= 0 && m < kMaxInbox;
+          const unsigned long long iu = mring[(((inbox ? m : 0) * kPrefetch + pslot) * 32 + lane) * 2];
+          xj[d] = code >= 0 ? rv : (code == kSrcPrev ? xprev : as_f64(iu));
+          if ((inbox && iu == kNotReady) || code <= kSrcDirect) slow |= 1u << d;
+        }
+        if (__any_sync(0xffffffffu, slow != 0)) {
 #pragma unroll
           for (int d = 0; d < W; ++d) {
-            const int code = cur.code[d];
-            if (code != kSrcSkip && code != kSrcOverflow) {
-              double xj;
-              if (code >= 0) {
-                xj = ring[code];
-              } else if (code == kSrcPrev) {
-                xj = xprev;
-              } else if (code >= kSrcInbox0 - (kMaxInbox - 1)) {
-                const int m = kSrcInbox0 - code;
-                const unsigned long long u = mring[((m * kPrefetch + pslot) * 32 + lane) * 2];
-                xj = as_f64(u);
-                if (u == kNotReady) {
-                  const unsigned long long* src = a.mbox + kMboxStride * mslot[(m * kPrefetch + pslot) * 32 + lane];
-                  ok = ok && wait.mailbox(src, ld_relaxed_u64(src), xj);
-                }
-              } else {
-                const unsigned long long* src = a.mbox + kMboxStride * (kSrcDirect - code);
-                ok = ok && wait.mailbox(src, ld_relaxed_u64(src), xj);
-              }
-              acc = fold<EXACT>(acc, cur.val[d], xj);
+            if (slow & (1u << d)) {
+              const int code = cur.code[d];
+              const int m = kSrcInbox0 - code;
+              const int slot = code <= kSrcDirect ? kSrcDirect - code : mslot[(m * kPrefetch + pslot) * 32 + lane];
+              xj[d] = poll(slot, alive);
             }
           }
-          if constexpr (W == kInlineDeps) {
-            // a row wider than kInlineDeps continues in the overflow list
-            if (cur.code[W - 1] == kSrcOverflow) {
-              const long long packed = __double_as_longlong(cur.val[W - 1]);
-              const long long start = packed >> 24, cnt = packed & 0xFFFFFF;
-              for (long long o = start; o < start + cnt; ++o) {
-                const int oc = __ldg(a.ovf_src + o);
-                const double ov = __ldg(a.ovf_val + o);
-                double oj;
-                if (oc >= 0) oj = ring[oc];
-                else if (oc == kSrcPrev) oj = xprev;
-                else {
-                  const unsigned long long* src = a.mbox + kMboxStride * (kSrcDirect - oc);
-                  ok = ok && wait.mailbox(src, ld_relaxed_u64(src), oj);
-                }
-                acc = fold<EXACT>(acc, ov, oj);
-              }
+        }
+        const double bi = (a.flags & kProbeNoB) ? 1.0 : bring[pslot * 32 + lane];
+        double acc = EXACT ? 0.0 : __dmul_rn(bi, cur.rdg);
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+          const double folded = fold<EXACT>(acc, cur.val[d], xj[d]);
+          acc = (cur.code[d] != kSrcSkip && cur.code[d] != kSrcOverflow) ? folded : acc;
+        }
+        if constexpr (W == kInlineDeps) {
+          // a row wider than kInlineDeps continues in the overflow list
+          if (cur.code[W - 1] == kSrcOverflow) {
+            const long long packed = __double_as_longlong(cur.val[W - 1]);
+            const long long start = packed >> 24, cnt = packed & 0xFFFFFF;
+            for (long long o = start; o < start + cnt; ++o) {
+              const int oc = __ldg(a.ovf_src + o);
+              const double ov = __ldg(a.ovf_val + o);
+              double oj;
+              if (oc >= 0) oj = ring[oc];
+              else if (oc == kSrcPrev) oj = xprev;
+              else oj = poll(kSrcDirect - oc, alive);
+              acc = fold<EXACT>(acc, ov, oj);
             }
           }
-          if (!ok) alive = false;
+        }
+        if (probe) stamp[2] = clock64();
+        if (cur.row >= 0) {
           double xi = EXACT ? div_exact(__dsub_rn(bi, acc), cur.dg, cur.rdg) : acc;
           const unsigned long long bits = publishable(xi);
           xi = as_f64(bits);
-          ring[lane * kRingSteps + (step % kRingSteps)] = xi;
+          ring[(step % kRingSteps) * 32 + lane] = xi;
           xprev = xi;
-          a.x[cur.row] = xi;
+          if (!(a.flags & kProbeNoStoreX)) a.x[cur.row] = xi;
           if (cur.mbo >= 0) st_relaxed_u64(a.mbox + kMboxStride * cur.mbo, bits);
         }
         // launch the copies for step + kPrefetch into the slots just consumed
         if (cur.pf_row >= 0) {
-          cp_async8(bring + pslot * 32 + lane, a.b + cur.pf_row);
+          if (!(a.flags & kProbeNoB)) cp_async8(bring + pslot * 32 + lane, a.b + cur.pf_row);
 #pragma unroll
           for (int m = 0; m < kMaxInbox; ++m) {
             const int slot = cur.pf_mbox[m];
@@ -305,11 +332,10 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
           }
         }
         cp_async_commit();
+        if (probe) stamp[3] = clock64();
         __syncwarp();
-        if (more) {
-          p += cur.bytes;
-          cur = nxt;
-        }
+        if (probe) stamp[4] = clock64();
+        cur = nxt;
       }
       if (!__all_sync(0xffffffffu, alive)) alive = false;
       __syncwarp();
@@ -323,10 +349,6 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
     }
   }
   cp_async_wait<0>();
-  unsigned long long sp = wait.spins;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, off);
-  if (lane == 0 && sp) atomicAdd(&a.status->spins, sp);
 }
 
 template <bool EXACT, int W>
@@ -363,6 +385,7 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.stream = chains.stream;
   a.chunk_off = chains.chunk_off;
   a.chunk_steps = chains.chunk_steps;
+  a.chunk_width = chains.chunk_width;
   a.task_chunk = chains.task_chunk;
   a.n_tasks = chains.n_tasks;
   a.n_inbox = chains.n_inbox;
@@ -377,6 +400,13 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
+  a.flags = opt.probe_flags;
+  if (opt.probe_flags & kProbeClock) {
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 5 * kProbeSteps) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, "probe buffer");
+    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 5 * kProbeSteps, s);
+    a.dbg = probe_buf;
+  }
   // one warp per CTA, at most 2 CTAs per SM (shared-memory budget)
   const int blocks = std::max(1, std::min(chains.n_tasks, num_sms * 2));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
