@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
           const bool inbox = m >= 0 && m < kMaxInbox;
           const unsigned long long iu = mring[(((inbox ? m : 0) * kPrefetch + pslot) * 32 + lane) * 2];
           xj[d] = code >= 0 ? rv : (code == kSrcPrev ? xprev : as_f64(iu));
-          if ((inbox && iu == kNotReady) || code <= kSrcDirect) slow |= 1u << d;
+          if ((inbox && iu == kNotReady) || (code <= kSrcDirect && code != kSrcSkip)) slow |= 1u << d;
         }
         if (__any_sync(0xffffffffu, slow != 0)) {
 #pragma unroll
