@@ -139,9 +139,8 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
             continue;
           }
           ++out.deps_in_task;
-          if (j == prev_in_lane[li]) {
-            ++out.deps_reg;
-          } else if (step_of[i] - step_of[j] < kRingSteps) {
+          if (j == prev_in_lane[li]) ++out.deps_reg;  // statistic: chain predecessor (read from the ring)
+          if (step_of[i] - step_of[j] < kRingSteps) {
             ++out.deps_ring;
           } else {
             ++out.deps_mbox;
@@ -218,20 +217,17 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
       st.resize(base + bytes);
       unsigned char* p = st.data() + base;
       std::memset(p, 0, bytes);
-      int32_t* hdr = reinterpret_cast<int32_t*>(p);
-      hdr[0] = width;
-      hdr[1] = M;
-      int32_t* srow = reinterpret_cast<int32_t*>(p + 16);
-      int32_t* smbo = reinterpret_cast<int32_t*>(p + 144);
-      double* srdg = reinterpret_cast<double*>(p + 272);
-      double* sdg = reinterpret_cast<double*>(p + 528);
-      const size_t deps_off = 528 + (in.exact ? 256 : 0);
-      int32_t* ssrc = reinterpret_cast<int32_t*>(p + deps_off);
-      double* sval = reinterpret_cast<double*>(p + deps_off + 128 * (size_t)width);
-      int32_t* spf = reinterpret_cast<int32_t*>(p + deps_off + 384 * (size_t)width);
-      int32_t* spfm = spf + 32;
+      const SliceGeom g(width, M, in.exact);
+      int32_t* srow = reinterpret_cast<int32_t*>(p);
+      int32_t* smbo = reinterpret_cast<int32_t*>(p + 128);
+      int32_t* spf = reinterpret_cast<int32_t*>(p + 256);
+      int32_t* spfm = reinterpret_cast<int32_t*>(p + g.pfm);
+      double* srdg = reinterpret_cast<double*>(p + g.rdg);
+      double* sdg = reinterpret_cast<double*>(p + g.dg);
+      int32_t* ssrc = reinterpret_cast<int32_t*>(p + g.src);
+      double* sval = reinterpret_cast<double*>(p + g.val);
       for (int q = 0; q < 32; ++q) {
-        // prefetch fields for step s + P
+        // prefetch fields for step s + P: b of that row, its inbox mailboxes
         const int f = pf[q];
         spf[q] = f;
         int m = 0;
@@ -261,16 +257,14 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
           int code;
           if (j < a) {
             if (inline_dep(d, nd) && inbox < M) {
-              code = kSrcInbox0 - inbox;
+              code = inbox_offset(inbox, s, q);  // prefetched kPrefetch steps ago
               ++inbox;
               ++out.deps_inbox;
             } else {
               code = kSrcDirect - mbox_of[j];
             }
-          } else if (j == prev_in_lane[q]) {
-            code = kSrcPrev;
           } else if (s - step_of[j] < kRingSteps) {
-            code = (step_of[j] % kRingSteps) * 32 + lane_of[j];  // [step][lane]: conflict-free
+            code = ring_offset(step_of[j], lane_of[j]);  // includes the chain predecessor
           } else {
             code = kSrcDirect - mbox_of[j];
           }

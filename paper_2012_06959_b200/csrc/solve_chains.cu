@@ -2,27 +2,27 @@
 //
 // Why: on B200 a value handed between SMs through L2 costs ~800 cycles one
 // way (tools/microbench/latency.cu: volatile ping-pong 1556 cycles round
-// trip), a warp-synchronous hand-off through shared memory ~35 cycles, a
-// register nothing. The sync-free component pool (solve_rows.cu) pays the L2
-// price on every level; a 2D Laplacian in natural order has 8191 of them.
+// trip), a warp-synchronous hand-off through shared memory ~35 cycles. The
+// sync-free component pool (solve_rows.cu) pays the L2 price on every level;
+// a 2D Laplacian in natural order has 8191 of them.
 //
 // How: the host scheduler (schedule.cu) cuts the rows into contiguous tasks
 // of <= 32 dependency chains, gives each chain a lane and each row a lockstep
 // step. One warp runs one task: at every step each lane solves its row,
-// reading the chain predecessor from a register, same-task values from a
+// reading same-task values (its chain predecessor included) from a
 // shared-memory ring written in earlier steps, and values of earlier tasks
 // from value-is-flag mailboxes in global memory. Tasks are dealt to
 // persistent warps by an ascending ticket counter.
 //
-// Latency hiding: every slice also names the row each lane will solve
-// kPrefetch steps later and that row's cross-task mailbox slots; the lane
-// issues cp.async (LDGSTS) copies of b and of those mailboxes into shared
-// memory right away, so by the time the row is solved its inputs sit in
-// shared memory. A copied mailbox that still held "not ready" is re-polled
-// from global memory (the slow path). The schedule stream itself is read
-// exactly once: lane 0 keeps kChunkBuffers chunks in flight with
-// cp.async.bulk (TMA bulk copies completing on mbarriers), and the next
-// step's record is loaded into registers while the current step computes.
+// The step is one warp's critical path, so it is kept short and branch-free:
+// every dependency is one shared-memory load at a byte offset the scheduler
+// baked into the stream (ring slot or inbox slot); the slice addresses follow
+// from the chunk's uniform width; b and cross-task mailbox values are fetched
+// kPrefetch steps ahead with cp.async (LDGSTS; mailboxes L2-only .cg) into
+// shared memory; a prefetched mailbox that still held "not ready" (and the
+// rare direct dependency) goes through an out-of-line polling slow path. The
+// schedule stream is read exactly once: lane 0 keeps kChunkBuffers chunks in
+// flight with cp.async.bulk (TMA bulk copies completing on mbarriers).
 #include "plan.hpp"
 #include "kernels.cuh"
 
@@ -49,23 +49,17 @@ struct ChainArgs {
   unsigned long long timeout_ns;
   int spin_initial;
   int spin_max_ns;
-  int flags;            // probe variants (kProbe*), 0 in production
-  long long* dbg;       // probe timestamps, nullptr unless kProbeClock
+  long long* dbg;  // probe timestamps (PROBE instantiation only)
 };
 
-// Probe variants (tools/chains_probe.py): switch parts of the step off to
-// attribute its cost, and record clock64 stamps of one warp's steps.
-constexpr int kProbeNoB = 1, kProbeNoStoreX = 2, kProbeNoWait = 4, kProbeClock = 16;
+// Probe (tools/chains_probe.py): clock64 stamps of block 0 lane 0 for steps
+// [kProbeFirstStep, kProbeFirstStep + kProbeSteps), 5 per step.
+constexpr int kProbeClock = 16;
 constexpr int kProbeFirstStep = 1000, kProbeSteps = 64;
 
 namespace {
 
-constexpr int kSmemChunks = kChunkBuffers * kChunkBytes;
-constexpr int kSmemRing = 32 * kRingSteps * 8;
-constexpr int kSmemB = kPrefetch * 32 * 8;
-constexpr int kSmemInbox = kMaxInbox * kPrefetch * 32 * 16;  // 16-byte slots (cp.async.cg granularity)
-constexpr int kSmemSlot = kMaxInbox * kPrefetch * 32 * 4;
-constexpr int kSmemTotal = kSmemChunks + kSmemRing + kSmemB + kSmemInbox + kSmemSlot + 64;
+constexpr int kMboxStride = 2;  // u64 words per mailbox slot (16-byte slots for cp.async.cg)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -90,65 +84,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-// b is read-only: an L1-allocating 8-byte async copy is fine.
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+// b is read-only: an L1-allocating 8-byte async copy.
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
 }
-// Mailboxes are written during the kernel: copy them L2-only (.cg, 16 bytes),
-// never from a stale L1 line. Mailbox slots are 16 bytes apart for this reason.
-__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+// Mailboxes are written during the kernel: copy them L2-only (.cg, 16 bytes).
+__device__ __forceinline__ void cp_async16_cg(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
-constexpr int kMboxStride = 2;  // u64 words per mailbox slot
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
 
-// Byte offsets inside a slice of a chunk whose uniform width is w: computed
-// once per chunk, so loading the next step's record never waits on a load.
-struct Geom {
-  int sb, deps, vals, pf;
-  __device__ __forceinline__ Geom(int w, int n_inbox, bool exact) {
-    sb = slice_bytes(w, n_inbox, exact);
-    deps = 528 + (exact ? 256 : 0);
-    vals = deps + 128 * w;
-    pf = deps + 384 * w;
-  }
-};
-
-// One lane's view of one slice, loaded a step ahead into registers.
-template <bool EXACT, int W>
-struct Rec {
-  int row, mbo, pf_row;
-  int pf_mbox[kMaxInbox];
-  double rdg, dg;
-  int code[W];
-  double val[W];
-
-  __device__ __forceinline__ void load(const unsigned char* p, const Geom& g, int w, int lane, int n_inbox) {
-    row = reinterpret_cast<const int*>(p + 16)[lane];
-    mbo = reinterpret_cast<const int*>(p + 144)[lane];
-    rdg = reinterpret_cast<const double*>(p + 272)[lane];
-    if (EXACT) dg = reinterpret_cast<const double*>(p + 528)[lane];
-    const int* src = reinterpret_cast<const int*>(p + g.deps);
-    const double* vals = reinterpret_cast<const double*>(p + g.vals);
-#pragma unroll
-    for (int d = 0; d < W; ++d) {
-      code[d] = d < w ? src[d * 32 + lane] : kSrcSkip;
-      val[d] = d < w ? vals[d * 32 + lane] : 0.0;
-    }
-    const int* pf = reinterpret_cast<const int*>(p + g.pf);
-    pf_row = pf[lane];
-#pragma unroll
-    for (int m = 0; m < kMaxInbox; ++m) pf_mbox[m] = m < n_inbox ? pf[32 + m * 32 + lane] : -1;
-  }
-};
-
-// Slow path, kept out of line: poll a mailbox until it is solved. Returns its
-// bits, or kNotReady when the launch is aborting (watchdog or another warp).
-// Spins are added to the device status here, off the hot path.
+// Slow path, out of line: poll a mailbox until it is solved. Returns its bits,
+// or kNotReady when the launch aborts (watchdog or another warp's abort).
 __device__ __noinline__ unsigned long long poll_mailbox(const unsigned long long* p, int* abort_flag,
                                                         DeviceStatus* status, int spin_initial, int spin_max_ns,
                                                         unsigned long long deadline) {
@@ -174,22 +130,43 @@ __device__ __noinline__ unsigned long long poll_mailbox(const unsigned long long
   return u;
 }
 
+// One lane's slice fields, loaded one step ahead into registers.
+template <bool EXACT, int W>
+struct Rec {
+  int row, mbo, pf_row;
+  int pf_mbox[kMaxInbox];
+  double rdg, dg;
+  int src[W];
+  double val[W];
+
+  __device__ __forceinline__ void load(const unsigned char* p, const SliceGeom& g, int w, int lane, int M) {
+    row = reinterpret_cast<const int*>(p)[lane];
+    mbo = reinterpret_cast<const int*>(p + 128)[lane];
+    pf_row = reinterpret_cast<const int*>(p + 256)[lane];
+#pragma unroll
+    for (int m = 0; m < kMaxInbox; ++m) pf_mbox[m] = m < M ? reinterpret_cast<const int*>(p + g.pfm)[m * 32 + lane] : -1;
+    rdg = reinterpret_cast<const double*>(p + g.rdg)[lane];
+    if (EXACT) dg = reinterpret_cast<const double*>(p + g.dg)[lane];
+#pragma unroll
+    for (int d = 0; d < W; ++d) {
+      src[d] = d < w ? reinterpret_cast<const int*>(p + g.src)[d * 32 + lane] : kSrcSkip;
+      val[d] = d < w ? reinterpret_cast<const double*>(p + g.val)[d * 32 + lane] : 0.0;
+    }
+  }
+};
+
 template <bool EXACT>
 __device__ __forceinline__ double fold(double acc, double v, double xj) {
   if (EXACT) return __dadd_rn(acc, __dmul_rn(v, xj));
   return __fma_rn(v, xj, acc);
 }
 
-template <bool EXACT, int W>
+template <bool EXACT, int W, bool PROBE>
 __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* chunks = smem;
-  double* ring = reinterpret_cast<double*>(smem + kSmemChunks);
-  double* bring = reinterpret_cast<double*>(smem + kSmemChunks + kSmemRing);
-  unsigned long long* mring = reinterpret_cast<unsigned long long*>(smem + kSmemChunks + kSmemRing + kSmemB);
-  int* mslot = reinterpret_cast<int*>(smem + kSmemChunks + kSmemRing + kSmemB + kSmemInbox);
-  unsigned long long* bars =
-      reinterpret_cast<unsigned long long*>(smem + kSmemChunks + kSmemRing + kSmemB + kSmemInbox + kSmemSlot);
+  const unsigned sbase = smem_u32(smem);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + kSmemBars);
+  const int* mslot = reinterpret_cast<const int*>(smem + kSmemSlot);
   const int lane = threadIdx.x;
   const int M = a.n_inbox;
   if (lane == 0) {
@@ -199,13 +176,13 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
   __syncwarp();
   unsigned phase_bits = 0;  // parity to wait for, per buffer
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
-  auto poll = [&](int slot, bool& ok) {
+  bool alive = true;
+  auto poll = [&](int slot) {
     const unsigned long long u =
         poll_mailbox(a.mbox + kMboxStride * slot, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-    ok = ok && u != kNotReady;
+    if (u == kNotReady) alive = false;
     return as_f64(u);
   };
-  bool alive = true;
 
   while (alive) {
     int t = 0;
@@ -214,7 +191,7 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
     if (t >= a.n_tasks) break;
     const int c0 = a.task_chunk[t], c1 = a.task_chunk[t + 1];
     int issued_hi = c0 - 1, awaited_hi = c0 - 1;
-    auto buf_of = [&](int c) { return chunks + (size_t)((c - c0) % kChunkBuffers) * kChunkBytes; };
+    auto buf_of = [&](int c) { return smem + kSmemChunks + (size_t)((c - c0) % kChunkBuffers) * kChunkBytes; };
     auto issue = [&](int c) {
       issued_hi = c;
       if (lane == 0) {
@@ -235,7 +212,6 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
     };
     for (int c = c0; c < c1 && c < c0 + kChunkBuffers; ++c) issue(c);
 
-    double xprev = 0.0;
     int step = 0;
     Rec<EXACT, W> cur, nxt;
     int w_next = a.chunk_width[c0], steps_next = a.chunk_steps[c0];
@@ -245,96 +221,100 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
         w_next = a.chunk_width[c + 1];
         steps_next = a.chunk_steps[c + 1];
       }
-      const Geom g(w, M, EXACT);
+      const SliceGeom g(w, M, EXACT);
       await(c);
       const unsigned char* p = buf_of(c);
       cur.load(p, g, w, lane, M);
       for (int s = 0; s < steps; ++s, ++step) {
-        // next record: fixed offsets, issued before this step's dependencies
-        // (past the chunk's last slice it reads padding that is never used)
-        nxt.load(p + (s + 1) * g.sb, g, w, lane, M);
-        const bool probe = a.dbg && blockIdx.x == 0 && lane == 0 && step >= kProbeFirstStep &&
-                           step < kProbeFirstStep + kProbeSteps;
-        long long* stamp = probe ? a.dbg + 5 * (step - kProbeFirstStep) : nullptr;
-        if (probe) stamp[0] = clock64();
+        long long* stamp = nullptr;
+        if constexpr (PROBE) {
+          if (blockIdx.x == 0 && lane == 0 && step >= kProbeFirstStep && step < kProbeFirstStep + kProbeSteps)
+            stamp = a.dbg + 5 * (step - kProbeFirstStep);
+          if (stamp) stamp[0] = clock64();
+        }
         const int pslot = step % kPrefetch;
-        // the copies for this step were issued kPrefetch steps ago
-        if (!(a.flags & kProbeNoWait)) cp_async_wait<kPrefetch - 1>();
-        if (probe) stamp[1] = clock64();
-        // gather every dependency value branch-free (ring / register / inbox),
-        // flag the rare ones that must be polled from global memory
-        double xj[W];
+        // the b / inbox copies for this step were issued kPrefetch steps ago
+        cp_async_wait<kPrefetch - 1>();
+        // dependency values: one shared-memory load each, at baked offsets
+        double xv[W];
+#pragma unroll
+        for (int d = 0; d < W; ++d) xv[d] = lds_f64(sbase + (unsigned)max(cur.src[d], 0));
+        const double bi = lds_f64(sbase + kSmemB + (pslot * 32 + lane) * 8);
+        // next step's record (fixed offsets; past the chunk's end it reads
+        // padding that is never used)
+        nxt.load(p + (s + 1) * g.sb, g, w, lane, M);
+        if constexpr (PROBE) {
+          if (stamp) stamp[1] = clock64();
+        }
         unsigned slow = 0;
 #pragma unroll
         for (int d = 0; d < W; ++d) {
-          const int code = cur.code[d];
-          const double rv = ring[code >= 0 ? code : 0];
-          const int m = kSrcInbox0 - code;
-          const bool inbox = m >= 0 && m < kMaxInbox;
-          const unsigned long long iu = mring[(((inbox ? m : 0) * kPrefetch + pslot) * 32 + lane) * 2];
-          xj[d] = code >= 0 ? rv : (code == kSrcPrev ? xprev : as_f64(iu));
-          if ((inbox && iu == kNotReady) || (code <= kSrcDirect && code != kSrcSkip)) slow |= 1u << d;
+          const int sc = cur.src[d];
+          const bool direct = sc <= kSrcDirect;
+          const bool not_ready = sc >= 0 && (unsigned long long)__double_as_longlong(xv[d]) == kNotReady;
+          slow |= (direct || not_ready) ? (1u << d) : 0u;
         }
         if (__any_sync(0xffffffffu, slow != 0)) {
 #pragma unroll
           for (int d = 0; d < W; ++d) {
             if (slow & (1u << d)) {
-              const int code = cur.code[d];
-              const int m = kSrcInbox0 - code;
-              const int slot = code <= kSrcDirect ? kSrcDirect - code : mslot[(m * kPrefetch + pslot) * 32 + lane];
-              xj[d] = poll(slot, alive);
+              const int sc = cur.src[d];
+              const int slot = sc <= kSrcDirect ? kSrcDirect - sc : mslot[(sc - kSmemInbox) / 16];
+              xv[d] = poll(slot);
             }
           }
         }
-        const double bi = (a.flags & kProbeNoB) ? 1.0 : bring[pslot * 32 + lane];
         double acc = EXACT ? 0.0 : __dmul_rn(bi, cur.rdg);
 #pragma unroll
         for (int d = 0; d < W; ++d) {
-          const double folded = fold<EXACT>(acc, cur.val[d], xj[d]);
-          acc = (cur.code[d] != kSrcSkip && cur.code[d] != kSrcOverflow) ? folded : acc;
+          const double folded = fold<EXACT>(acc, cur.val[d], xv[d]);
+          acc = (cur.src[d] >= 0 || cur.src[d] <= kSrcDirect) ? folded : acc;
         }
         if constexpr (W == kInlineDeps) {
           // a row wider than kInlineDeps continues in the overflow list
-          if (cur.code[W - 1] == kSrcOverflow) {
+          if (cur.src[W - 1] == kSrcOverflow) {
             const long long packed = __double_as_longlong(cur.val[W - 1]);
             const long long start = packed >> 24, cnt = packed & 0xFFFFFF;
             for (long long o = start; o < start + cnt; ++o) {
               const int oc = __ldg(a.ovf_src + o);
               const double ov = __ldg(a.ovf_val + o);
-              double oj;
-              if (oc >= 0) oj = ring[oc];
-              else if (oc == kSrcPrev) oj = xprev;
-              else oj = poll(kSrcDirect - oc, alive);
+              double oj = oc >= 0 ? lds_f64(sbase + (unsigned)oc) : poll(kSrcDirect - oc);
               acc = fold<EXACT>(acc, ov, oj);
             }
           }
         }
-        if (probe) stamp[2] = clock64();
+        if constexpr (PROBE) {
+          if (stamp) stamp[2] = clock64();
+        }
         if (cur.row >= 0) {
           double xi = EXACT ? div_exact(__dsub_rn(bi, acc), cur.dg, cur.rdg) : acc;
           const unsigned long long bits = publishable(xi);
           xi = as_f64(bits);
-          ring[(step % kRingSteps) * 32 + lane] = xi;
-          xprev = xi;
-          if (!(a.flags & kProbeNoStoreX)) a.x[cur.row] = xi;
+          *reinterpret_cast<double*>(smem + ring_offset(step, lane)) = xi;
+          a.x[cur.row] = xi;
           if (cur.mbo >= 0) st_relaxed_u64(a.mbox + kMboxStride * cur.mbo, bits);
         }
-        // launch the copies for step + kPrefetch into the slots just consumed
+        // copies for step + kPrefetch into the slots just consumed
         if (cur.pf_row >= 0) {
-          if (!(a.flags & kProbeNoB)) cp_async8(bring + pslot * 32 + lane, a.b + cur.pf_row);
+          cp_async8(sbase + kSmemB + (pslot * 32 + lane) * 8, a.b + cur.pf_row);
 #pragma unroll
           for (int m = 0; m < kMaxInbox; ++m) {
             const int slot = cur.pf_mbox[m];
             if (slot >= 0) {
-              cp_async16_cg(mring + ((m * kPrefetch + pslot) * 32 + lane) * 2, a.mbox + kMboxStride * slot);
-              mslot[(m * kPrefetch + pslot) * 32 + lane] = slot;
+              const int idx = inbox_index(m, step, lane);
+              cp_async16_cg(sbase + kSmemInbox + idx * 16, a.mbox + kMboxStride * slot);
+              reinterpret_cast<int*>(smem + kSmemSlot)[idx] = slot;
             }
           }
         }
         cp_async_commit();
-        if (probe) stamp[3] = clock64();
+        if constexpr (PROBE) {
+          if (stamp) stamp[3] = clock64();
+        }
         __syncwarp();
-        if (probe) stamp[4] = clock64();
+        if constexpr (PROBE) {
+          if (stamp) stamp[4] = clock64();
+        }
         cur = nxt;
       }
       if (!__all_sync(0xffffffffu, alive)) alive = false;
@@ -351,23 +331,27 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
   cp_async_wait<0>();
 }
 
-template <bool EXACT, int W>
+template <bool EXACT, int W, bool PROBE>
 cudaError_t launch_variant(const ChainArgs& a, int blocks, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_chains<EXACT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_chains<EXACT, W, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_chains<EXACT, W><<<blocks, 32, kSmemTotal, s>>>(a);
+  k_chains<EXACT, W, PROBE><<<blocks, 32, kSmemTotal, s>>>(a);
   return cudaGetLastError();
 }
 
-template <bool EXACT>
+template <bool EXACT, bool PROBE>
 cudaError_t launch_width(int w, const ChainArgs& a, int blocks, cudaStream_t s) {
-  if (w <= 4) return launch_variant<EXACT, 4>(a, blocks, s);
-  if (w <= 8) return launch_variant<EXACT, 8>(a, blocks, s);
-  return launch_variant<EXACT, kInlineDeps>(a, blocks, s);
+  if (w <= 1) return launch_variant<EXACT, 1, PROBE>(a, blocks, s);
+  if (w <= 2) return launch_variant<EXACT, 2, PROBE>(a, blocks, s);
+  if (w <= 3) return launch_variant<EXACT, 3, PROBE>(a, blocks, s);
+  if (w <= 4) return launch_variant<EXACT, 4, PROBE>(a, blocks, s);
+  if (w <= 8) return launch_variant<EXACT, 8, PROBE>(a, blocks, s);
+  return launch_variant<EXACT, kInlineDeps, PROBE>(a, blocks, s);
 }
 
 }  // namespace
@@ -375,8 +359,7 @@ cudaError_t launch_width(int w, const ChainArgs& a, int blocks, cudaStream_t s) 
 int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   if (!chains.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "chains schedule not built");
   cudaError_t e;
-  if ((e = cudaMemsetAsync(chains.mbox, 0xFF, 16 * (size_t)std::max(chains.n_mbox, 1ll), s)) !=
-          cudaSuccess ||
+  if ((e = cudaMemsetAsync(chains.mbox, 0xFF, 16 * (size_t)std::max(chains.n_mbox, 1ll), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(chains.ticket, 0, sizeof(int), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
@@ -400,8 +383,8 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
-  a.flags = opt.probe_flags;
-  if (opt.probe_flags & kProbeClock) {
+  const bool probe = (opt.probe_flags & kProbeClock) != 0;
+  if (probe) {
     if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 5 * kProbeSteps) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, "probe buffer");
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 5 * kProbeSteps, s);
@@ -410,8 +393,9 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   // one warp per CTA, at most 2 CTAs per SM (shared-memory budget)
   const int blocks = std::max(1, std::min(chains.n_tasks, num_sms * 2));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  e = chains.exact ? launch_width<true>(chains.max_width, a, blocks, s)
-                   : launch_width<false>(chains.max_width, a, blocks, s);
+  const int w = chains.max_width;
+  if (chains.exact) e = probe ? launch_width<true, true>(w, a, blocks, s) : launch_width<true, false>(w, a, blocks, s);
+  else e = probe ? launch_width<false, true>(w, a, blocks, s) : launch_width<false, false>(w, a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;

@@ -67,7 +67,7 @@ def main():
         name, make = cases[key]
         l = make()
         if variants:
-            for flags in (CLOCK, NO_B | CLOCK, NO_STORE_X | CLOCK, NO_WAIT | NO_B | CLOCK, NO_B | NO_STORE_X | NO_WAIT):
+            for flags in (CLOCK, 0):
                 run(name, l, "chains", "fast", probe_flags=flags)
         else:
             for prec in ("fast", "exact"):
