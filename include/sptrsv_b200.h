@@ -44,8 +44,11 @@ enum { SPTRSV_PRECISION_EXACT = 0, SPTRSV_PRECISION_FAST = 1 };
 
 /* Which device executor runs the solve. ROWS: sync-free component pool over
  * a level-ordered ticket queue (paper Alg. 3). CHAINS: lane-chain lockstep
- * warps over contiguous row tasks. AUTO picks by the analysis statistics. */
-enum { SPTRSV_EXECUTOR_AUTO = 0, SPTRSV_EXECUTOR_ROWS = 1, SPTRSV_EXECUTOR_CHAINS = 2 };
+ * warps over contiguous row tasks. STENCIL: register-blocked wavefront for L
+ * with 2D five-point lower structure (detected; any coefficients). AUTO:
+ * STENCIL when the structure is detected, else CHAINS when most dependencies
+ * stay inside a warp task, else ROWS. */
+enum { SPTRSV_EXECUTOR_AUTO = 0, SPTRSV_EXECUTOR_ROWS = 1, SPTRSV_EXECUTOR_CHAINS = 2, SPTRSV_EXECUTOR_STENCIL = 3 };
 
 /* plan flags */
 enum {

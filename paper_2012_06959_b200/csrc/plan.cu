@@ -139,12 +139,26 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
 
   executor_used = SPTRSV_EXECUTOR_ROWS;
   if (!structure_only && opt.executor != SPTRSV_EXECUTOR_ROWS) {
-    rc = build_chains();
+    // host copy of the CSR structure for the schedulers
+    std::vector<int> h_rp(n + 1), h_ci(noff);
+    P_TRY(cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
+    if (noff) P_TRY(cudaMemcpy(h_ci.data(), ci, sizeof(int) * noff, cudaMemcpyDeviceToHost));
+    if (opt.executor == SPTRSV_EXECUTOR_AUTO || opt.executor == SPTRSV_EXECUTOR_STENCIL) {
+      rc = build_stencil(h_rp, h_ci);
+      if (rc != SPTRSV_OK) return rc;
+      if (stencil.ready) {
+        executor_used = SPTRSV_EXECUTOR_STENCIL;
+        return SPTRSV_OK;
+      }
+      if (opt.executor == SPTRSV_EXECUTOR_STENCIL)
+        return plan_fail(SPTRSV_E_UNSUPPORTED, "stencil executor requested but L is not 2D five-point lower structured");
+    }
+    rc = build_chains(h_rp, h_ci);
     if (rc != SPTRSV_OK) return rc;
     if (chains.ready && (opt.executor == SPTRSV_EXECUTOR_CHAINS || chains_preferred()))
       executor_used = SPTRSV_EXECUTOR_CHAINS;
     else if (opt.executor == SPTRSV_EXECUTOR_CHAINS)
-      return plan_fail(SPTRSV_E_UNSUPPORTED, "chains executor requested but the matrix has rows wider than its slice limit");
+      return plan_fail(SPTRSV_E_UNSUPPORTED, "chains schedule could not be built");
   }
   return SPTRSV_OK;
 }

@@ -7,6 +7,7 @@
 #include "../../include/sptrsv_b200.h"
 #include "common.cuh"
 #include "chains.hpp"
+#include "stencil.hpp"
 
 namespace sptrsv {
 
@@ -48,6 +49,7 @@ struct DevicePlan {
   int** lseg_dev = nullptr;
 
   ChainPlan chains;
+  StencilPlan stencil;
   long long* probe_buf = nullptr;  // diagnostics (probe_flags)
   int executor_used = SPTRSV_EXECUTOR_ROWS;
 
@@ -61,8 +63,10 @@ struct DevicePlan {
   int rows_grid(int mode) const;
   int solve_rows(const double* d_b, double* d_x, cudaStream_t s);
   int solve_chains(const double* d_b, double* d_x, cudaStream_t s);
-  int build_chains();
+  int build_chains(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
   bool chains_preferred() const;
+  int build_stencil(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
+  int solve_stencil(const double* d_b, double* d_x, cudaStream_t s);
   int solve_device(const double* d_b, double* d_x, cudaStream_t s);
   int finish(sptrsv_stats* st);
   void release();

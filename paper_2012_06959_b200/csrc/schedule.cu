@@ -298,18 +298,15 @@ static void build_schedule(const ScheduleInput& in, ScheduleOutput& out) {
   out.task_chunk.push_back((int)out.chunk_steps.size());
 }
 
-int DevicePlan::build_chains() {
+int DevicePlan::build_chains(const std::vector<int>& h_rp, const std::vector<int>& h_ci) {
   auto t0 = std::chrono::steady_clock::now();
   chains.release();
   chains.exact = opt.precision != SPTRSV_PRECISION_FAST;
   chains.lanes = opt.chain_lanes;
-  // host copies of the device CSR (already built by the transpose)
-  std::vector<int> h_rp(n + 1), h_ci(noff);
+  // host copies of the device CSR values (the structure is passed in)
   std::vector<double> h_val(noff), h_dg(chains.exact ? n : 0), h_rdg(n);
   cudaError_t e;
-  if ((e = cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (noff && (e = cudaMemcpy(h_ci.data(), ci, sizeof(int) * noff, cudaMemcpyDeviceToHost)) != cudaSuccess) ||
-      (noff && (e = cudaMemcpy(h_val.data(), chains.exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
+  if ((noff && (e = cudaMemcpy(h_val.data(), chains.exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
                    cudaSuccess) ||
       (chains.exact && (e = cudaMemcpy(h_dg.data(), dg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess) ||
       (e = cudaMemcpy(h_rdg.data(), rdg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)

@@ -1,0 +1,468 @@
+// Register-blocked wavefront executor for 2D five-point lower structure.
+//
+// Structure: row i = y*nx + x stores (i, i-nx) iff y > 0 and (i, i-1) iff
+// x > 0 (plus the diagonal), any coefficients — detected from the CSR at plan
+// time. The dependency DAG is then the nx-by-ny grid wavefront: 8191 levels
+// for 4096 x 4096.
+//
+// Layout of the work: a task (one warp) owns a band of kStBand = 64 grid
+// rows; lane l owns rows 2l, 2l+1 of the band and, at lockstep step s, solves
+// the 2 x kStC block of columns [jC, jC + C) with j = s - l. Everything a
+// block needs from outside arrives in registers: the row above from lane l-1's
+// block of the previous step by one __shfl_up_sync, the left neighbours from
+// this lane's previous block. Inside the block the wavefront is resolved in
+// registers (critical path: one FMA per element along a row). Bands depend on
+// the band above through value-is-flag mailboxes (the band's bottom grid row),
+// prefetched kStPrefetch steps ahead by lane 0 with cp.async.cg; a stale
+// prefetch falls back to polling and then re-synchronises the lag so later
+// prefetches land.
+//
+// Data: coefficients are repacked at plan time into a per-task stream in
+// (step, field, element-pair, lane) order and moved to shared memory by TMA
+// bulk copies (cp.async.bulk + mbarrier), kStBuffers steps ahead; b is
+// gathered with cp.async kStPrefetch steps ahead; x is written with 16-byte
+// stores. No column indices are read at all: per element the solve moves
+// 24 B of coefficients (fast) + 8 B b + 8 B x.
+//
+// Arithmetic: fast: x = wl*left + (wu*up + b/d) with pre-scaled coefficients;
+// exact: s = 0 + wu*up, s = s + wl*left, x = (b - s)/d — the serial oracle's
+// order (ascending columns), with absent boundary terms contributing +0, which
+// leaves every partial sum unchanged, so the result stays bit-identical.
+#include <vector>
+#include <chrono>
+#include <cstring>
+#include "plan.hpp"
+#include "kernels.cuh"
+
+namespace sptrsv {
+
+int plan_fail(int code, const char* msg);
+
+namespace {
+
+struct StArgs {
+  const unsigned char* stream;
+  unsigned long long* mbox;
+  int* ticket;
+  const double* b;
+  double* x;
+  DeviceStatus* status;
+  int* abort_flag;
+  unsigned long long timeout_ns;
+  int spin_initial, spin_max_ns;
+  int nx, ny, n_tasks, steps;
+};
+
+constexpr int kStBlkPairs = kStBlock / 2;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, int* abort_flag, DeviceStatus* status,
+                                                   int spin_initial, int spin_max_ns, unsigned long long deadline) {
+  unsigned long long u = ld_relaxed_u64(p);
+  int polls = 0, sleep_ns = 32;
+  while (u == kNotReady) {
+    ++polls;
+    if (polls > spin_initial) {
+      if ((polls & 63) == 0) {
+        if (ld_relaxed_s32(abort_flag)) break;
+        if (deadline && globaltimer_ns() > deadline) {
+          atomicExch(&status->code, 5);
+          atomicExch(abort_flag, 1);
+          break;
+        }
+      }
+      __nanosleep(sleep_ns);
+      if (sleep_ns < spin_max_ns) sleep_ns <<= 1;
+    }
+    u = ld_relaxed_u64(p);
+  }
+  if (polls) atomicAdd(&status->spins, (unsigned long long)polls);
+  return u;
+}
+
+template <bool EXACT>
+struct StSmem {
+  static constexpr int kStep = st_step_bytes(EXACT);
+  static constexpr int kStream = 0;
+  static constexpr int kB = kStBuffers * kStep;                                   // b ring
+  static constexpr int kInbox = kB + kStPrefetch * kStLanes * kStBlock * 8;       // lane 0's mailbox copies
+  static constexpr int kBars = kInbox + kStPrefetch * kStC * 8;
+  static constexpr int kTotal = kBars + 8 * kStBuffers;
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
+  using S = StSmem<EXACT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
+  double* bring = reinterpret_cast<double*>(smem + S::kB);
+  double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
+  const int lane = threadIdx.x;
+  constexpr int NF = st_fields(EXACT);
+  if (lane == 0) {
+    for (int k = 0; k < kStBuffers; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase_bits = 0;
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  const int nblk = a.nx / kStC;
+  bool alive = true;
+
+  while (alive) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= a.n_tasks) break;
+    const int y0 = t * kStBand + kStR * lane;  // first grid row of this lane
+    const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+    const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
+    unsigned long long* below = a.mbox + (size_t)t * a.nx;
+    const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
+
+    auto issue = [&](int s) {
+      if (lane == 0) {
+        unsigned long long* bar = &bars[s % kStBuffers];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, S::kStep);
+        bulk_g2s(smem + S::kStream + (s % kStBuffers) * S::kStep, tstream + (size_t)s * S::kStep, S::kStep, bar);
+      }
+    };
+    auto await = [&](int s) {
+      const int k = s % kStBuffers;
+      const unsigned ph = (phase_bits >> k) & 1u;
+      while (!mbar_try_wait(&bars[k], ph)) {
+      }
+      phase_bits ^= 1u << k;
+    };
+    // b block and (lane 0) the band-above row for step s, into ring slot s % P
+    auto prefetch = [&](int s) {
+      const int j = s - lane;
+      if (j >= 0 && j < nblk) {
+        double* dst = bring + ((s % kStPrefetch) * kStLanes + lane) * kStBlock;
+#pragma unroll
+        for (int r = 0; r < kStR; ++r) {
+          if (y0 + r < a.ny) {
+            const double* src = a.b + (size_t)(y0 + r) * a.nx + j * kStC;
+#pragma unroll
+            for (int c = 0; c < kStC; c += 2) cp_async16_ca(dst + r * kStC + c, src + c);
+          }
+        }
+        if (lane == 0 && above) {
+#pragma unroll
+          for (int c = 0; c < kStC; c += 2)
+            cp_async16_cg(inbox + (s % kStPrefetch) * kStC + c, above + j * kStC + c);
+        }
+      }
+      cp_async_commit();
+    };
+
+    const int steps = a.steps;
+    for (int s = 0; s < steps && s < kStBuffers; ++s) issue(s);
+    for (int s = 0; s < kStPrefetch; ++s) prefetch(s);
+
+    double xleft[kStR];
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
+    double bottom[kStC];
+#pragma unroll
+    for (int c = 0; c < kStC; ++c) bottom[c] = 0.0;
+    bool resync = false;
+
+    for (int s = 0; s < steps; ++s) {
+      const int j = s - lane;
+      const bool active = j >= 0 && j < nblk;
+      // row above: lane l-1's bottom row of the previous step
+      double top[kStC];
+#pragma unroll
+      for (int c = 0; c < kStC; ++c) top[c] = __shfl_up_sync(0xffffffffu, bottom[c], 1);
+      await(s);
+      cp_async_wait<kStPrefetch - 1>();
+      const int slot = s % kStPrefetch;
+      if (lane == 0) {
+        if (above && active) {
+          bool stale = false;
+#pragma unroll
+          for (int c = 0; c < kStC; ++c) {
+            top[c] = inbox[slot * kStC + c];
+            if ((unsigned long long)__double_as_longlong(top[c]) == kNotReady) {
+              const unsigned long long u =
+                  st_poll(above + j * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+              if (u == kNotReady) alive = false;
+              top[c] = as_f64(u);
+              stale = true;
+            }
+          }
+          resync = stale;
+        } else {
+#pragma unroll
+          for (int c = 0; c < kStC; ++c) top[c] = 0.0;  // grid row 0: no entry above
+        }
+      }
+      // coefficients of this lane's block: field-major, element pairs, lanes
+      const double2* cs = reinterpret_cast<const double2*>(smem + S::kStream + (s % kStBuffers) * S::kStep);
+      double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock];
+#pragma unroll
+      for (int k = 0; k < kStBlkPairs; ++k) {
+        const double2 u = cs[(0 * kStBlkPairs + k) * kStLanes + lane];
+        const double2 l = cs[(1 * kStBlkPairs + k) * kStLanes + lane];
+        wu[2 * k] = u.x, wu[2 * k + 1] = u.y;
+        wl[2 * k] = l.x, wl[2 * k + 1] = l.y;
+        if (EXACT) {
+          const double2 d = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
+          const double2 r = cs[(3 * kStBlkPairs + k) * kStLanes + lane];
+          dd[2 * k] = d.x, dd[2 * k + 1] = d.y;
+          rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+        } else {
+          const double2 r = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
+          rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+        }
+      }
+      const double2* bs = reinterpret_cast<const double2*>(bring + (slot * kStLanes + lane) * kStBlock);
+      double bv[kStBlock];
+#pragma unroll
+      for (int k = 0; k < kStBlkPairs; ++k) {
+        const double2 v = bs[k];
+        bv[2 * k] = v.x, bv[2 * k + 1] = v.y;
+      }
+      // solve the block: row by row, columns left to right
+      double xb[kStR][kStC];
+#pragma unroll
+      for (int r = 0; r < kStR; ++r) {
+#pragma unroll
+        for (int c = 0; c < kStC; ++c) {
+          const int e = r * kStC + c;
+          const double up = r == 0 ? top[c] : xb[r - 1][c];
+          const double left = c == 0 ? xleft[r] : xb[r][c - 1];
+          double xi;
+          if (EXACT) {
+            double acc = __dadd_rn(0.0, __dmul_rn(wu[e], up));
+            acc = __dadd_rn(acc, __dmul_rn(wl[e], left));
+            xi = div_exact(__dsub_rn(bv[e], acc), dd[e], rd[e]);
+          } else {
+            xi = __fma_rn(wl[e], left, __fma_rn(wu[e], up, __dmul_rn(bv[e], rd[e])));
+          }
+          xb[r][c] = as_f64(publishable(xi));
+        }
+      }
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < kStR; ++r) {
+          xleft[r] = xb[r][kStC - 1];
+          if (y0 + r < a.ny) {
+            double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
+#pragma unroll
+            for (int c = 0; c < kStC; c += 2) dst[c / 2] = make_double2(xb[r][c], xb[r][c + 1]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kStC; ++c) bottom[c] = xb[kStR - 1][c];
+        if (publish) {
+#pragma unroll
+          for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, (unsigned long long)__double_as_longlong(bottom[c]));
+        }
+      }
+      // a stale inbox means this band caught up with the band above: fall
+      // back kStPrefetch steps so the copies issued from now on land ready
+      if (__any_sync(0xffffffffu, resync) && lane == 0 && above) {
+        const int jn = s + kStPrefetch;
+        if (jn < nblk) {
+#pragma unroll
+          for (int c = 0; c < kStC; ++c) {
+            const unsigned long long u =
+                st_poll(above + jn * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+            if (u == kNotReady) alive = false;
+          }
+        }
+        resync = false;
+      }
+      prefetch(s + kStPrefetch);
+      __syncwarp();
+      if (s + kStBuffers < steps) issue(s + kStBuffers);
+      if (!__all_sync(0xffffffffu, alive)) {
+        alive = false;
+        // drain the bulk copies in flight into this CTA's shared memory
+        for (int q = s + 1; q < steps && q < s + 1 + kStBuffers; ++q) await(q);
+        break;
+      }
+    }
+    cp_async_wait<0>();
+  }
+  cp_async_wait<0>();
+}
+
+template <bool EXACT>
+cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_stencil2d<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, StSmem<EXACT>::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_stencil2d<EXACT><<<blocks, 32, StSmem<EXACT>::kTotal, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Detect the 2D five-point lower structure on the host CSR; returns nx or 0.
+static int detect_stencil2d(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
+  if (n < 4) return 0;
+  long long nx = 0;
+  for (long long i = 1; i < n && !nx; ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k)
+      if (i - ci[k] > 1) {
+        nx = i - ci[k];
+        break;
+      }
+  if (nx < 2 || nx % kStC != 0 || n % nx != 0 || nx > (1 << 28)) return 0;
+  for (long long i = 0; i < n; ++i) {
+    const long long x = i % nx, y = i / nx;
+    int k = rp[i];
+    if (y > 0) {
+      if (k >= rp[i + 1] || ci[k] != i - nx) return 0;
+      ++k;
+    }
+    if (x > 0) {
+      if (k >= rp[i + 1] || ci[k] != i - 1) return 0;
+      ++k;
+    }
+    if (k != rp[i + 1]) return 0;
+  }
+  return (int)nx;
+}
+
+int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<int>& h_ci) {
+  auto t0 = std::chrono::steady_clock::now();
+  stencil.release();
+  const int nx = detect_stencil2d(n, h_rp, h_ci);
+  if (!nx) return SPTRSV_OK;
+  const bool exact = opt.precision != SPTRSV_PRECISION_FAST;
+  stencil.exact = exact;
+  stencil.nx = nx;
+  stencil.ny = (int)(n / nx);
+  stencil.n_tasks = (stencil.ny + kStBand - 1) / kStBand;
+  stencil.steps_per_task = nx / kStC + kStLanes - 1;
+  const int NF = st_fields(exact);
+  const size_t step_bytes = st_step_bytes(exact);
+  const size_t bytes = step_bytes * stencil.steps_per_task * stencil.n_tasks;
+  // coefficients (host copies of the device CSR values)
+  std::vector<double> h_val(noff), h_dg(n), h_rdg(n);
+  cudaError_t e;
+  if ((noff && (e = cudaMemcpy(h_val.data(), exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
+                   cudaSuccess) ||
+      (e = cudaMemcpy(h_dg.data(), dg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(h_rdg.data(), rdg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  std::vector<double> st(bytes / 8, 0.0);
+  const int nblk = nx / kStC;
+  const int pairs = kStBlock / 2;
+  for (int t = 0; t < stencil.n_tasks; ++t) {
+    for (int s = 0; s < stencil.steps_per_task; ++s) {
+      double* stepbuf = st.data() + ((size_t)t * stencil.steps_per_task + s) * (step_bytes / 8);
+      for (int l = 0; l < kStLanes; ++l) {
+        const int j = s - l;
+        if (j < 0 || j >= nblk) continue;
+        for (int r = 0; r < kStR; ++r) {
+          const long long y = (long long)t * kStBand + kStR * l + r;
+          if (y >= stencil.ny) continue;
+          for (int c = 0; c < kStC; ++c) {
+            const long long i = y * nx + (long long)j * kStC + c;
+            const int e_ = r * kStC + c;
+            const int k = e_ / 2, half = e_ % 2;
+            double fu = 0.0, fl = 0.0;
+            int kk = h_rp[i];
+            if (y > 0) fu = h_val[kk++];
+            if (j * kStC + c > 0) fl = h_val[kk];
+            double f[4];
+            if (exact) {
+              f[0] = fu, f[1] = fl, f[2] = h_dg[i], f[3] = h_rdg[i];
+            } else {
+              f[0] = fu, f[1] = fl, f[2] = h_rdg[i];
+            }
+            for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
+          }
+        }
+      }
+    }
+  }
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  if ((e = al((void**)&stencil.stream, bytes)) != cudaSuccess ||
+      (e = al((void**)&stencil.mbox, sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
+      (e = al((void**)&stencil.ticket, sizeof(int))) != cudaSuccess ||
+      (e = cudaMemcpy(stencil.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  stencil.stream_bytes = (long long)bytes;
+  stencil.ready = true;
+  stencil.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
+  if (!stencil.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 2D five-point lower structured");
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(stencil.mbox, 0xFF, sizeof(unsigned long long) * (size_t)stencil.n_tasks * stencil.nx, s)) !=
+          cudaSuccess ||
+      (e = cudaMemsetAsync(stencil.ticket, 0, sizeof(int), s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  StArgs a{};
+  a.stream = stencil.stream;
+  a.mbox = stencil.mbox;
+  a.ticket = stencil.ticket;
+  a.b = d_b;
+  a.x = d_x;
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.spin_initial = opt.spin_initial;
+  a.spin_max_ns = opt.spin_max_ns;
+  a.nx = stencil.nx;
+  a.ny = stencil.ny;
+  a.n_tasks = stencil.n_tasks;
+  a.steps = stencil.steps_per_task;
+  const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
+  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  launches = 1;
+  return SPTRSV_OK;
+}
+
+}  // namespace sptrsv

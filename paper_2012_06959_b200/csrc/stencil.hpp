@@ -1,0 +1,52 @@
+// Register-blocked wavefront executor for 2D five-point lower-triangular
+// structure ("stencil2d"). Selected automatically when every row i = y*nx + x
+// of L stores exactly the entries (i, i-nx) when y > 0 and (i, i-1) when x > 0
+// besides its diagonal — the lower triangle of a 5-point operator on an
+// nx-by-ny grid in natural order, with ARBITRARY coefficients. Design in
+// stencil.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sptrsv {
+
+// Block of one lane per lockstep step: kStR grid rows x kStC grid columns.
+constexpr int kStR = 2;
+constexpr int kStC = 4;
+constexpr int kStLanes = 32;
+constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one warp)
+constexpr int kStBlock = kStR * kStC;     // elements per lane per step
+constexpr int kStBuffers = 8;             // stream steps in flight per warp
+constexpr int kStPrefetch = 8;            // b / inbox prefetch distance (steps)
+
+// Per step, per lane: kStBlock elements; per element NF doubles:
+//   fast : wu = -L[i,i-nx]/d, wl = -L[i,i-1]/d, rdg = 1/d
+//   exact: wu = L[i,i-nx],   wl = L[i,i-1],    d, rdg
+// stored field-major, then element pairs, then lanes, so each lane reads a
+// pair of doubles with one conflict-free 16-byte shared load.
+__host__ __device__ constexpr int st_fields(bool exact) { return exact ? 4 : 3; }
+__host__ __device__ constexpr int st_step_bytes(bool exact) { return st_fields(exact) * kStBlock * kStLanes * 8; }
+
+struct StencilPlan {
+  bool ready = false;
+  bool exact = true;
+  int nx = 0, ny = 0;
+  int n_tasks = 0;
+  int steps_per_task = 0;  // nx / kStC + kStLanes - 1
+  long long stream_bytes = 0;
+  double build_ms = 0.0;
+  unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
+  unsigned long long* mbox = nullptr;  // [n_tasks][nx] bottom grid row of each task (value-is-flag)
+  int* ticket = nullptr;
+  void release() {
+    void* ptrs[] = {stream, mbox, ticket};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    stream = nullptr;
+    mbox = nullptr;
+    ticket = nullptr;
+    ready = false;
+  }
+};
+
+}  // namespace sptrsv

@@ -180,3 +180,46 @@ def test_device_resident_solve_matches_host_path():
     torch.cuda.synchronize()
     x_host, _ = plan.solve(b)
     assert dx.cpu().numpy().tobytes() == x_host.tobytes()
+
+
+def _random_coefficients(l, seed):
+    """Same structure, random off-diagonals in [-1, 1], dominant diagonal."""
+    rng = np.random.default_rng(seed)
+    vals = l.values.copy()
+    cols = l.entry_columns()
+    off = l.row_idx != cols
+    vals[off] = rng.uniform(-1.0, 1.0, off.sum())
+    dom = 1.0 + np.bincount(l.row_idx[off], weights=np.abs(vals[off]), minlength=l.n)
+    vals[~off] = np.where(rng.random(l.n) < 0.5, -1.0, 1.0) * dom
+    return sp.CscMatrix(n=l.n, col_ptr=l.col_ptr, row_idx=l.row_idx, values=vals)
+
+
+@pytest.mark.parametrize("shape", [(4, 1), (8, 3), (64, 64), (128, 65), (256, 200), (1024, 130)])
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_stencil_executor_matches_oracle(shape, precision):
+    nx, ny = shape
+    l = _random_coefficients(synth.lap2d(nx, ny), nx * 1000 + ny)
+    b = np.random.default_rng(ny).uniform(-1.0, 1.0, l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="auto")
+    assert plan.info()["executor"] == "stencil"
+    for _ in range(2):  # repeat solves reuse the mailboxes
+        x, _ = plan.solve(b)
+        if precision == "exact":
+            assert x.tobytes() == ref.tobytes()
+        else:
+            assert sp.compare_solutions(x, ref, FAST_TOL).within_tol
+    plan.close()
+
+
+def test_stencil_not_chosen_for_other_structures():
+    l = synth.lap2d(30, 10)  # nx not a multiple of the column block: general executors
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="auto")
+    assert plan.info()["executor"] != "stencil"
+    plan.close()
+    with pytest.raises(sp.errors.SptrsvError if hasattr(sp, "errors") else Exception):
+        _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="stencil")
+    l3 = synth.lap3d(8)
+    plan = _native.NativePlan(l3.col_ptr, l3.row_idx, l3.values, l3.n, executor="auto")
+    assert plan.info()["executor"] != "stencil"
+    plan.close()

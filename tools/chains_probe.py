@@ -71,6 +71,7 @@ def main():
                 run(name, l, "chains", "fast", probe_flags=flags)
         else:
             for prec in ("fast", "exact"):
+                run(name, l, "stencil", prec)
                 run(name, l, "chains", prec)
             run(name, l, "rows", "fast", reps=2)
 
