@@ -194,7 +194,7 @@ def _random_coefficients(l, seed):
     return sp.CscMatrix(n=l.n, col_ptr=l.col_ptr, row_idx=l.row_idx, values=vals)
 
 
-@pytest.mark.parametrize("shape", [(4, 1), (8, 3), (64, 64), (128, 65), (256, 200), (1024, 130)])
+@pytest.mark.parametrize("shape", [(4, 2), (8, 3), (64, 64), (128, 65), (256, 200), (1024, 130)])
 @pytest.mark.parametrize("precision", ["exact", "fast"])
 def test_stencil_executor_matches_oracle(shape, precision):
     nx, ny = shape
