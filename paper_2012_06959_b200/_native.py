@@ -172,7 +172,7 @@ class NativePlan:
     """A device-resident plan for one matrix (C handle ``sptrsv_plan*``)."""
 
     def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
-                 timeout=60.0, spin_initial=16, spin_max_ns=512, structure_only=False, chain_lanes=32,
+                 timeout=60.0, spin_initial=1024, spin_max_ns=64, structure_only=False, chain_lanes=32,
                  probe_flags=0):
         lib = require_gpu()
         self._lib = lib

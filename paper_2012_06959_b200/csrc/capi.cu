@@ -232,8 +232,8 @@ void sptrsv_default_options(sptrsv_options* opt) {
   opt->executor = SPTRSV_EXECUTOR_AUTO;
   opt->device = 0;
   opt->timeout_s = 60.0;
-  opt->spin_initial = 16;
-  opt->spin_max_ns = 512;
+  opt->spin_initial = 1024;  // Backoff(16, 512) of the reference: 16 x 64 device polls, then sleeps up to 512/8 ns
+  opt->spin_max_ns = 64;
   opt->chain_lanes = 32;
 }
 

@@ -296,10 +296,11 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
         }
       }
       // a stale inbox means this band caught up with the band above: fall
-      // back kStPrefetch steps so the copies issued from now on land ready
+      // back until the row above is ready kStPrefetch + kStResync blocks
+      // ahead, so the copies issued from now on land ready with margin
       if (__any_sync(0xffffffffu, resync) && lane == 0 && above) {
-        const int jn = s + kStPrefetch;
-        if (jn < nblk) {
+        const int jn = min(s + kStPrefetch + kStResync, nblk - 1);
+        {
 #pragma unroll
           for (int c = 0; c < kStC; ++c) {
             const unsigned long long u =

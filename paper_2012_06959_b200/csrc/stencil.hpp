@@ -18,6 +18,7 @@ constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one warp)
 constexpr int kStBlock = kStR * kStC;     // elements per lane per step
 constexpr int kStBuffers = 8;             // stream steps in flight per warp
 constexpr int kStPrefetch = 8;            // b / inbox prefetch distance (steps)
+constexpr int kStResync = 8;              // extra lag a band takes after catching up with the band above
 
 // Per step, per lane: kStBlock elements; per element NF doubles:
 //   fast : wu = -L[i,i-nx]/d, wl = -L[i,i-1]/d, rdg = 1/d

@@ -268,8 +268,8 @@ def _run(l: CscMatrix, b, plan: PartitionPlan, cfg: SolverConfig, expected: Engi
         executor=cfg.executor,
         device=cfg.device,
         timeout=cfg.timeout,
-        spin_initial=cfg.spin_backoff.initial_pause,
-        spin_max_ns=cfg.spin_backoff.max_pause,
+        spin_initial=64 * cfg.spin_backoff.initial_pause,
+        spin_max_ns=max(16, cfg.spin_backoff.max_pause // 8),
     )
     setup = time.perf_counter() - ts
     ts = time.perf_counter()

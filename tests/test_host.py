@@ -144,7 +144,7 @@ def test_library_loads_and_exports_every_header_symbol():
         assert hasattr(lib, s), s
     assert lib.sptrsv_abi_version() == 1
     opt = _native.default_options()
-    assert opt.timeout_s == 60.0 and opt.spin_initial == 16 and opt.spin_max_ns == 512
+    assert opt.timeout_s == 60.0 and opt.spin_initial == 1024 and opt.spin_max_ns == 64
     assert ctypes.sizeof(_native.Options) == lib.sptrsv_sizeof_options()
     assert ctypes.sizeof(_native.Stats) == lib.sptrsv_sizeof_stats()
 
