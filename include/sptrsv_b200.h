@@ -139,6 +139,25 @@ int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats);
 
 int sptrsv_plan_destroy(sptrsv_plan* plan);
 
+/* ---- PE partitions: the read-only inter-PE layer (solve_partitioned,
+ * engine.py:438-582; Alg. 3). owner[n] is PartitionPlan.owner_arr
+ * (partition.py:30-64). Each PE publishes its components' x only into its own
+ * segment; other PEs read it with one-sided loads (no remote writes, no
+ * collectives inside the solve).
+ *   my_pe < 0 : every PE on this plan's device (one launch serves them all);
+ *               solves gather x from the segments.
+ *   my_pe >= 0: this process is PE my_pe only (one process per GPU); peers'
+ *               segments are attached with sptrsv_plan_import_segment (CUDA
+ *               IPC) or sptrsv_plan_set_peer_segment (same-process peer
+ *               pointer). The caller must order consecutive solves across
+ *               processes (a barrier) because each solve resets the segments. */
+int sptrsv_plan_set_partition(sptrsv_plan* plan, const int32_t* owner, int32_t n_pes, int32_t my_pe);
+int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* ipc_handle_out);
+int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* ipc_handle);
+int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr);
+void* sptrsv_plan_segment(const sptrsv_plan* plan); /* this process's first segment (device pointer) */
+int sptrsv_ipc_handle_size(void);
+
 /* Diagnostics: copy up to `count` probe timestamps (clock64) recorded by the
  * last solve when options.probe_flags asked for them. */
 int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count);

@@ -129,6 +129,18 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_plan_get_info.restype = C.c_int
     lib.sptrsv_plan_probe_read.argtypes = [C.c_void_p, _P64, C.c_int32]
     lib.sptrsv_plan_probe_read.restype = C.c_int
+    lib.sptrsv_plan_set_partition.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int32, C.c_int32]
+    lib.sptrsv_plan_set_partition.restype = C.c_int
+    lib.sptrsv_plan_export_segment.argtypes = [C.c_void_p, C.c_void_p]
+    lib.sptrsv_plan_export_segment.restype = C.c_int
+    lib.sptrsv_plan_import_segment.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    lib.sptrsv_plan_import_segment.restype = C.c_int
+    lib.sptrsv_plan_set_peer_segment.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+    lib.sptrsv_plan_set_peer_segment.restype = C.c_int
+    lib.sptrsv_plan_segment.argtypes = [C.c_void_p]
+    lib.sptrsv_plan_segment.restype = C.c_void_p
+    lib.sptrsv_ipc_handle_size.argtypes = []
+    lib.sptrsv_ipc_handle_size.restype = C.c_int
 
 
 def load_library() -> C.CDLL:
@@ -213,6 +225,30 @@ class NativePlan:
         rc = self._lib.sptrsv_plan_get_info(self._h, C.byref(inf))
         raise_for_status(rc, _err(self._lib))
         return inf.as_dict()
+
+    # --- PE partitions (read-only inter-PE layer) -------------------------
+    def set_partition(self, owner, n_pes: int, my_pe: int = -1) -> None:
+        """Own components per ``owner`` (PartitionPlan.owner_arr); my_pe < 0: all PEs on this device."""
+        own = np.ascontiguousarray(owner, dtype=np.int32)
+        if own.shape != (self.n,):
+            raise ValueError(f"owner has shape {own.shape}, need ({self.n},)")
+        rc = self._lib.sptrsv_plan_set_partition(self._h, own.ctypes.data_as(C.POINTER(C.c_int32)), int(n_pes),
+                                                 int(my_pe))
+        raise_for_status(rc, _err(self._lib))
+
+    def export_segment(self) -> bytes:
+        buf = C.create_string_buffer(self._lib.sptrsv_ipc_handle_size())
+        rc = self._lib.sptrsv_plan_export_segment(self._h, buf)
+        raise_for_status(rc, _err(self._lib))
+        return buf.raw
+
+    def import_segment(self, pe: int, handle: bytes) -> None:
+        buf = C.create_string_buffer(bytes(handle), len(handle))
+        rc = self._lib.sptrsv_plan_import_segment(self._h, int(pe), buf)
+        raise_for_status(rc, _err(self._lib))
+
+    def segment_ptr(self) -> int:
+        return int(self._lib.sptrsv_plan_segment(self._h) or 0)
 
     def probe_stamps(self) -> np.ndarray:
         out = np.zeros(5 * 64, dtype=np.int64)

@@ -54,6 +54,7 @@ void DevicePlan::release() {
     if (p) cudaFree(p);
   chains.release();
   stencil.release();
+  release_partition();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (evk0) cudaEventDestroy(evk0);
@@ -185,7 +186,8 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   if (structure_only) return fail(SPTRSV_E_ARGUMENT, "plan was created structure-only; it cannot solve");
   int rc;
   CUDA_TRY(cudaEventRecord(ev0, s));
-  if (executor_used == SPTRSV_EXECUTOR_STENCIL) rc = solve_stencil(d_b, d_x, s);
+  if (seg_table) rc = solve_partitioned_rows(d_b, d_x, s);
+  else if (executor_used == SPTRSV_EXECUTOR_STENCIL) rc = solve_stencil(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
   else rc = solve_rows(d_b, d_x, s);
   if (rc != SPTRSV_OK) return rc;

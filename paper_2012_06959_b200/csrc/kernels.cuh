@@ -44,10 +44,15 @@ struct RowsArgs {
   unsigned long long* const* xseg;
   int* const* lseg;
   const unsigned char* owner;  // owner PE of each component, nullptr when n_pes == 1
-  int my_pe;
+  // PEs served by this launch: block b works for PE pe_base + b % n_pe_local
+  // (one PE per GPU in a multi-process run; all PEs when they share a device)
+  int pe_base;
+  int n_pe_local;
+  int my_pe;                // set per block by the kernel
+  const long long* pe_order_off;  // [n_pe_local + 1] slices of `order` per PE; nullptr: one PE, all of it
   const int* order;         // ticket slot -> row (topological order); -1 = padding
   long long order_len;      // number of slots (multiple of 32 when padded)
-  int* ticket;              // pool counter, zero at launch
+  int* ticket;              // pool counter(s), one per local PE, zero at launch
   DeviceStatus* status;
   int* abort_flag;
   unsigned long long timeout_ns;   // watchdog per thread from its first poll; 0 = none

@@ -1,0 +1,228 @@
+// PE partitions: the read-only inter-PE layer (paper Alg. 3, PAPER.md:339-399;
+// reference solve_partitioned, engine.py:438-582).
+//
+// Each PE owns the components of PartitionPlan.owner_arr and publishes their x
+// only into its own segment (a full-length value-is-flag array in its HBM);
+// every other PE reads that segment with one-sided loads and never writes it.
+// Two deployments share this code:
+//   * all PEs on one device (virtual PEs, one process): every segment is local,
+//     one launch serves all PEs (block b works for PE b % n_pes) so all
+//     persistent warps are co-resident;
+//   * one PE per GPU (one process per GPU): the PE's own segment is local, the
+//     others are peer mappings of other processes' segments opened from CUDA
+//     IPC handles, read over NVLink/NVSwitch with .sys-scope relaxed loads.
+// Inside the solve there is no collective and no remote write; scattering b
+// and gathering x around it is the caller's (NCCL in bench.py).
+#include <vector>
+#include <algorithm>
+#include <cstring>
+#include "plan.hpp"
+#include "kernels.cuh"
+#include "../../include/sptrsv_b200.h"
+
+namespace sptrsv {
+
+int plan_fail(int code, const char* msg);
+
+namespace {
+
+// x[i] = segment of owner(i) at i, for the PEs of this process.
+__global__ void k_gather_owned(unsigned long long* const* segs, const unsigned char* owner, int pe_base, int n_local,
+                               long long n, double* x) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int p = owner[i];
+    if (p >= pe_base && p < pe_base + n_local) x[i] = __longlong_as_double((long long)segs[p][i]);
+  }
+}
+
+}  // namespace
+
+void DevicePlan::release_partition() {
+  for (auto* s : local_segs) cudaFree(s);
+  local_segs.clear();
+  for (void* p : opened_peers) cudaIpcCloseMemHandle(p);
+  opened_peers.clear();
+  void* ptrs[] = {owner_dev, seg_table, pe_order, pe_order_off, pe_tickets};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  owner_dev = nullptr;
+  seg_table = nullptr;
+  pe_order = nullptr;
+  pe_order_off = nullptr;
+  pe_tickets = nullptr;
+  host_seg_table.clear();
+  n_pes = 1;
+  n_pe_local = 1;
+  pe_base = 0;
+}
+
+int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
+  if (structure_only) return plan_fail(SPTRSV_E_ARGUMENT, "structure-only plan");
+  if (pes < 1 || pes > 255) return plan_fail(SPTRSV_E_INVALID_PE, "need 1 <= n_pes <= 255");
+  if (my_pe >= pes) return plan_fail(SPTRSV_E_INVALID_PE, "my_pe out of range");
+  std::vector<unsigned char> own(n);
+  for (long long i = 0; i < n; ++i) {
+    if (owner[i] < 0 || owner[i] >= pes) return plan_fail(SPTRSV_E_INVALID_PE, "owner entry out of range");
+    own[i] = (unsigned char)owner[i];
+  }
+  cudaSetDevice(device);
+  release_partition();
+  n_pes = pes;
+  pe_base = my_pe < 0 ? 0 : my_pe;
+  n_pe_local = my_pe < 0 ? pes : 1;
+  // per-PE ticket orders: the PE's components in level order (ascending rows per level)
+  std::vector<int> h_by_level(n);
+  cudaError_t e;
+  if ((e = cudaMemcpy(h_by_level.data(), by_level, sizeof(int) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  std::vector<long long> off(n_pe_local + 1, 0);
+  for (long long k = 0; k < n; ++k) {
+    const int p = own[h_by_level[k]];
+    if (p >= pe_base && p < pe_base + n_pe_local) ++off[p - pe_base + 1];
+  }
+  for (int q = 0; q < n_pe_local; ++q) off[q + 1] += off[q];
+  std::vector<int> ord(std::max<long long>(off[n_pe_local], 1));
+  std::vector<long long> fill(off.begin(), off.end() - 1);
+  for (long long k = 0; k < n; ++k) {
+    const int r = h_by_level[k];
+    const int p = own[r];
+    if (p >= pe_base && p < pe_base + n_pe_local) ord[fill[p - pe_base]++] = r;
+  }
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  if ((e = al((void**)&owner_dev, n)) != cudaSuccess ||
+      (e = al((void**)&pe_order, sizeof(int) * ord.size())) != cudaSuccess ||
+      (e = al((void**)&pe_order_off, sizeof(long long) * off.size())) != cudaSuccess ||
+      (e = al((void**)&pe_tickets, sizeof(int) * n_pe_local)) != cudaSuccess ||
+      (e = al((void**)&seg_table, sizeof(void*) * pes)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  cudaMemcpy(owner_dev, own.data(), n, cudaMemcpyHostToDevice);
+  cudaMemcpy(pe_order, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(pe_order_off, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice);
+  host_seg_table.assign(pes, nullptr);
+  for (int q = 0; q < n_pe_local; ++q) {
+    unsigned long long* seg = nullptr;
+    if ((e = al((void**)&seg, sizeof(unsigned long long) * n)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    local_segs.push_back(seg);
+    host_seg_table[pe_base + q] = seg;
+  }
+  if ((e = cudaMemcpy(seg_table, host_seg_table.data(), sizeof(void*) * pes, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // the read-only inter-PE layer is the component pool (warp per component,
+  // value-is-flag peer loads)
+  executor_used = SPTRSV_EXECUTOR_ROWS;
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStream_t s) {
+  for (int p = 0; p < n_pes; ++p)
+    if (!host_seg_table[p]) return plan_fail(SPTRSV_E_INVALID_PE, "a peer segment was never imported");
+  const int mode = opt.precision == SPTRSV_PRECISION_FAST ? kModeFast : kModeExact;
+  cudaError_t e = cudaSuccess;
+  for (auto* seg : local_segs)
+    if ((e = cudaMemsetAsync(seg, 0xFF, sizeof(unsigned long long) * n, s)) != cudaSuccess) break;
+  if (e == cudaSuccess) e = cudaMemsetAsync(pe_tickets, 0, sizeof(int) * n_pe_local, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  RowsArgs a{};
+  a.n = (int)n;
+  a.rp = rp;
+  a.ci = ci;
+  a.val = mode == kModeFast ? wv : cv;
+  a.dg = dg;
+  a.rdg = rdg;
+  a.b = d_b;
+  a.xseg = seg_table;
+  a.lseg = lseg_dev;
+  a.owner = owner_dev;
+  a.pe_base = pe_base;
+  a.n_pe_local = n_pe_local;
+  a.pe_order_off = pe_order_off;
+  a.order = pe_order;
+  a.order_len = 0;
+  a.ticket = pe_tickets;
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.spin_initial = opt.spin_initial;
+  a.spin_max_ns = opt.spin_max_ns;
+  a.coop_long = 0;
+  a.long_deps = 1 << 30;
+  int per_sm = rows_blocks_per_sm(mode);
+  int blocks = std::max(1, num_sms * std::max(per_sm, 1));
+  blocks = std::max(n_pe_local, blocks - blocks % n_pe_local);
+  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = launch_rows(mode, a, blocks, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if (d_x) {
+    k_gather_owned<<<std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(seg_table, owner_dev, pe_base,
+                                                                                   n_pe_local, n, d_x);
+    if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  launches = 2;
+  return SPTRSV_OK;
+}
+
+}  // namespace sptrsv
+
+using namespace sptrsv;
+
+extern "C" {
+
+int sptrsv_plan_set_partition(sptrsv_plan* plan, const int32_t* owner, int32_t n_pes, int32_t my_pe) {
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || !owner) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  return p->set_partition(owner, n_pes, my_pe);
+}
+
+int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* handle_out) {
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p || !handle_out) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (p->local_segs.size() != 1) return plan_fail(SPTRSV_E_ARGUMENT, "export needs a one-PE-per-process partition");
+  cudaSetDevice(p->device);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, p->local_segs[0]);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return SPTRSV_OK;
+}
+
+int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle) {
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || !handle) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (pe < 0 || pe >= p->n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+  if (pe >= p->pe_base && pe < p->pe_base + p->n_pe_local) return plan_fail(SPTRSV_E_ARGUMENT, "pe is local");
+  cudaSetDevice(p->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* ptr = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  p->opened_peers.push_back(ptr);
+  p->host_seg_table[pe] = reinterpret_cast<unsigned long long*>(ptr);
+  e = cudaMemcpy(p->seg_table, p->host_seg_table.data(), sizeof(void*) * p->n_pes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  return SPTRSV_OK;
+}
+
+int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr) {
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || !device_ptr) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (pe < 0 || pe >= p->n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+  cudaSetDevice(p->device);
+  p->host_seg_table[pe] = reinterpret_cast<unsigned long long*>(device_ptr);
+  cudaError_t e = cudaMemcpy(p->seg_table, p->host_seg_table.data(), sizeof(void*) * p->n_pes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  return SPTRSV_OK;
+}
+
+void* sptrsv_plan_segment(const sptrsv_plan* plan) {
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p || p->local_segs.empty()) return nullptr;
+  return p->local_segs[0];
+}
+
+int sptrsv_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+}  // extern "C"

@@ -50,6 +50,23 @@ struct DevicePlan {
 
   ChainPlan chains;
   StencilPlan stencil;
+
+  // PE partition (partition.cu): each PE owns components (PartitionPlan.owner_arr)
+  // and publishes their x only into its own segment; other PEs read it.
+  int n_pes = 1;          // PEs in the partition
+  int n_pe_local = 1;     // PEs served by this process (all of them when they share the device)
+  int pe_base = 0;        // first local PE
+  unsigned char* owner_dev = nullptr;
+  std::vector<unsigned long long*> local_segs;  // owned by this plan
+  std::vector<void*> opened_peers;              // cudaIpcOpenMemHandle'd segments of other processes
+  unsigned long long** seg_table = nullptr;     // device [n_pes] segment pointers
+  std::vector<unsigned long long*> host_seg_table;
+  int* pe_order = nullptr;
+  long long* pe_order_off = nullptr;
+  int* pe_tickets = nullptr;
+  int set_partition(const int32_t* owner, int pes, int my_pe);
+  int solve_partitioned_rows(const double* d_b, double* d_x, cudaStream_t s);
+  void release_partition();
   long long* probe_buf = nullptr;  // diagnostics (probe_flags)
   int executor_used = SPTRSV_EXECUTOR_ROWS;
 

@@ -255,8 +255,19 @@ __device__ bool level_row_warp(const RowsArgs& a, Poller& poll, int i, int lane)
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_rows(RowsArgs a) {
+__global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
   const int lane = threadIdx.x & 31;
+  // the PE this block works for: its slice of the order and its ticket pool
+  RowsArgs a = a_in;
+  const int n_local = a_in.n_pe_local > 0 ? a_in.n_pe_local : 1;
+  const int pe_local = blockIdx.x % n_local;
+  a.my_pe = a_in.pe_base + pe_local;
+  a.ticket = a_in.ticket + pe_local;
+  if (a_in.pe_order_off) {
+    const long long lo = a_in.pe_order_off[pe_local], hi = a_in.pe_order_off[pe_local + 1];
+    a.order = a_in.order + lo;
+    a.order_len = hi - lo;
+  }
   Poller poll(a);
   while (true) {
     int t = 0;
