@@ -1,0 +1,88 @@
+"""One process per GPU: the read-only inter-GPU layer over CUDA IPC + torch.distributed.
+
+Each rank is one PE of a ``PartitionPlan`` (column-block ``block_partition`` by
+default, as in BASELINE.json's multi-GPU config; ``task_round_robin_partition``
+works too). A rank builds the device plan of the whole matrix, keeps only its
+own components' x in its segment, exports the segment as a CUDA IPC handle and
+opens every peer's segment; inside the solve its kernel reads peers' x with
+one-sided loads over NVLink/NVSwitch. ``torch.distributed`` carries only the
+64-byte handles at setup and a barrier between solves (a solve resets the
+segments, so no rank may start solve k+1 while a peer still reads solve k);
+scatter of b / gather of x, when a caller wants x on one rank, is NCCL.
+
+The orchestration (handle exchange, ownership, x assembly) is plain Python so
+the multi-process logic is testable on CPU with the gloo backend
+(tests/test_multi_gloo.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .partition import PartitionPlan, block_partition, task_round_robin_partition
+
+
+def rank_partition(n: int, world: int, kind: str = "block", tasks_per_pe: int = 1) -> PartitionPlan:
+    """The partition every rank must agree on (deterministic in its arguments)."""
+    if kind == "block":
+        return block_partition(n, world)
+    return task_round_robin_partition(n, world, tasks_per_pe)
+
+
+def exchange_handles(local: bytes, group=None) -> list[bytes]:
+    """All-gather each rank's segment handle (CPU objects over the default group)."""
+    import torch.distributed as dist
+
+    out: list = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, local, group=group)
+    return [bytes(h) for h in out]
+
+
+def owned_rows(owner: np.ndarray, rank: int) -> np.ndarray:
+    return np.flatnonzero(np.asarray(owner) == rank)
+
+
+def assemble_x(parts: list[tuple[np.ndarray, np.ndarray]], n: int) -> np.ndarray:
+    """Full x from (rows, values) pieces of every rank; every row exactly once."""
+    x = np.full(n, np.nan)
+    seen = np.zeros(n, dtype=np.int64)
+    for rows, vals in parts:
+        x[rows] = vals
+        seen[rows] += 1
+    if not np.all(seen == 1):
+        raise ValueError("pieces do not cover every component exactly once")
+    return x
+
+
+class DistributedSolver:
+    """This rank's PE of a partitioned solve (needs a GPU and an initialised process group)."""
+
+    def __init__(self, l, plan: PartitionPlan, rank: int, *, device: int, precision: str = "fast",
+                 timeout: float = 60.0, group=None):
+        from . import _native
+
+        if plan.n != l.n:
+            raise ValueError("partition does not match the matrix")
+        self.rank = rank
+        self.world = plan.n_pes
+        self.group = group
+        self.native = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision,
+                                         executor="rows", device=device, timeout=timeout)
+        self.native.set_partition(plan.owner_arr, plan.n_pes, rank)
+        handles = exchange_handles(self.native.export_segment(), group)
+        for pe, h in enumerate(handles):
+            if pe != rank:
+                self.native.import_segment(pe, h)
+        self.rows = owned_rows(plan.owner_arr, rank)
+
+    def barrier(self) -> None:
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+    def solve_device_async(self, d_b: int, d_x: int, stream: int) -> None:
+        """Solve this rank's components; x of the owned rows lands in d_x (others untouched)."""
+        self.native.solve_device_async(d_b, d_x, stream)
+
+    def synchronize(self) -> dict:
+        return self.native.synchronize()
