@@ -337,5 +337,31 @@ def plan_for(l, **kw) -> NativePlan:
     return plan
 
 
+def partitioned_plan_for(l, partition, **kw) -> NativePlan:
+    """Device plan of ``l`` split into the PEs of ``partition`` (all PEs on this device).
+
+    Cached per (matrix, partition object); the partition is kept alive with the
+    entry so its identity stays a valid key.
+    """
+    key = ("pe", id(partition)) + tuple(sorted(kw.items()))
+    ident = id(l)
+    with _cache_lock:
+        per = _cache.get(ident)
+        if per is None:
+            per = {}
+            _cache[ident] = per
+            weakref.finalize(l, _evict, ident)
+        hit = per.get(key)
+    if hit is not None and hit[0] is partition:
+        return hit[1]
+    kw = dict(kw)
+    kw["executor"] = "rows"
+    plan = NativePlan(l.col_ptr, l.row_idx, l.values, l.n, **kw)
+    plan.set_partition(partition.owner_arr, partition.n_pes, -1)
+    with _cache_lock:
+        per[key] = (partition, plan)
+    return plan
+
+
 def env_device() -> int:
     return int(os.environ.get("SPTRSV_DEVICE", "0"))

@@ -123,6 +123,38 @@ struct StSmem {
   static constexpr int kTotal = kBars + 8 * kStBuffers;
 };
 
+// One lane's inputs of one step, held in registers a step ahead.
+template <bool EXACT>
+struct StBlk {
+  double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock], bv[kStBlock];
+  double inbox[kStC];  // lane 0: the band-above row for this step (copied kStPrefetch steps ago)
+
+  __device__ __forceinline__ void load(const unsigned char* step_buf, const double* bslot, const double* islot,
+                                       int lane) {
+    const double2* cs = reinterpret_cast<const double2*>(step_buf);
+#pragma unroll
+    for (int k = 0; k < kStBlkPairs; ++k) {
+      const double2 u = cs[(0 * kStBlkPairs + k) * kStLanes + lane];
+      const double2 l = cs[(1 * kStBlkPairs + k) * kStLanes + lane];
+      wu[2 * k] = u.x, wu[2 * k + 1] = u.y;
+      wl[2 * k] = l.x, wl[2 * k + 1] = l.y;
+      if (EXACT) {
+        const double2 d = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
+        const double2 r = cs[(3 * kStBlkPairs + k) * kStLanes + lane];
+        dd[2 * k] = d.x, dd[2 * k + 1] = d.y;
+        rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+      } else {
+        const double2 r = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
+        rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+      }
+      const double2 v = reinterpret_cast<const double2*>(bslot)[k];
+      bv[2 * k] = v.x, bv[2 * k + 1] = v.y;
+    }
+#pragma unroll
+    for (int c = 0; c < kStC; ++c) inbox[c] = islot[c];
+  }
+};
+
 template <bool EXACT>
 __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
   using S = StSmem<EXACT>;
@@ -131,7 +163,6 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
   double* bring = reinterpret_cast<double*>(smem + S::kB);
   double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
   const int lane = threadIdx.x;
-  constexpr int NF = st_fields(EXACT);
   if (lane == 0) {
     for (int k = 0; k < kStBuffers; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -152,6 +183,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
     const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
     unsigned long long* below = a.mbox + (size_t)t * a.nx;
     const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
+    const int steps = a.steps;
 
     auto issue = [&](int s) {
       if (lane == 0) {
@@ -189,8 +221,15 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
       }
       cp_async_commit();
     };
+    // wait for step s's stream chunk and copies, then pull its inputs into registers
+    auto stage = [&](int s, StBlk<EXACT>& blk) {
+      await(s);
+      cp_async_wait<kStPrefetch - 1>();
+      const int slot = s % kStPrefetch;
+      blk.load(smem + S::kStream + (s % kStBuffers) * S::kStep, bring + (slot * kStLanes + lane) * kStBlock,
+               inbox + slot * kStC, lane);
+    };
 
-    const int steps = a.steps;
     for (int s = 0; s < steps && s < kStBuffers; ++s) issue(s);
     for (int s = 0; s < kStPrefetch; ++s) prefetch(s);
 
@@ -200,63 +239,46 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
     double bottom[kStC];
 #pragma unroll
     for (int c = 0; c < kStC; ++c) bottom[c] = 0.0;
-    bool resync = false;
 
-    for (int s = 0; s < steps; ++s) {
+    // one lockstep step; `cur` holds its inputs, `nxt` receives step s + 1's
+    auto step = [&](int s, StBlk<EXACT>& cur, StBlk<EXACT>& nxt) {
       const int j = s - lane;
       const bool active = j >= 0 && j < nblk;
-      // row above: lane l-1's bottom row of the previous step
+      // row above: lane l-1's bottom row of the previous step; lane 0 takes the
+      // band above (or zeros on grid row 0)
       double top[kStC];
 #pragma unroll
       for (int c = 0; c < kStC; ++c) top[c] = __shfl_up_sync(0xffffffffu, bottom[c], 1);
-      await(s);
-      cp_async_wait<kStPrefetch - 1>();
-      const int slot = s % kStPrefetch;
+      bool stale = false;
       if (lane == 0) {
-        if (above && active) {
-          bool stale = false;
+#pragma unroll
+        for (int c = 0; c < kStC; ++c) {
+          top[c] = above ? cur.inbox[c] : 0.0;
+          stale |= above && active && (unsigned long long)__double_as_longlong(top[c]) == kNotReady;
+        }
+      }
+      if (__any_sync(0xffffffffu, stale)) {
+        // this band caught up with the band above: poll the missing values, then
+        // fall back until the row above is ready kStPrefetch + kStResync blocks
+        // ahead, so copies issued from now on land ready with margin
+        if (stale) {
 #pragma unroll
           for (int c = 0; c < kStC; ++c) {
-            top[c] = inbox[slot * kStC + c];
             if ((unsigned long long)__double_as_longlong(top[c]) == kNotReady) {
               const unsigned long long u =
                   st_poll(above + j * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
               if (u == kNotReady) alive = false;
               top[c] = as_f64(u);
-              stale = true;
             }
           }
-          resync = stale;
-        } else {
+          const int jn = min(s + kStPrefetch + kStResync, nblk - 1);
 #pragma unroll
-          for (int c = 0; c < kStC; ++c) top[c] = 0.0;  // grid row 0: no entry above
+          for (int c = 0; c < kStC; ++c) {
+            const unsigned long long u =
+                st_poll(above + jn * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+            if (u == kNotReady) alive = false;
+          }
         }
-      }
-      // coefficients of this lane's block: field-major, element pairs, lanes
-      const double2* cs = reinterpret_cast<const double2*>(smem + S::kStream + (s % kStBuffers) * S::kStep);
-      double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock];
-#pragma unroll
-      for (int k = 0; k < kStBlkPairs; ++k) {
-        const double2 u = cs[(0 * kStBlkPairs + k) * kStLanes + lane];
-        const double2 l = cs[(1 * kStBlkPairs + k) * kStLanes + lane];
-        wu[2 * k] = u.x, wu[2 * k + 1] = u.y;
-        wl[2 * k] = l.x, wl[2 * k + 1] = l.y;
-        if (EXACT) {
-          const double2 d = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
-          const double2 r = cs[(3 * kStBlkPairs + k) * kStLanes + lane];
-          dd[2 * k] = d.x, dd[2 * k + 1] = d.y;
-          rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
-        } else {
-          const double2 r = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
-          rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
-        }
-      }
-      const double2* bs = reinterpret_cast<const double2*>(bring + (slot * kStLanes + lane) * kStBlock);
-      double bv[kStBlock];
-#pragma unroll
-      for (int k = 0; k < kStBlkPairs; ++k) {
-        const double2 v = bs[k];
-        bv[2 * k] = v.x, bv[2 * k + 1] = v.y;
       }
       // solve the block: row by row, columns left to right
       double xb[kStR][kStC];
@@ -267,15 +289,13 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
           const int e = r * kStC + c;
           const double up = r == 0 ? top[c] : xb[r - 1][c];
           const double left = c == 0 ? xleft[r] : xb[r][c - 1];
-          double xi;
           if (EXACT) {
-            double acc = __dadd_rn(0.0, __dmul_rn(wu[e], up));
-            acc = __dadd_rn(acc, __dmul_rn(wl[e], left));
-            xi = div_exact(__dsub_rn(bv[e], acc), dd[e], rd[e]);
+            double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
+            acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
+            xb[r][c] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
           } else {
-            xi = __fma_rn(wl[e], left, __fma_rn(wu[e], up, __dmul_rn(bv[e], rd[e])));
+            xb[r][c] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
           }
-          xb[r][c] = as_f64(publishable(xi));
         }
       }
       if (active) {
@@ -292,33 +312,30 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
         for (int c = 0; c < kStC; ++c) bottom[c] = xb[kStR - 1][c];
         if (publish) {
 #pragma unroll
-          for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, (unsigned long long)__double_as_longlong(bottom[c]));
+          for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, publishable(bottom[c]));
         }
-      }
-      // a stale inbox means this band caught up with the band above: fall
-      // back until the row above is ready kStPrefetch + kStResync blocks
-      // ahead, so the copies issued from now on land ready with margin
-      if (__any_sync(0xffffffffu, resync) && lane == 0 && above) {
-        const int jn = min(s + kStPrefetch + kStResync, nblk - 1);
-        {
-#pragma unroll
-          for (int c = 0; c < kStC; ++c) {
-            const unsigned long long u =
-                st_poll(above + jn * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-            if (u == kNotReady) alive = false;
-          }
-        }
-        resync = false;
       }
       prefetch(s + kStPrefetch);
       __syncwarp();
       if (s + kStBuffers < steps) issue(s + kStBuffers);
-      if (!__all_sync(0xffffffffu, alive)) {
-        alive = false;
-        // drain the bulk copies in flight into this CTA's shared memory
-        for (int q = s + 1; q < steps && q < s + 1 + kStBuffers; ++q) await(q);
-        break;
-      }
+      if (s + 1 < steps) stage(s + 1, nxt);
+    };
+
+    StBlk<EXACT> A, B;
+    stage(0, A);
+    int s = 0;
+    for (; s + 1 < steps && alive; s += 2) {
+      step(s, A, B);
+      step(s + 1, B, A);
+      if (!__all_sync(0xffffffffu, alive)) alive = false;
+    }
+    if (s < steps && alive) step(s, A, B);
+    if (!__all_sync(0xffffffffu, alive)) {
+      alive = false;
+      // drain the bulk copies in flight into this CTA's shared memory
+      const int first = phase_bits;  // (unused) every issued step below `steps` is awaited
+      (void)first;
+      for (int q = s + 2; q < steps && q < s + 2 + kStBuffers; ++q) await(q);
     }
     cp_async_wait<0>();
   }

@@ -262,15 +262,19 @@ def _run(l: CscMatrix, b, plan: PartitionPlan, cfg: SolverConfig, expected: Engi
         return x, SolveReport(x=x, wall_time=0.0, setup_time=0.0, solve_time=0.0, engine=expected,
                               n_pes=cfg.n_pes, per_pe=[PeStats(pe=p) for p in range(cfg.n_pes)])
     ts = time.perf_counter()
-    native = _native.plan_for(
-        l,
+    knobs = dict(
         precision=cfg.precision,
-        executor=cfg.executor,
         device=cfg.device,
         timeout=cfg.timeout,
         spin_initial=64 * cfg.spin_backoff.initial_pause,
         spin_max_ns=max(16, cfg.spin_backoff.max_pause // 8),
     )
+    if expected is Engine.PARTITIONED_READ_ONLY and cfg.n_pes > 1:
+        # one published segment per PE (owner-only writes, read-only peers)
+        native = _native.partitioned_plan_for(l, plan, **knobs)
+    else:
+        # one published segment shared by all PEs
+        native = _native.plan_for(l, executor=cfg.executor, **knobs)
     setup = time.perf_counter() - ts
     ts = time.perf_counter()
     x, dev = native.solve(b)
