@@ -51,7 +51,10 @@ struct StArgs {
   unsigned long long timeout_ns;
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
+  int probe;  // diagnostics only: kStProbe* bits switch parts of the step off (results are then wrong)
 };
+constexpr int kStProbeNoAwait = 1, kStProbeNoFence = 2, kStProbeNoWaitB = 4, kStProbeNoPrefetch = 8,
+              kStProbeNoStore = 32;
 
 constexpr int kStBlkPairs = kStBlock / 2;
 
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
     auto issue = [&](int s) {
       if (lane == 0) {
         unsigned long long* bar = &bars[s % kStBuffers];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (!(a.probe & kStProbeNoFence)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(bar, S::kStep);
         bulk_g2s(smem + S::kStream + (s % kStBuffers) * S::kStep, tstream + (size_t)s * S::kStep, S::kStep, bar);
       }
@@ -196,12 +199,16 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
     auto await = [&](int s) {
       const int k = s % kStBuffers;
       const unsigned ph = (phase_bits >> k) & 1u;
-      while (!mbar_try_wait(&bars[k], ph)) {
+      while (!(a.probe & kStProbeNoAwait) && !mbar_try_wait(&bars[k], ph)) {
       }
       phase_bits ^= 1u << k;
     };
     // b block and (lane 0) the band-above row for step s, into ring slot s % P
     auto prefetch = [&](int s) {
+      if (a.probe & kStProbeNoPrefetch) {
+        cp_async_commit();
+        return;
+      }
       const int j = s - lane;
       if (j >= 0 && j < nblk) {
         double* dst = bring + ((s % kStPrefetch) * kStLanes + lane) * kStBlock;
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
     // wait for step s's stream chunk and copies, then pull its inputs into registers
     auto stage = [&](int s, StBlk<EXACT>& blk) {
       await(s);
-      cp_async_wait<kStPrefetch - 1>();
+      if (!(a.probe & kStProbeNoWaitB)) cp_async_wait<kStPrefetch - 1>();
       const int slot = s % kStPrefetch;
       blk.load(smem + S::kStream + (s % kStBuffers) * S::kStep, bring + (slot * kStLanes + lane) * kStBlock,
                inbox + slot * kStC, lane);
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
           }
         }
       }
-      if (active) {
+      if (active && !(a.probe & kStProbeNoStore)) {
 #pragma unroll
         for (int r = 0; r < kStR; ++r) {
           xleft[r] = xb[r][kStC - 1];
@@ -474,6 +481,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.ny = stencil.ny;
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
+  a.probe = opt.probe_flags;
   const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);
