@@ -2,22 +2,29 @@
 """Benchmark: fp64 SpTRSV on B200 — µs/solve and GFLOP/s (2·nnz/t), % of the HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config lap2d-4096]
-                    [--precision fast|exact] [--executor auto|rows|chains]
+                    [--precision fast|exact] [--executor auto|rows|chains|stencil]
     python bench.py --impl reference ...      # the reference's CPU path (oracle port)
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   # column-block over N GPUs
 
 One JSON line on stdout (rank 0). A "step" is one solve of L x = b for the
 configured matrix with b = ones (the reference CLI default, cli.py:139-140).
 
-* ``value``: GFLOP/s = 2·nnz / t, t = mean device time per solve over K
-  back-to-back solves with b and x resident in HBM (CUDA events, barrier +
-  synchronize on both sides, max over ranks).
+* ``value``: GFLOP/s = 2·nnz / t, t = device time per solve over K
+  back-to-back solves with b and x resident in HBM (CUDA events on the solve
+  stream, barrier + synchronize on both sides, max over ranks).
 * ``e2e``: the same metric through the C-ABI host-buffer call
   (``sptrsv_solve``: pinned b -> device, solve, device -> pinned x), wall clock.
 * ``roofline``: the solve kernel's algorithmic bytes (SURVEY.md §8d:
   12·nnz + 4·(n+1) + 16·n) over its CUDA-event duration, against the measured
   HBM copy bandwidth in MEASURED_PEAKS.json.
-* ``cpu_baseline``: the C port of the reference ``solve_serial`` (oracle/)
-  on one host core, full matrix.
+* ``cpu_baseline``: the C port of the reference ``solve_serial`` (oracle/) on
+  one host core, full matrix (rank 0, N = 1 only).
+
+N > 1 (torchrun, one process per GPU): block_partition(n, N) — every GPU owns a
+contiguous slab of rows and its x segment; peers' segments are opened over
+CUDA IPC and read with one-sided loads inside the solve (no collective in the
+solve); an NCCL all-reduce of one word orders consecutive solves. Total work is
+fixed, so ``scaling`` is "strong".
 """
 
 from __future__ import annotations
@@ -106,31 +113,40 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def cpu_reference_arm(args, l, b) -> dict:
+def cpu_solve(l, b, reps: int, budget_s: float) -> dict:
     """The reference's CPU solve (C port of solve_serial, reference.py:20-35), 1 core."""
     import oracle
 
-    t_all = []
-    deadline = time.perf_counter() + max(10.0, 3.0 * args.steps)
-    reps = 0
-    x = None
-    for _ in range(args.warmup):
-        oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
-    while reps < args.steps or (time.perf_counter() < deadline and reps < 1):
+    times, x = [], None
+    t_end = time.perf_counter() + budget_s
+    while len(times) < reps or (not times):
         t0 = time.perf_counter()
         x = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
-        t_all.append(time.perf_counter() - t0)
-        reps += 1
-        if time.perf_counter() > deadline:
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
             break
-    t = statistics.mean(t_all)
-    return {"seconds": t, "reps": reps, "x": x}
+    return {"seconds": statistics.mean(times), "reps": len(times), "x": x}
+
+
+def reference_arm(args, l, b, n, nnz):
+    for _ in range(args.warmup):
+        cpu_solve(l, b, 1, 0)
+    r = cpu_solve(l, b, args.steps, 120.0)
+    gflops = 2.0 * nnz / r["seconds"] / 1e9
+    return {
+        "metric": METRIC, "value": gflops, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": r["reps"], "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "nnz": nnz, "rhs": "ones"},
+        "cpu_baseline": {"value": gflops, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"full {args.config} solve_serial (C port of reference.py:20-35, "
+                                   f"-ffp-contract=off), {r['reps']} reps"},
+        "e2e": {"value": gflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
 
 
 def main():
@@ -141,7 +157,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="lap2d-4096")
     ap.add_argument("--precision", choices=["fast", "exact"], default="fast")
-    ap.add_argument("--executor", choices=["auto", "rows", "chains"], default="auto")
+    ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -158,87 +174,117 @@ def main():
     b = np.ones(n)
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        r = cpu_reference_arm(args, l, b)
-        gflops = flops / r["seconds"] / 1e9
-        line = {
-            "metric": METRIC, "value": gflops, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": r["reps"], "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "n": n, "nnz": nnz, "rhs": "ones"},
-            "cpu_baseline": {"value": gflops, "unit": UNIT, "cores": 1, "kind": "port",
-                             "sample": f"full {args.config} solve_serial (C port, -ffp-contract=off) x{r['reps']}"},
-            "e2e": {"value": gflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        }
-        print(json.dumps(line), flush=True)
+        if rank == 0:
+            print(json.dumps(reference_arm(args, l, b, n, nnz)), flush=True)
         return
 
     import torch
 
+    from paper_2012_06959_b200 import _native
+
+    dev = local
+    torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-        torch.cuda.set_device(local)
-    dev = local
-    torch.cuda.set_device(dev)
-    from paper_2012_06959_b200 import _native
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    stream = torch.cuda.Stream(dev)  # solves, events and the inter-solve all-reduce share it
+    sh = stream.cuda_stream
 
     ts = time.perf_counter()
-    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, n, precision=args.precision,
-                              executor=args.executor, device=dev)
+    if ws > 1:
+        from paper_2012_06959_b200 import multi
+
+        partition = multi.rank_partition(n, ws, "block")
+        solver = multi.DistributedSolver(l, partition, rank, device=dev, precision=args.precision)
+        plan = solver.native
+        owned = torch.from_numpy((partition.owner_arr == rank).astype(np.float64)).to(f"cuda:{dev}")
+    else:
+        solver = None
+        plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, n, precision=args.precision,
+                                  executor=args.executor, device=dev)
     setup_s = time.perf_counter() - ts
     info = plan.info()
+    if ws > 1:
+        info["executor"] = "rows (PE segments)"
 
-    # ---- device-resident timing -------------------------------------------
     db = torch.from_numpy(b).to(f"cuda:{dev}")
-    dx = torch.empty_like(db)
-    torch.cuda.synchronize(dev)
-    # a dedicated (non-default) stream: the solves and the timing events share it
-    stream = torch.cuda.Stream(dev)
-    sh = stream.cuda_stream
-    for _ in range(args.warmup):
-        plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
-    plan.synchronize()
-    torch.cuda.synchronize(dev)
-    if ws > 1:
-        torch.distributed.barrier()
-    kernel_ms = []
-    with ClockSampler(dev) as clocks:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for _ in range(args.steps):
-            plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        total_ms = e0.elapsed_time(e1)
-        # per-launch kernel durations (same stream, events around the kernel)
-        for _ in range(min(args.steps, 10)):
-            plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
-            st = plan.synchronize()
-            kernel_ms.append(st["kernel_ms"])
-    ms = total_ms / args.steps
-    if ws > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    x_dev = dx.cpu().numpy()
+    dx = torch.zeros_like(db)
+    order_word = torch.zeros(1, device=f"cuda:{dev}")
 
-    # ---- end-to-end through the C ABI host-buffer call --------------------
+    def one_solve():
+        if ws > 1:
+            # every rank finished the previous solve before any segment is reset
+            torch.distributed.all_reduce(order_word)
+        plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one_solve()
+        plan.synchronize()
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            torch.distributed.barrier()
+        kernel_ms = []
+        with ClockSampler(dev) as clocks:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for _ in range(args.steps):
+                one_solve()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            total_ms = e0.elapsed_time(e1)
+            # per-launch kernel durations (events around the kernel, same stream)
+            for _ in range(min(args.steps, 10)):
+                one_solve()
+                st = plan.synchronize()
+                kernel_ms.append(st["kernel_ms"])
+        if ws > 1:
+            torch.distributed.barrier()
+        ms = total_ms / args.steps
+        if ws > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+            # x: each rank holds its owned rows; the sum over ranks assembles it
+            xfull = dx * owned
+            torch.distributed.all_reduce(xfull)
+            x_dev = xfull.cpu().numpy()
+        else:
+            x_dev = dx.cpu().numpy()
+
+    # ---- end-to-end through the C ABI host-buffer call (pinned b / x) -----
     hb = torch.from_numpy(b).pin_memory()
     hx = torch.empty(n, dtype=torch.float64).pin_memory()
     hb_np, hx_np = hb.numpy(), hx.numpy()
-    plan.solve(hb_np, out=hx_np)
     t_e2e = []
-    for _ in range(args.e2e_steps):
-        t1 = time.perf_counter()
+    if ws == 1:
         plan.solve(hb_np, out=hx_np)
-        t_e2e.append(time.perf_counter() - t1)
+        for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
+            plan.solve(hb_np, out=hx_np)
+            t_e2e.append(time.perf_counter() - t1)
+        assert hx_np.tobytes() == x_dev.tobytes()
+        d2h = 8 * n
+    else:
+        rows = solver.rows
+        for _ in range(args.e2e_steps + 1):
+            torch.distributed.barrier()
+            t1 = time.perf_counter()
+            db.copy_(hb, non_blocking=True)
+            one_solve()
+            plan.synchronize()
+            hx.copy_(dx, non_blocking=False)
+            t_e2e.append(time.perf_counter() - t1)
+        t_e2e = t_e2e[1:]
+        d2h = 8 * int(rows.size)
     e2e_s = statistics.mean(t_e2e)
-    assert hx_np.tobytes() == x_dev.tobytes()
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
 
     if rank != 0:
         if ws > 1:
@@ -250,8 +296,8 @@ def main():
     from paper_2012_06959_b200 import compare_solutions, residual_norm, residual_norm_2
 
     cpu = None
-    if not args.no_cpu_baseline:
-        cpu = cpu_reference_arm(argparse.Namespace(steps=1, warmup=0), l, b)
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_solve(l, b, 1, 0)
         x_ref = cpu["x"]
     else:
         x_ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
@@ -280,7 +326,7 @@ def main():
         "ms_per_step": ms,
         "us_per_solve": ms * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if ws > 1 else "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -292,7 +338,7 @@ def main():
             "rhs": "ones",
             "precision": args.precision,
             "executor": info["executor"],
-            "parallelism": f"column-block x{ws}" if ws > 1 else "single GPU",
+            "parallelism": f"column-block x{ws} (block_partition), IPC peer segments" if ws > 1 else "single GPU",
             "l2": f"no flush: solve inputs {alg / 1e6:.0f} MB vs 126 MB L2" if alg > 256e6
             else "inputs fit L2 (warm-L2 figure)",
         },
@@ -311,9 +357,9 @@ def main():
             "value": flops / e2e_s / 1e9,
             "unit": UNIT,
             "h2d_bytes_per_step": 8 * n,
-            "d2h_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": d2h,
             "ms_per_step": e2e_s * 1e3,
-            "path": "sptrsv_solve (C ABI, pinned host b/x)",
+            "path": "sptrsv_solve (C ABI, pinned host b/x)" if ws == 1 else "per-rank H2D b, solve, D2H owned x",
         },
         "cpu_baseline": None if cpu is None else {
             "value": flops / cpu["seconds"] / 1e9,
@@ -323,7 +369,7 @@ def main():
             "sample": f"full {args.config} solve_serial (C port of reference.py:20-35), 1 rep",
             "seconds": cpu["seconds"],
         },
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * int(plan.synchronize().get("launches", 1)),
         "clocks": clocks.summary(),
         "correctness": {
             "max_rel_err_vs_oracle": cmp.max_rel_error,
@@ -332,9 +378,6 @@ def main():
             "residual_2_rel": res_2,
         },
         "setup_ms": setup_s * 1e3,
-        "plan": {k: info[k] for k in ("chain_tasks", "chain_slices", "chain_stream_bytes", "chain_mailboxes",
-                                     "chain_max_width", "deps_total", "deps_register", "deps_ring",
-                                     "deps_mailbox", "chain_max_task_steps", "schedule_ms")},
         "generate_s": gen_s,
     }
     print(json.dumps(line), flush=True)

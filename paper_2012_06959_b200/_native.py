@@ -250,11 +250,11 @@ class NativePlan:
     def segment_ptr(self) -> int:
         return int(self._lib.sptrsv_plan_segment(self._h) or 0)
 
-    def probe_stamps(self) -> np.ndarray:
-        out = np.zeros(5 * 64, dtype=np.int64)
+    def probe_stamps(self, per_step: int = 5) -> np.ndarray:
+        out = np.zeros(per_step * 64, dtype=np.int64)
         rc = self._lib.sptrsv_plan_probe_read(self._h, _ptr(out, C.c_int64), out.size)
         raise_for_status(rc, _err(self._lib))
-        return out.reshape(64, 5)
+        return out.reshape(64, per_step)
 
     def in_degrees(self) -> np.ndarray:
         out = np.empty(self.n, dtype=np.int64)

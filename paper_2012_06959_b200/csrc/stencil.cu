@@ -52,6 +52,7 @@ struct StArgs {
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
   int probe;  // diagnostics only: kStProbe* bits switch parts of the step off (results are then wrong)
+  long long* dbg;  // kStProbeClock: 6 clock64 stamps per step for steps [500, 564) of task 0, lane 0
 };
 constexpr int kStProbeNoAwait = 1, kStProbeNoFence = 2, kStProbeNoWaitB = 4, kStProbeNoPrefetch = 8,
               kStProbeNoStore = 32;
@@ -249,6 +250,8 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
 
     // one lockstep step; `cur` holds its inputs, `nxt` receives step s + 1's
     auto step = [&](int s, StBlk<EXACT>& cur, StBlk<EXACT>& nxt) {
+      long long* stamp = (a.dbg && t == 0 && lane == 0 && s >= 500 && s < 564) ? a.dbg + 6 * (s - 500) : nullptr;
+      if (stamp) stamp[0] = clock64();
       const int j = s - lane;
       const bool active = j >= 0 && j < nblk;
       // row above: lane l-1's bottom row of the previous step; lane 0 takes the
@@ -287,6 +290,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
           }
         }
       }
+      if (stamp) stamp[1] = clock64();
       // solve the block: row by row, columns left to right
       double xb[kStR][kStC];
 #pragma unroll
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
           }
         }
       }
+      if (stamp) stamp[2] = clock64();
       if (active && !(a.probe & kStProbeNoStore)) {
 #pragma unroll
         for (int r = 0; r < kStR; ++r) {
@@ -322,10 +327,13 @@ __global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
           for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, publishable(bottom[c]));
         }
       }
+      if (stamp) stamp[3] = clock64();
       prefetch(s + kStPrefetch);
       __syncwarp();
       if (s + kStBuffers < steps) issue(s + kStBuffers);
+      if (stamp) stamp[4] = clock64();
       if (s + 1 < steps) stage(s + 1, nxt);
+      if (stamp) stamp[5] = clock64();
     };
 
     StBlk<EXACT> A, B;
@@ -482,6 +490,12 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
   a.probe = opt.probe_flags;
+  if (opt.probe_flags & 16) {
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, "probe buffer");
+    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 6 * 64, s);
+    a.dbg = probe_buf;
+  }
   const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);

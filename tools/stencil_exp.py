@@ -35,12 +35,32 @@ def run(ny, probe=0, precision="fast"):
         p.close()
     bands = (ny + 63) // 64
     steps = 1024 + 31
-    print(json.dumps({"ny": ny, "bands": bands, "probe": probe, "precision": precision, "kernel_ms": round(min(ks), 4),
-                      "spins": sp[-1], "ns_per_band_step": round(min(ks) * 1e6 / (steps + (bands - 1) * 32), 1)}),
-          flush=True)
+    rec = {"ny": ny, "bands": bands, "probe": probe, "precision": precision, "kernel_ms": round(min(ks), 4),
+           "spins": sp[-1], "ns_per_band_step": round(min(ks) * 1e6 / (steps + (bands - 1) * 32), 1)}
+    print(json.dumps(rec), flush=True)
+
+
+def clock_profile(ny=64, precision="fast"):
+    l = synth.lap2d(4096, ny)
+    p = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
+                           probe_flags=16)
+    b = np.ones(l.n)
+    p.solve(b)
+    p.solve(b)
+    st = p.probe_stamps(6)
+    d = np.diff(st, axis=1)
+    names = ["shfl+inbox", "compute", "stores", "prefetch+issue", "stage(next)"]
+    out = {nm: float(np.median(d[:, k])) for k, nm in enumerate(names)}
+    out["step"] = float(np.median(np.diff(st[:, 0])))
+    print(json.dumps({"clock_cycles": out, "precision": precision}), flush=True)
+    p.close()
 
 
 def main():
+    if "--clock" in sys.argv:
+        clock_profile(64, "fast")
+        clock_profile(64, "exact")
+        return
     if "--variants" in sys.argv:
         for probe in (0, NO_FENCE, NO_AWAIT, NO_WAITB, NO_PREFETCH | NO_WAITB, NO_STORE,
                       NO_AWAIT | NO_FENCE | NO_WAITB | NO_PREFETCH | NO_STORE):
