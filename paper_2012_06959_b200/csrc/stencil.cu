@@ -1,28 +1,31 @@
-// Register-blocked wavefront executor for 2D five-point lower structure.
+// Register-blocked, warp-specialised wavefront executor for 2D five-point
+// lower structure.
 //
 // Structure: row i = y*nx + x stores (i, i-nx) iff y > 0 and (i, i-1) iff
 // x > 0 (plus the diagonal), any coefficients — detected from the CSR at plan
 // time. The dependency DAG is then the nx-by-ny grid wavefront: 8191 levels
 // for 4096 x 4096.
 //
-// Layout of the work: a task (one warp) owns a band of kStBand = 64 grid
-// rows; lane l owns rows 2l, 2l+1 of the band and, at lockstep step s, solves
-// the 2 x kStC block of columns [jC, jC + C) with j = s - l. Everything a
-// block needs from outside arrives in registers: the row above from lane l-1's
-// block of the previous step by one __shfl_up_sync, the left neighbours from
-// this lane's previous block. Inside the block the wavefront is resolved in
-// registers (critical path: one FMA per element along a row). Bands depend on
-// the band above through value-is-flag mailboxes (the band's bottom grid row),
-// prefetched kStPrefetch steps ahead by lane 0 with cp.async.cg; a stale
-// prefetch falls back to polling and then re-synchronises the lag so later
-// prefetches land.
+// Work: a task (one CTA) owns a band of kStBand = 64 grid rows. Its compute
+// warp's lane l owns rows 2l, 2l+1 and, at lockstep step s, solves the 2 x kStC
+// block of columns [jC, jC + C) with j = s - l. The row above comes from lane
+// l-1's block of the previous step by one __shfl_up_sync, the left neighbours
+// from this lane's previous block; inside the block the wavefront is resolved
+// in registers. Bands depend on the band above through value-is-flag
+// mailboxes (the band's bottom grid row).
 //
-// Data: coefficients are repacked at plan time into a per-task stream in
-// (step, field, element-pair, lane) order and moved to shared memory by TMA
-// bulk copies (cp.async.bulk + mbarrier), kStBuffers steps ahead; b is
-// gathered with cp.async kStPrefetch steps ahead; x is written with 16-byte
-// stores. No column indices are read at all: per element the solve moves
-// 24 B of coefficients (fast) + 8 B b + 8 B x.
+// The compute warp is the critical path, so it only shuffles, multiplies and
+// writes shared memory. Two helper warps run beside it (other SM
+// sub-partitions):
+//   * loader: streams the band's coefficient stream into a kStSlots ring with
+//     TMA bulk copies (cp.async.bulk + mbarrier), gathers b with cp.async, and
+//     polls the band-above mailbox for each step before handing the step over —
+//     so the compute warp never waits on global memory;
+//   * storer: writes the solved blocks from a shared-memory ring to x with
+//     16-byte stores.
+// Hand-offs are monotone step counters in shared memory (release/acquire at
+// CTA scope). No column indices are read: per element the solve moves 24 B of
+// coefficients (fast) + 8 B b + 8 B x.
 //
 // Arithmetic: fast: x = wl*left + (wu*up + b/d) with pre-scaled coefficients;
 // exact: s = 0 + wu*up, s = s + wl*left, x = (b - s)/d — the serial oracle's
@@ -51,11 +54,7 @@ struct StArgs {
   unsigned long long timeout_ns;
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
-  int probe;  // diagnostics only: kStProbe* bits switch parts of the step off (results are then wrong)
-  long long* dbg;  // kStProbeClock: 6 clock64 stamps per step for steps [500, 564) of task 0, lane 0
 };
-constexpr int kStProbeNoAwait = 1, kStProbeNoFence = 2, kStProbeNoWaitB = 4, kStProbeNoPrefetch = 8,
-              kStProbeNoStore = 32;
 
 constexpr int kStBlkPairs = kStBlock / 2;
 
@@ -81,16 +80,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// step counters shared by the three warps of a CTA
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, int* abort_flag, DeviceStatus* status,
@@ -117,25 +122,39 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
   return u;
 }
 
+// control words of one task
+enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5 };
+
 template <bool EXACT>
 struct StSmem {
   static constexpr int kStep = st_step_bytes(EXACT);
-  static constexpr int kStream = 0;
-  static constexpr int kB = kStBuffers * kStep;                                   // b ring
-  static constexpr int kInbox = kB + kStPrefetch * kStLanes * kStBlock * 8;       // lane 0's mailbox copies
-  static constexpr int kBars = kInbox + kStPrefetch * kStC * 8;
-  static constexpr int kTotal = kBars + 8 * kStBuffers;
+  static constexpr int kCoef = 0;                                      // [kStSlots][kStep]
+  static constexpr int kB = kCoef + kStSlots * kStep;                  // [kStSlots][lane][kStBlock] f64
+  static constexpr int kInbox = kB + kStSlots * kStLanes * kStBlock * 8;  // [kStSlots][kStC] f64
+  static constexpr int kOut = kInbox + kStSlots * kStC * 8;            // [kStOut][lane][kStBlock] f64
+  static constexpr int kBars = kOut + kStOut * kStLanes * kStBlock * 8;
+  static constexpr int kCtl = kBars + 8 * kStSlots;
+  static constexpr int kTotal = kCtl + 64;
 };
 
-// One lane's inputs of one step, held in registers a step ahead.
+// Spin on a step counter; false when the task is being aborted.
+__device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need) {
+  while (ld_acquire_cta(ctl + which) < need) {
+    if (ld_acquire_cta(ctl + kCtlAbort)) return false;
+  }
+  return true;
+}
+
+// One lane's inputs of one step, loaded a step ahead into registers.
 template <bool EXACT>
 struct StBlk {
   double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock], bv[kStBlock];
-  double inbox[kStC];  // lane 0: the band-above row for this step (copied kStPrefetch steps ago)
+  double inbox[kStC];
 
-  __device__ __forceinline__ void load(const unsigned char* step_buf, const double* bslot, const double* islot,
-                                       int lane) {
-    const double2* cs = reinterpret_cast<const double2*>(step_buf);
+  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int lane) {
+    using S = StSmem<EXACT>;
+    const double2* cs = reinterpret_cast<const double2*>(smem + S::kCoef + slot * S::kStep);
+    const double2* bs = reinterpret_cast<const double2*>(smem + S::kB) + (slot * kStLanes + lane) * kStBlkPairs;
 #pragma unroll
     for (int k = 0; k < kStBlkPairs; ++k) {
       const double2 u = cs[(0 * kStBlkPairs + k) * kStLanes + lane];
@@ -151,210 +170,226 @@ struct StBlk {
         const double2 r = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
         rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
       }
-      const double2 v = reinterpret_cast<const double2*>(bslot)[k];
+      const double2 v = bs[k];
       bv[2 * k] = v.x, bv[2 * k + 1] = v.y;
     }
+    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + slot * kStC;
 #pragma unroll
-    for (int c = 0; c < kStC; ++c) inbox[c] = islot[c];
+    for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
   }
 };
 
+// ---- warp 1: stream coefficients, gather b, poll the band above ------------
 template <bool EXACT>
-__global__ void __launch_bounds__(32, 1) k_stencil2d(StArgs a) {
+__device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned& phase_bits,
+                       unsigned long long deadline) {
   using S = StSmem<EXACT>;
-  extern __shared__ __align__(128) unsigned char smem[];
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
   double* bring = reinterpret_cast<double*>(smem + S::kB);
   double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
-  const int lane = threadIdx.x;
-  if (lane == 0) {
-    for (int k = 0; k < kStBuffers; ++k) mbar_init(&bars[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  unsigned phase_bits = 0;
-  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
-  const int nblk = a.nx / kStC;
-  bool alive = true;
-
-  while (alive) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(a.ticket, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= a.n_tasks) break;
-    const int y0 = t * kStBand + kStR * lane;  // first grid row of this lane
-    const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
-    const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
-    unsigned long long* below = a.mbox + (size_t)t * a.nx;
-    const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
-    const int steps = a.steps;
-
-    auto issue = [&](int s) {
-      if (lane == 0) {
-        unsigned long long* bar = &bars[s % kStBuffers];
-        if (!(a.probe & kStProbeNoFence)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, S::kStep);
-        bulk_g2s(smem + S::kStream + (s % kStBuffers) * S::kStep, tstream + (size_t)s * S::kStep, S::kStep, bar);
-      }
-    };
-    auto await = [&](int s) {
-      const int k = s % kStBuffers;
-      const unsigned ph = (phase_bits >> k) & 1u;
-      while (!(a.probe & kStProbeNoAwait) && !mbar_try_wait(&bars[k], ph)) {
-      }
-      phase_bits ^= 1u << k;
-    };
-    // b block and (lane 0) the band-above row for step s, into ring slot s % P
-    auto prefetch = [&](int s) {
-      if (a.probe & kStProbeNoPrefetch) {
-        cp_async_commit();
-        return;
-      }
-      const int j = s - lane;
-      if (j >= 0 && j < nblk) {
-        double* dst = bring + ((s % kStPrefetch) * kStLanes + lane) * kStBlock;
-#pragma unroll
-        for (int r = 0; r < kStR; ++r) {
-          if (y0 + r < a.ny) {
-            const double* src = a.b + (size_t)(y0 + r) * a.nx + j * kStC;
-#pragma unroll
-            for (int c = 0; c < kStC; c += 2) cp_async16_ca(dst + r * kStC + c, src + c);
-          }
-        }
-        if (lane == 0 && above) {
-#pragma unroll
-          for (int c = 0; c < kStC; c += 2)
-            cp_async16_cg(inbox + (s % kStPrefetch) * kStC + c, above + j * kStC + c);
-        }
-      }
-      cp_async_commit();
-    };
-    // wait for step s's stream chunk and copies, then pull its inputs into registers
-    auto stage = [&](int s, StBlk<EXACT>& blk) {
-      await(s);
-      if (!(a.probe & kStProbeNoWaitB)) cp_async_wait<kStPrefetch - 1>();
-      const int slot = s % kStPrefetch;
-      blk.load(smem + S::kStream + (s % kStBuffers) * S::kStep, bring + (slot * kStLanes + lane) * kStBlock,
-               inbox + slot * kStC, lane);
-    };
-
-    for (int s = 0; s < steps && s < kStBuffers; ++s) issue(s);
-    for (int s = 0; s < kStPrefetch; ++s) prefetch(s);
-
-    double xleft[kStR];
-#pragma unroll
-    for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
-    double bottom[kStC];
-#pragma unroll
-    for (int c = 0; c < kStC; ++c) bottom[c] = 0.0;
-
-    // one lockstep step; `cur` holds its inputs, `nxt` receives step s + 1's
-    auto step = [&](int s, StBlk<EXACT>& cur, StBlk<EXACT>& nxt) {
-      long long* stamp = (a.dbg && t == 0 && lane == 0 && s >= 500 && s < 564) ? a.dbg + 6 * (s - 500) : nullptr;
-      if (stamp) stamp[0] = clock64();
-      const int j = s - lane;
-      const bool active = j >= 0 && j < nblk;
-      // row above: lane l-1's bottom row of the previous step; lane 0 takes the
-      // band above (or zeros on grid row 0)
-      double top[kStC];
-#pragma unroll
-      for (int c = 0; c < kStC; ++c) top[c] = __shfl_up_sync(0xffffffffu, bottom[c], 1);
-      bool stale = false;
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < kStC; ++c) {
-          top[c] = above ? cur.inbox[c] : 0.0;
-          stale |= above && active && (unsigned long long)__double_as_longlong(top[c]) == kNotReady;
-        }
-      }
-      if (__any_sync(0xffffffffu, stale)) {
-        // this band caught up with the band above: poll the missing values, then
-        // fall back until the row above is ready kStPrefetch + kStResync blocks
-        // ahead, so copies issued from now on land ready with margin
-        if (stale) {
-#pragma unroll
-          for (int c = 0; c < kStC; ++c) {
-            if ((unsigned long long)__double_as_longlong(top[c]) == kNotReady) {
-              const unsigned long long u =
-                  st_poll(above + j * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-              if (u == kNotReady) alive = false;
-              top[c] = as_f64(u);
-            }
-          }
-          const int jn = min(s + kStPrefetch + kStResync, nblk - 1);
-#pragma unroll
-          for (int c = 0; c < kStC; ++c) {
-            const unsigned long long u =
-                st_poll(above + jn * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-            if (u == kNotReady) alive = false;
-          }
-        }
-      }
-      if (stamp) stamp[1] = clock64();
-      // solve the block: row by row, columns left to right
-      double xb[kStR][kStC];
+  const int steps = a.steps, nblk = a.nx / kStC;
+  const int y0 = t * kStBand + kStR * lane;
+  const unsigned char* tstream = a.stream + (size_t)t * steps * S::kStep;
+  const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
+  int issued = 0;
+  bool ok = true;
+  auto issue = [&](int s) {
+    const int slot = s % kStSlots;
+    if (s >= kStSlots) ok = ok && wait_ctl(ctl, kCtlInDone, s - kStSlots + 1);  // slot consumed
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[slot], S::kStep);
+      bulk_g2s(smem + S::kCoef + slot * S::kStep, tstream + (size_t)s * S::kStep, S::kStep, &bars[slot]);
+    }
+    const int j = s - lane;
+    if (j >= 0 && j < nblk) {
+      double* dst = bring + (slot * kStLanes + lane) * kStBlock;
 #pragma unroll
       for (int r = 0; r < kStR; ++r) {
+        if (y0 + r < a.ny) {
+          const double* src = a.b + (size_t)(y0 + r) * a.nx + j * kStC;
 #pragma unroll
-        for (int c = 0; c < kStC; ++c) {
-          const int e = r * kStC + c;
-          const double up = r == 0 ? top[c] : xb[r - 1][c];
-          const double left = c == 0 ? xleft[r] : xb[r][c - 1];
-          if (EXACT) {
-            double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
-            acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
-            xb[r][c] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
-          } else {
-            xb[r][c] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
-          }
+          for (int c = 0; c < kStC; c += 2) cp_async16(dst + r * kStC + c, src + c);
         }
       }
-      if (stamp) stamp[2] = clock64();
-      if (active && !(a.probe & kStProbeNoStore)) {
+    }
+    cp_async_commit();
+    ++issued;
+  };
+  auto retire = [&](int q, bool draining) {
+    const int slot = q % kStSlots;
+    const unsigned ph = (phase_bits >> slot) & 1u;
+    while (!mbar_try_wait(&bars[slot], ph)) {
+    }
+    phase_bits ^= 1u << slot;
+    if (draining) cp_async_wait<0>();
+    else cp_async_wait<kStLook>();
+    if (lane == 0 && above && q < nblk) {  // lane 0's block at step q is column block q
 #pragma unroll
-        for (int r = 0; r < kStR; ++r) {
-          xleft[r] = xb[r][kStC - 1];
-          if (y0 + r < a.ny) {
-            double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
-#pragma unroll
-            for (int c = 0; c < kStC; c += 2) dst[c / 2] = make_double2(xb[r][c], xb[r][c + 1]);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < kStC; ++c) bottom[c] = xb[kStR - 1][c];
-        if (publish) {
-#pragma unroll
-          for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, publishable(bottom[c]));
-        }
+      for (int c = 0; c < kStC; ++c) {
+        const unsigned long long u =
+            st_poll(above + q * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+        if (u == kNotReady) ok = false;
+        inbox[slot * kStC + c] = __longlong_as_double((long long)u);
       }
-      if (stamp) stamp[3] = clock64();
-      prefetch(s + kStPrefetch);
-      __syncwarp();
-      if (s + kStBuffers < steps) issue(s + kStBuffers);
-      if (stamp) stamp[4] = clock64();
-      if (s + 1 < steps) stage(s + 1, nxt);
-      if (stamp) stamp[5] = clock64();
-    };
-
-    StBlk<EXACT> A, B;
-    stage(0, A);
-    int s = 0;
-    for (; s + 1 < steps && alive; s += 2) {
-      step(s, A, B);
-      step(s + 1, B, A);
-      if (!__all_sync(0xffffffffu, alive)) alive = false;
     }
-    if (s < steps && alive) step(s, A, B);
-    if (!__all_sync(0xffffffffu, alive)) {
-      alive = false;
-      // drain the bulk copies in flight into this CTA's shared memory
-      const int first = phase_bits;  // (unused) every issued step below `steps` is awaited
-      (void)first;
-      for (int q = s + 2; q < steps && q < s + 2 + kStBuffers; ++q) await(q);
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kCtlInReady, q + 1);
+  };
+  for (int s = 0; s < steps + kStLook; ++s) {
+    if (s < steps) issue(s);
+    const int q = s - kStLook;
+    if (q >= 0) retire(q, s >= steps);
+    if (!__all_sync(0xffffffffu, ok)) {
+      // abort: settle the bulk copies in flight, then tell the other warps
+      for (int r = max(q + 1, 0); r < issued; ++r) {
+        const int slot = r % kStSlots;
+        const unsigned ph = (phase_bits >> slot) & 1u;
+        while (!mbar_try_wait(&bars[slot], ph)) {
+        }
+        phase_bits ^= 1u << slot;
+      }
+      cp_async_wait<0>();
+      if (lane == 0) st_release_cta(ctl + kCtlAbort, 1);
+      return;
     }
-    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
+}
+
+// ---- warp 2: solved blocks from shared memory to x --------------------------
+template <bool EXACT>
+__device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane) {
+  using S = StSmem<EXACT>;
+  const double2* out = reinterpret_cast<const double2*>(smem + S::kOut);
+  const int steps = a.steps, nblk = a.nx / kStC;
+  const int y0 = t * kStBand + kStR * lane;
+  for (int s = 0; s < steps; ++s) {
+    if (!wait_ctl(ctl, kCtlOutReady, s + 1)) return;
+    const int j = s - lane;
+    if (j >= 0 && j < nblk) {
+      const double2* src = out + ((s % kStOut) * kStLanes + lane) * kStBlkPairs;
+#pragma unroll
+      for (int r = 0; r < kStR; ++r) {
+        if (y0 + r < a.ny) {
+          double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
+#pragma unroll
+          for (int c = 0; c < kStC / 2; ++c) dst[c] = src[r * (kStC / 2) + c];
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kCtlOutDone, s + 1);
+  }
+}
+
+// ---- warp 0: the lockstep wavefront -----------------------------------------
+template <bool EXACT>
+__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane) {
+  using S = StSmem<EXACT>;
+  double2* out = reinterpret_cast<double2*>(smem + S::kOut);
+  const int steps = a.steps, nblk = a.nx / kStC;
+  const bool has_above = t > 0;
+  unsigned long long* below = a.mbox + (size_t)t * a.nx;
+  const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
+  double xleft[kStR];
+#pragma unroll
+  for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
+  double bottom[kStC];
+#pragma unroll
+  for (int c = 0; c < kStC; ++c) bottom[c] = 0.0;
+
+  auto step = [&](int s, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt) -> bool {
+    const int j = s - lane;
+    const bool active = j >= 0 && j < nblk;
+    double top[kStC];
+#pragma unroll
+    for (int c = 0; c < kStC; ++c) {
+      const double up = __shfl_up_sync(0xffffffffu, bottom[c], 1);
+      top[c] = lane == 0 ? (has_above ? cur.inbox[c] : 0.0) : up;
+    }
+    double xb[kStR][kStC];
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) {
+#pragma unroll
+      for (int c = 0; c < kStC; ++c) {
+        const int e = r * kStC + c;
+        const double up = r == 0 ? top[c] : xb[r - 1][c];
+        const double left = c == 0 ? xleft[r] : xb[r][c - 1];
+        if (EXACT) {
+          double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
+          acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
+          xb[r][c] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
+        } else {
+          xb[r][c] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
+        }
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
+#pragma unroll
+      for (int c = 0; c < kStC; ++c) bottom[c] = xb[kStR - 1][c];
+      if (publish) {
+#pragma unroll
+        for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, publishable(bottom[c]));
+      }
+    }
+    if (s >= kStOut && !wait_ctl(ctl, kCtlOutDone, s - kStOut + 1)) return false;
+    double2* dst = out + ((s % kStOut) * kStLanes + lane) * kStBlkPairs;
+#pragma unroll
+    for (int r = 0; r < kStR; ++r)
+#pragma unroll
+      for (int c = 0; c < kStC; c += 2) dst[r * (kStC / 2) + c / 2] = make_double2(xb[r][c], xb[r][c + 1]);
+    __syncwarp();
+    if (lane == 0) {
+      st_release_cta(ctl + kCtlOutReady, s + 1);
+      st_release_cta(ctl + kCtlInDone, s + 1);
+    }
+    if (s + 1 < steps) {
+      if (!wait_ctl(ctl, kCtlInReady, s + 2)) return false;
+      nxt.load(smem, (s + 1) % kStSlots, lane);
+    }
+    return true;
+  };
+
+  StBlk<EXACT> A, B;
+  if (!wait_ctl(ctl, kCtlInReady, 1)) return;
+  A.load(smem, 0, lane);
+  int s = 0;
+  for (; s + 1 < steps; s += 2) {
+    if (!step(s, A, B)) return;
+    if (!step(s + 1, B, A)) return;
+  }
+  if (s < steps) step(s, A, B);
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
+  using S = StSmem<EXACT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  int* ctl = reinterpret_cast<int*>(smem + S::kCtl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
+    for (int k = 0; k < kStSlots; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned phase_bits = 0;
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      ctl[kCtlTask] = atomicAdd(a.ticket, 1);
+      ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
+    }
+    __syncthreads();
+    const int t = ctl[kCtlTask];
+    if (t >= a.n_tasks) break;
+    if (warp == 0) compute<EXACT>(a, smem, ctl, t, lane);
+    else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
+    else storer<EXACT>(a, smem, ctl, t, lane);
+    __syncthreads();
+    if (ctl[kCtlAbort]) break;
+  }
 }
 
 template <bool EXACT>
@@ -366,7 +401,7 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stencil2d<EXACT><<<blocks, 32, StSmem<EXACT>::kTotal, s>>>(a);
+  k_stencil2d<EXACT><<<blocks, 96, StSmem<EXACT>::kTotal, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -489,13 +524,6 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.ny = stencil.ny;
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
-  a.probe = opt.probe_flags;
-  if (opt.probe_flags & 16) {
-    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, "probe buffer");
-    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 6 * 64, s);
-    a.dbg = probe_buf;
-  }
   const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);

@@ -14,11 +14,11 @@ namespace sptrsv {
 constexpr int kStR = 2;
 constexpr int kStC = 4;
 constexpr int kStLanes = 32;
-constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one warp)
+constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one CTA)
 constexpr int kStBlock = kStR * kStC;     // elements per lane per step
-constexpr int kStBuffers = 8;             // stream steps in flight per warp
-constexpr int kStPrefetch = 8;            // b / inbox prefetch distance (steps)
-constexpr int kStResync = 8;              // extra lag a band takes after catching up with the band above
+constexpr int kStSlots = 16;              // input ring: steps staged ahead of the compute warp
+constexpr int kStLook = 8;                // loader: copies in flight ahead of the step it hands over
+constexpr int kStOut = 8;                 // output ring between the compute and the store warp
 
 // Per step, per lane: kStBlock elements; per element NF doubles:
 //   fast : wu = -L[i,i-nx]/d, wl = -L[i,i-1]/d, rdg = 1/d
