@@ -17,7 +17,7 @@
 // The compute warp is the critical path, so it only shuffles, multiplies and
 // writes shared memory. Two helper warps run beside it (other SM
 // sub-partitions):
-//   * loader: streams the band's coefficient stream into a kStSlots ring with
+//   * loader: streams the band's coefficient stream into a st_slots() ring with
 //     TMA bulk copies (cp.async.bulk + mbarrier), gathers b with cp.async, and
 //     polls the band-above mailbox for each step before handing the step over —
 //     so the compute warp never waits on global memory;
@@ -127,13 +127,14 @@ enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutD
 
 template <bool EXACT>
 struct StSmem {
+  static constexpr int kSlots = st_slots(EXACT);
   static constexpr int kStep = st_step_bytes(EXACT);
-  static constexpr int kCoef = 0;                                      // [kStSlots][kStep]
-  static constexpr int kB = kCoef + kStSlots * kStep;                  // [kStSlots][lane][kStBlock] f64
-  static constexpr int kInbox = kB + kStSlots * kStLanes * kStBlock * 8;  // [kStSlots][kStC] f64
-  static constexpr int kOut = kInbox + kStSlots * kStC * 8;            // [kStOut][lane][kStBlock] f64
+  static constexpr int kCoef = 0;                                      // [kSlots][kStep]
+  static constexpr int kB = kCoef + kSlots * kStep;                    // [kSlots][lane][kStBlock] f64
+  static constexpr int kInbox = kB + kSlots * kStLanes * kStBlock * 8;  // [kSlots][kStC] f64
+  static constexpr int kOut = kInbox + kSlots * kStC * 8;              // [kStOut][lane][kStBlock] f64
   static constexpr int kBars = kOut + kStOut * kStLanes * kStBlock * 8;
-  static constexpr int kCtl = kBars + 8 * kStSlots;
+  static constexpr int kCtl = kBars + 8 * kSlots;
   static constexpr int kTotal = kCtl + 64;
 };
 
@@ -191,11 +192,13 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int y0 = t * kStBand + kStR * lane;
   const unsigned char* tstream = a.stream + (size_t)t * steps * S::kStep;
   const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
-  int issued = 0;
+  constexpr int NB = S::kSlots;
   bool ok = true;
+  // One mbarrier per ring slot completes when the step's coefficient bulk copy
+  // (lane 0's arrive.expect_tx) and all 32 lanes' b copies (cp.async arrivals)
+  // have landed: init count 33.
   auto issue = [&](int s) {
-    const int slot = s % kStSlots;
-    if (s >= kStSlots) ok = ok && wait_ctl(ctl, kCtlInDone, s - kStSlots + 1);  // slot consumed
+    const int slot = s % NB;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[slot], S::kStep);
@@ -213,43 +216,37 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
         }
       }
     }
-    cp_async_commit();
-    ++issued;
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[slot])) : "memory");
   };
-  auto retire = [&](int q, bool draining) {
-    const int slot = q % kStSlots;
+  auto settle = [&](int q) {
+    const int slot = q % NB;
     const unsigned ph = (phase_bits >> slot) & 1u;
     while (!mbar_try_wait(&bars[slot], ph)) {
     }
     phase_bits ^= 1u << slot;
-    if (draining) cp_async_wait<0>();
-    else cp_async_wait<kStLook>();
+  };
+  // Issue as far ahead as the ring allows (bounded by the compute warp's
+  // progress, never by the band above), hand steps over in order; only the
+  // hand-over waits on the band-above mailbox.
+  int issued = 0;
+  for (int q = 0; q < steps; ++q) {
+    const int done = ld_acquire_cta(ctl + kCtlInDone);
+    while (issued < steps && issued < done + NB) issue(issued++);
+    settle(q);
     if (lane == 0 && above && q < nblk) {  // lane 0's block at step q is column block q
 #pragma unroll
       for (int c = 0; c < kStC; ++c) {
         const unsigned long long u =
             st_poll(above + q * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
         if (u == kNotReady) ok = false;
-        inbox[slot * kStC + c] = __longlong_as_double((long long)u);
+        inbox[(q % NB) * kStC + c] = __longlong_as_double((long long)u);
       }
     }
     __syncwarp();
     if (lane == 0) st_release_cta(ctl + kCtlInReady, q + 1);
-  };
-  for (int s = 0; s < steps + kStLook; ++s) {
-    if (s < steps) issue(s);
-    const int q = s - kStLook;
-    if (q >= 0) retire(q, s >= steps);
     if (!__all_sync(0xffffffffu, ok)) {
-      // abort: settle the bulk copies in flight, then tell the other warps
-      for (int r = max(q + 1, 0); r < issued; ++r) {
-        const int slot = r % kStSlots;
-        const unsigned ph = (phase_bits >> slot) & 1u;
-        while (!mbar_try_wait(&bars[slot], ph)) {
-        }
-        phase_bits ^= 1u << slot;
-      }
-      cp_async_wait<0>();
+      // abort: settle the copies in flight, then tell the other warps
+      for (int r = q + 1; r < issued; ++r) settle(r);
       if (lane == 0) st_release_cta(ctl + kCtlAbort, 1);
       return;
     }
@@ -347,7 +344,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     }
     if (s + 1 < steps) {
       if (!wait_ctl(ctl, kCtlInReady, s + 2)) return false;
-      nxt.load(smem, (s + 1) % kStSlots, lane);
+      nxt.load(smem, (s + 1) % S::kSlots, lane);
     }
     return true;
   };
@@ -371,7 +368,7 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-    for (int k = 0; k < kStSlots; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1 + kStLanes);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned phase_bits = 0;
