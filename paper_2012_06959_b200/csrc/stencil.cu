@@ -15,15 +15,15 @@
 // mailboxes (the band's bottom grid row).
 //
 // The compute warp is the critical path, so it only shuffles, multiplies and
-// writes shared memory. Two helper warps run beside it (other SM
-// sub-partitions):
-//   * loader: streams the band's coefficient stream into a st_slots() ring with
-//     TMA bulk copies (cp.async.bulk + mbarrier), gathers b with cp.async, and
-//     polls the band-above mailbox for each step before handing the step over —
-//     so the compute warp never waits on global memory;
+// writes shared memory. Two helper warps run beside it on other SM
+// sub-partitions, and every hand-over is per chunk of kStG steps:
+//   * loader: per chunk, one TMA bulk copy of the coefficient stream plus one
+//     bulk copy per grid row of b (both complete on the slot's mbarrier), then
+//     the band-above mailbox values of the chunk's steps (polled), st_slots()
+//     chunks ahead — the compute warp never waits on global memory;
 //   * storer: writes the solved blocks from a shared-memory ring to x with
 //     16-byte stores.
-// Hand-offs are monotone step counters in shared memory (release/acquire at
+// Hand-overs are monotone chunk counters in shared memory (release/acquire at
 // CTA scope). No column indices are read: per element the solve moves 24 B of
 // coefficients (fast) + 8 B b + 8 B x.
 //
@@ -57,6 +57,7 @@ struct StArgs {
 };
 
 constexpr int kStBlkPairs = kStBlock / 2;
+constexpr int kStBRow = kStG * kStC;  // b doubles per lane-row per chunk
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
@@ -80,15 +81,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// step counters shared by the three warps of a CTA
+// chunk counters shared by the three warps of a CTA
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
   int v;
   asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
@@ -122,28 +115,43 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
   return u;
 }
 
-// control words of one task
+// control words of one task (chunk counters)
 enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5 };
 
 template <bool EXACT>
 struct StSmem {
   static constexpr int kSlots = st_slots(EXACT);
   static constexpr int kStep = st_step_bytes(EXACT);
-  static constexpr int kCoef = 0;                                      // [kSlots][kStep]
-  static constexpr int kB = kCoef + kSlots * kStep;                    // [kSlots][lane][kStBlock] f64
-  static constexpr int kInbox = kB + kSlots * kStLanes * kStBlock * 8;  // [kSlots][kStC] f64
-  static constexpr int kOut = kInbox + kSlots * kStC * 8;              // [kStOut][lane][kStBlock] f64
-  static constexpr int kBars = kOut + kStOut * kStLanes * kStBlock * 8;
+  static constexpr int kCoefChunk = kStG * kStep;
+  static constexpr int kBChunk = kStLanes * kStR * kStBRow * 8;
+  static constexpr int kCoef = 0;                                       // [kSlots][kStG][kStep]
+  static constexpr int kB = kCoef + kSlots * kCoefChunk;                // [kSlots][lane][r][kStBRow] f64
+  static constexpr int kInbox = kB + kSlots * kBChunk;                  // [kSlots][kStG][kStC] f64
+  static constexpr int kOut = kInbox + kSlots * kStG * kStC * 8;        // [kStOutSlots][kStG][lane][kStBlock] f64
+  static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
+  static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kCtl = kBars + 8 * kSlots;
   static constexpr int kTotal = kCtl + 64;
 };
 
-// Spin on a step counter; false when the task is being aborted.
-__device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need) {
+// Spin on a chunk counter; false when the task is being aborted or the
+// watchdog deadline passed (the caller then aborts the task).
+__device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, unsigned long long deadline) {
+  int polls = 0;
   while (ld_acquire_cta(ctl + which) < need) {
     if (ld_acquire_cta(ctl + kCtlAbort)) return false;
+    if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
   }
   return true;
+}
+
+// A wait failed (watchdog or a peer warp's abort): stop this task everywhere.
+__device__ __forceinline__ void abort_task(const StArgs& a, int* ctl, int lane) {
+  if (lane == 0) {
+    atomicExch(&a.status->code, 5);
+    atomicExch(a.abort_flag, 1);
+    st_release_cta(ctl + kCtlAbort, 1);
+  }
 }
 
 // One lane's inputs of one step, loaded a step ahead into registers.
@@ -152,139 +160,160 @@ struct StBlk {
   double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock], bv[kStBlock];
   double inbox[kStC];
 
-  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int lane) {
+  // step k of the chunk in input slot `slot`
+  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int k, int lane) {
     using S = StSmem<EXACT>;
-    const double2* cs = reinterpret_cast<const double2*>(smem + S::kCoef + slot * S::kStep);
-    const double2* bs = reinterpret_cast<const double2*>(smem + S::kB) + (slot * kStLanes + lane) * kStBlkPairs;
+    const double2* cs = reinterpret_cast<const double2*>(smem + S::kCoef + slot * S::kCoefChunk + k * S::kStep);
 #pragma unroll
-    for (int k = 0; k < kStBlkPairs; ++k) {
-      const double2 u = cs[(0 * kStBlkPairs + k) * kStLanes + lane];
-      const double2 l = cs[(1 * kStBlkPairs + k) * kStLanes + lane];
-      wu[2 * k] = u.x, wu[2 * k + 1] = u.y;
-      wl[2 * k] = l.x, wl[2 * k + 1] = l.y;
+    for (int p = 0; p < kStBlkPairs; ++p) {
+      const double2 u = cs[(0 * kStBlkPairs + p) * kStLanes + lane];
+      const double2 l = cs[(1 * kStBlkPairs + p) * kStLanes + lane];
+      wu[2 * p] = u.x, wu[2 * p + 1] = u.y;
+      wl[2 * p] = l.x, wl[2 * p + 1] = l.y;
       if (EXACT) {
-        const double2 d = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
-        const double2 r = cs[(3 * kStBlkPairs + k) * kStLanes + lane];
-        dd[2 * k] = d.x, dd[2 * k + 1] = d.y;
-        rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+        const double2 d = cs[(2 * kStBlkPairs + p) * kStLanes + lane];
+        const double2 r = cs[(3 * kStBlkPairs + p) * kStLanes + lane];
+        dd[2 * p] = d.x, dd[2 * p + 1] = d.y;
+        rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
       } else {
-        const double2 r = cs[(2 * kStBlkPairs + k) * kStLanes + lane];
-        rd[2 * k] = r.x, rd[2 * k + 1] = r.y;
+        const double2 r = cs[(2 * kStBlkPairs + p) * kStLanes + lane];
+        rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
       }
-      const double2 v = bs[k];
-      bv[2 * k] = v.x, bv[2 * k + 1] = v.y;
     }
-    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + slot * kStC;
+    const double* bb = reinterpret_cast<const double*>(smem + S::kB + slot * S::kBChunk) + lane * kStR * kStBRow;
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) {
+#pragma unroll
+      for (int c = 0; c < kStC; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(bb + r * kStBRow + k * kStC + c);
+        bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
+      }
+    }
+    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (slot * kStG + k) * kStC;
 #pragma unroll
     for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
   }
 };
 
-// ---- warp 1: stream coefficients, gather b, poll the band above ------------
+// ---- warp 1: stream coefficients and b, poll the band above -----------------
 template <bool EXACT>
 __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned& phase_bits,
                        unsigned long long deadline) {
   using S = StSmem<EXACT>;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-  double* bring = reinterpret_cast<double*>(smem + S::kB);
-  double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
-  const int steps = a.steps, nblk = a.nx / kStC;
-  const int y0 = t * kStBand + kStR * lane;
-  const unsigned char* tstream = a.stream + (size_t)t * steps * S::kStep;
-  const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
   constexpr int NB = S::kSlots;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
+  double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
+  const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
+  const int y0 = t * kStBand + kStR * lane;
+  const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+  const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
   bool ok = true;
-  // One mbarrier per ring slot completes when the step's coefficient bulk copy
-  // (lane 0's arrive.expect_tx) and all 32 lanes' b copies (cp.async arrivals)
-  // have landed: init count 33.
-  auto issue = [&](int s) {
-    const int slot = s % NB;
+  // chunk c: its coefficient block and, per lane and grid row, the b segment of
+  // column blocks [c*G - lane, c*G - lane + G) clipped to the grid
+  auto issue = [&](int c) {
+    const int slot = c % NB;
+    const int j0 = c * kStG - lane;
+    const int jlo = max(j0, 0), jhi = min(j0 + kStG, nblk);
+    unsigned my_bytes = 0;
+    if (jlo < jhi)
+      for (int r = 0; r < kStR; ++r)
+        if (y0 + r < a.ny) my_bytes += (unsigned)(jhi - jlo) * kStC * 8;
+    const unsigned b_bytes = __reduce_add_sync(0xffffffffu, my_bytes);
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[slot], S::kStep);
-      bulk_g2s(smem + S::kCoef + slot * S::kStep, tstream + (size_t)s * S::kStep, S::kStep, &bars[slot]);
+      mbar_expect_tx(&bars[slot], S::kCoefChunk + b_bytes);
+      bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk, &bars[slot]);
     }
-    const int j = s - lane;
-    if (j >= 0 && j < nblk) {
-      double* dst = bring + (slot * kStLanes + lane) * kStBlock;
+    __syncwarp();
+    if (jlo < jhi) {
+      double* dst = reinterpret_cast<double*>(smem + S::kB + slot * S::kBChunk) + lane * kStR * kStBRow;
 #pragma unroll
       for (int r = 0; r < kStR; ++r) {
-        if (y0 + r < a.ny) {
-          const double* src = a.b + (size_t)(y0 + r) * a.nx + j * kStC;
+        if (y0 + r < a.ny)
+          bulk_g2s(dst + r * kStBRow + (jlo - j0) * kStC, a.b + (size_t)(y0 + r) * a.nx + jlo * kStC,
+                   (unsigned)(jhi - jlo) * kStC * 8, &bars[slot]);
+      }
+    }
+  };
+  auto settle = [&](int c) -> bool {
+    const int slot = c % NB;
+    const unsigned ph = (phase_bits >> slot) & 1u;
+    int polls = 0;
+    while (!mbar_try_wait(&bars[slot], ph)) {
+      if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
+    }
+    phase_bits ^= 1u << slot;
+    return true;
+  };
+  // Issue as far ahead as the ring allows (bounded by the compute warp's
+  // progress, never by the band above); hand chunks over in order; only the
+  // hand-over waits on the band-above mailbox.
+  int issued = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int done = ld_acquire_cta(ctl + kCtlInDone);
+    while (issued < nchunks && issued < done + NB) issue(issued++);
+    while (ok && issued <= c) {  // chunk c itself must be in flight: wait for its slot
+      ok = wait_ctl(ctl, kCtlInDone, issued - NB + 1, deadline);
+      if (ok) issue(issued++);
+    }
+    if (ok) ok = settle(c);
+    if (ok && lane < kStG && above) {  // lane k fetches step c*G+k's row above (lane 0's block)
+      const int j = c * kStG + lane;
+      if (j < nblk) {
 #pragma unroll
-          for (int c = 0; c < kStC; c += 2) cp_async16(dst + r * kStC + c, src + c);
+        for (int q = 0; q < kStC; ++q) {
+          const unsigned long long u =
+              st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+          if (u == kNotReady) ok = false;
+          inbox[((c % NB) * kStG + lane) * kStC + q] = __longlong_as_double((long long)u);
         }
       }
     }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[slot])) : "memory");
-  };
-  auto settle = [&](int q) {
-    const int slot = q % NB;
-    const unsigned ph = (phase_bits >> slot) & 1u;
-    while (!mbar_try_wait(&bars[slot], ph)) {
-    }
-    phase_bits ^= 1u << slot;
-  };
-  // Issue as far ahead as the ring allows (bounded by the compute warp's
-  // progress, never by the band above), hand steps over in order; only the
-  // hand-over waits on the band-above mailbox.
-  int issued = 0;
-  for (int q = 0; q < steps; ++q) {
-    const int done = ld_acquire_cta(ctl + kCtlInDone);
-    while (issued < steps && issued < done + NB) issue(issued++);
-    settle(q);
-    if (lane == 0 && above && q < nblk) {  // lane 0's block at step q is column block q
-#pragma unroll
-      for (int c = 0; c < kStC; ++c) {
-        const unsigned long long u =
-            st_poll(above + q * kStC + c, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-        if (u == kNotReady) ok = false;
-        inbox[(q % NB) * kStC + c] = __longlong_as_double((long long)u);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) st_release_cta(ctl + kCtlInReady, q + 1);
-    if (!__all_sync(0xffffffffu, ok)) {
-      // abort: settle the copies in flight, then tell the other warps
-      for (int r = q + 1; r < issued; ++r) settle(r);
-      if (lane == 0) st_release_cta(ctl + kCtlAbort, 1);
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
+      abort_task(a, ctl, lane);
+      for (int r = c + 1; r < issued; ++r) settle(r);  // bounded by the deadline
       return;
     }
+    if (lane == 0) st_release_cta(ctl + kCtlInReady, c + 1);
   }
 }
 
 // ---- warp 2: solved blocks from shared memory to x --------------------------
 template <bool EXACT>
-__device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane) {
+__device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
   using S = StSmem<EXACT>;
-  const double2* out = reinterpret_cast<const double2*>(smem + S::kOut);
-  const int steps = a.steps, nblk = a.nx / kStC;
+  const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
-  for (int s = 0; s < steps; ++s) {
-    if (!wait_ctl(ctl, kCtlOutReady, s + 1)) return;
-    const int j = s - lane;
-    if (j >= 0 && j < nblk) {
-      const double2* src = out + ((s % kStOut) * kStLanes + lane) * kStBlkPairs;
+  for (int c = 0; c < nchunks; ++c) {
+    if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline)) return abort_task(a, ctl, lane);
+    const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
 #pragma unroll
-      for (int r = 0; r < kStR; ++r) {
-        if (y0 + r < a.ny) {
-          double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
+    for (int k = 0; k < kStG; ++k) {
+      const int j = c * kStG + k - lane;
+      if (j >= 0 && j < nblk) {
+        const double2* blk = src + (k * kStLanes + lane) * kStBlkPairs;
 #pragma unroll
-          for (int c = 0; c < kStC / 2; ++c) dst[c] = src[r * (kStC / 2) + c];
+        for (int r = 0; r < kStR; ++r) {
+          if (y0 + r < a.ny) {
+            double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
+#pragma unroll
+            for (int q = 0; q < kStC / 2; ++q) dst[q] = blk[r * (kStC / 2) + q];
+          }
         }
       }
     }
     __syncwarp();
-    if (lane == 0) st_release_cta(ctl + kCtlOutDone, s + 1);
+    if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
   }
 }
 
 // ---- warp 0: the lockstep wavefront -----------------------------------------
 template <bool EXACT>
-__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane) {
+__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
   using S = StSmem<EXACT>;
-  double2* out = reinterpret_cast<double2*>(smem + S::kOut);
-  const int steps = a.steps, nblk = a.nx / kStC;
+  constexpr int NB = S::kSlots;
+  const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const bool has_above = t > 0;
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
@@ -293,31 +322,33 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
   double bottom[kStC];
 #pragma unroll
-  for (int c = 0; c < kStC; ++c) bottom[c] = 0.0;
+  for (int q = 0; q < kStC; ++q) bottom[q] = 0.0;
 
-  auto step = [&](int s, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt) -> bool {
+  // step k of chunk c; `nxt` receives the next step's inputs
+  auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt) -> bool {
+    const int s = c * kStG + k;
     const int j = s - lane;
     const bool active = j >= 0 && j < nblk;
     double top[kStC];
 #pragma unroll
-    for (int c = 0; c < kStC; ++c) {
-      const double up = __shfl_up_sync(0xffffffffu, bottom[c], 1);
-      top[c] = lane == 0 ? (has_above ? cur.inbox[c] : 0.0) : up;
+    for (int q = 0; q < kStC; ++q) {
+      const double up = __shfl_up_sync(0xffffffffu, bottom[q], 1);
+      top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
     }
     double xb[kStR][kStC];
 #pragma unroll
     for (int r = 0; r < kStR; ++r) {
 #pragma unroll
-      for (int c = 0; c < kStC; ++c) {
-        const int e = r * kStC + c;
-        const double up = r == 0 ? top[c] : xb[r - 1][c];
-        const double left = c == 0 ? xleft[r] : xb[r][c - 1];
+      for (int q = 0; q < kStC; ++q) {
+        const int e = r * kStC + q;
+        const double up = r == 0 ? top[q] : xb[r - 1][q];
+        const double left = q == 0 ? xleft[r] : xb[r][q - 1];
         if (EXACT) {
           double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
           acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
-          xb[r][c] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
+          xb[r][q] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
         } else {
-          xb[r][c] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
+          xb[r][q] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
         }
       }
     }
@@ -325,39 +356,47 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
       for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
 #pragma unroll
-      for (int c = 0; c < kStC; ++c) bottom[c] = xb[kStR - 1][c];
+      for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
       if (publish) {
 #pragma unroll
-        for (int c = 0; c < kStC; ++c) st_relaxed_u64(below + j * kStC + c, publishable(bottom[c]));
+        for (int q = 0; q < kStC; ++q) st_relaxed_u64(below + j * kStC + q, publishable(bottom[q]));
       }
     }
-    if (s >= kStOut && !wait_ctl(ctl, kCtlOutDone, s - kStOut + 1)) return false;
-    double2* dst = out + ((s % kStOut) * kStLanes + lane) * kStBlkPairs;
+    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
+                   (k * kStLanes + lane) * kStBlkPairs;
 #pragma unroll
     for (int r = 0; r < kStR; ++r)
 #pragma unroll
-      for (int c = 0; c < kStC; c += 2) dst[r * (kStC / 2) + c / 2] = make_double2(xb[r][c], xb[r][c + 1]);
-    __syncwarp();
-    if (lane == 0) {
-      st_release_cta(ctl + kCtlOutReady, s + 1);
-      st_release_cta(ctl + kCtlInDone, s + 1);
-    }
-    if (s + 1 < steps) {
-      if (!wait_ctl(ctl, kCtlInReady, s + 2)) return false;
-      nxt.load(smem, (s + 1) % S::kSlots, lane);
+      for (int q = 0; q < kStC; q += 2) dst[r * (kStC / 2) + q / 2] = make_double2(xb[r][q], xb[r][q + 1]);
+    if (k + 1 < kStG) {
+      nxt.load(smem, c % NB, k + 1, lane);
+    } else {
+      // chunk boundary: hand over the outputs and the input slot, take the next chunk
+      __syncwarp();
+      if (lane == 0) {
+        st_release_cta(ctl + kCtlOutReady, c + 1);
+        st_release_cta(ctl + kCtlInDone, c + 1);
+      }
+      if (c + 1 < nchunks) {
+        if (!wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
+        if (c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline)) return false;
+        nxt.load(smem, (c + 1) % NB, 0, lane);
+      }
     }
     return true;
   };
 
   StBlk<EXACT> A, B;
-  if (!wait_ctl(ctl, kCtlInReady, 1)) return;
-  A.load(smem, 0, lane);
-  int s = 0;
-  for (; s + 1 < steps; s += 2) {
-    if (!step(s, A, B)) return;
-    if (!step(s + 1, B, A)) return;
+  if (!wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
+  A.load(smem, 0, 0, lane);
+  for (int c = 0; c < nchunks; ++c) {
+    static_assert(kStG % 2 == 0, "chunks hold an even number of steps");
+#pragma unroll
+    for (int k = 0; k < kStG; k += 2) {
+      if (!step(c, k, A, B)) return abort_task(a, ctl, lane);
+      if (!step(c, k + 1, B, A)) return abort_task(a, ctl, lane);
+    }
   }
-  if (s < steps) step(s, A, B);
 }
 
 template <bool EXACT>
@@ -368,7 +407,7 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1 + kStLanes);
+    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned phase_bits = 0;
@@ -381,9 +420,9 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
     __syncthreads();
     const int t = ctl[kCtlTask];
     if (t >= a.n_tasks) break;
-    if (warp == 0) compute<EXACT>(a, smem, ctl, t, lane);
+    if (warp == 0) compute<EXACT>(a, smem, ctl, t, lane, deadline);
     else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
-    else storer<EXACT>(a, smem, ctl, t, lane);
+    else storer<EXACT>(a, smem, ctl, t, lane, deadline);
     __syncthreads();
     if (ctl[kCtlAbort]) break;
   }
@@ -441,7 +480,8 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   stencil.nx = nx;
   stencil.ny = (int)(n / nx);
   stencil.n_tasks = (stencil.ny + kStBand - 1) / kStBand;
-  stencil.steps_per_task = nx / kStC + kStLanes - 1;
+  const int raw_steps = nx / kStC + kStLanes - 1;
+  stencil.steps_per_task = (raw_steps + kStG - 1) / kStG * kStG;
   const int NF = st_fields(exact);
   const size_t step_bytes = st_step_bytes(exact);
   const size_t bytes = step_bytes * stencil.steps_per_task * stencil.n_tasks;

@@ -16,10 +16,8 @@ constexpr int kStC = 4;
 constexpr int kStLanes = 32;
 constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one CTA)
 constexpr int kStBlock = kStR * kStC;     // elements per lane per step
-// input ring: steps staged ahead of the compute warp. At ~0.1 us per step and
-// ~1.5 us DRAM latency the ring must cover ~16+ steps in flight.
-__host__ __device__ constexpr int st_slots(bool exact) { return exact ? 18 : 24; }
-constexpr int kStOut = 8;                 // output ring between the compute and the store warp
+constexpr int kStG = 4;                   // steps per ring slot ("chunk"): the unit of every hand-over
+constexpr int kStOutSlots = 3;            // output ring (chunks) between the compute and the store warp
 
 // Per step, per lane: kStBlock elements; per element NF doubles:
 //   fast : wu = -L[i,i-nx]/d, wl = -L[i,i-1]/d, rdg = 1/d
@@ -28,13 +26,16 @@ constexpr int kStOut = 8;                 // output ring between the compute and
 // pair of doubles with one conflict-free 16-byte shared load.
 __host__ __device__ constexpr int st_fields(bool exact) { return exact ? 4 : 3; }
 __host__ __device__ constexpr int st_step_bytes(bool exact) { return st_fields(exact) * kStBlock * kStLanes * 8; }
+// Input ring depth in chunks: (slots - 1) * kStG steps of copies stay in flight
+// (~20 steps at ~0.1 us per step covers the ~1.5 us DRAM latency).
+__host__ __device__ constexpr int st_slots(bool exact) { return exact ? 4 : 5; }
 
 struct StencilPlan {
   bool ready = false;
   bool exact = true;
   int nx = 0, ny = 0;
   int n_tasks = 0;
-  int steps_per_task = 0;  // nx / kStC + kStLanes - 1
+  int steps_per_task = 0;  // nx / kStC + kStLanes - 1, rounded up to a multiple of kStG
   long long stream_bytes = 0;
   double build_ms = 0.0;
   unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
