@@ -54,7 +54,14 @@ struct StArgs {
   unsigned long long timeout_ns;
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
+  long long* dbg;  // diagnostics (probe_flags & 16): per-chunk clock stamps of task 0, chunks [64, 128)
 };
+constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
+__device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
+  return (a.dbg && t == 0 && lane == 0 && c >= kStProbeFirst && c < kStProbeFirst + kStProbeChunks)
+             ? a.dbg + 6 * (c - kStProbeFirst) + slot
+             : nullptr;
+}
 
 constexpr int kStBlkPairs = kStBlock / 2;
 constexpr int kStBRow = kStG * kStC;  // b doubles per lane-row per chunk
@@ -250,13 +257,16 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // hand-over waits on the band-above mailbox.
   int issued = 0;
   for (int c = 0; c < nchunks; ++c) {
+    if (long long* p = st_stamp(a, t, c, lane, 2)) *p = clock64();
     const int done = ld_acquire_cta(ctl + kCtlInDone);
     while (issued < nchunks && issued < done + NB) issue(issued++);
     while (ok && issued <= c) {  // chunk c itself must be in flight: wait for its slot
       ok = wait_ctl(ctl, kCtlInDone, issued - NB + 1, deadline);
       if (ok) issue(issued++);
     }
+    if (long long* p = st_stamp(a, t, c, lane, 3)) *p = clock64();
     if (ok) ok = settle(c);
+    if (long long* p = st_stamp(a, t, c, lane, 4)) *p = clock64();
     if (ok && lane < kStG && above) {  // lane k fetches step c*G+k's row above (lane 0's block)
       const int j = c * kStG + lane;
       if (j < nblk) {
@@ -276,6 +286,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       return;
     }
     if (lane == 0) st_release_cta(ctl + kCtlInReady, c + 1);
+    if (long long* p = st_stamp(a, t, c, lane, 5)) *p = clock64();
   }
 }
 
@@ -378,7 +389,9 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
         st_release_cta(ctl + kCtlInDone, c + 1);
       }
       if (c + 1 < nchunks) {
+        if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
         if (!wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
+        if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
         if (c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline)) return false;
         nxt.load(smem, (c + 1) % NB, 0, lane);
       }
@@ -561,6 +574,12 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.ny = stencil.ny;
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
+  if (opt.probe_flags & 16) {
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, "probe buffer");
+    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 6 * 64, s);
+    a.dbg = probe_buf;
+  }
   const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);

@@ -1,6 +1,7 @@
-"""Stencil executor experiments (GPU): per-band step time vs band count.
+"""Stencil executor experiments (GPU): per-band step time vs band count, and
+per-chunk clock stamps of the compute and loader warps (--clock).
 
-    python tools/stencil_exp.py
+    python tools/stencil_exp.py [--clock]
 """
 
 import json
@@ -33,7 +34,34 @@ def run(ny, precision="fast", nx=4096):
           flush=True)
 
 
+def clock(ny=64, precision="fast"):
+    l = synth.lap2d(4096, ny)
+    p = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
+                           probe_flags=16)
+    b = np.ones(l.n)
+    p.solve(b)
+    p.solve(b)
+    st = p.probe_stamps(6).astype(np.float64)
+    # compute: [0] before waiting for the chunk, [1] after; loader: [2] loop top, [3] before settle,
+    # [4] after settle, [5] after hand-over
+    rec = {
+        "compute_chunk_period": float(np.median(np.diff(st[:, 1]))),
+        "compute_wait": float(np.median(st[:, 1] - st[:, 0])),
+        "loader_chunk_period": float(np.median(np.diff(st[:, 2]))),
+        "loader_issue": float(np.median(st[:, 3] - st[:, 2])),
+        "loader_settle": float(np.median(st[:, 4] - st[:, 3])),
+        "loader_handover": float(np.median(st[:, 5] - st[:, 4])),
+        "loader_ahead_of_compute": float(np.median(st[:, 1] - st[:, 5])),
+    }
+    print(json.dumps({"ny": ny, "precision": precision, "cycles": rec}), flush=True)
+    p.close()
+
+
 def main():
+    if "--clock" in sys.argv:
+        clock(64)
+        clock(256)
+        return
     for ny in (64, 128, 256, 1024, 4096):
         run(ny)
     run(4096, precision="exact")
