@@ -55,6 +55,7 @@ struct StArgs {
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
   long long* dbg;  // diagnostics (probe_flags & 16): per-chunk clock stamps of task 0, chunks [64, 128)
+  int probe;       // diagnostics: bit 2 = fetch b as one contiguous bulk copy (timing only, wrong x)
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -225,14 +226,18 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     if (jlo < jhi)
       for (int r = 0; r < kStR; ++r)
         if (y0 + r < a.ny) my_bytes += (unsigned)(jhi - jlo) * kStC * 8;
-    const unsigned b_bytes = __reduce_add_sync(0xffffffffu, my_bytes);
+    const bool contiguous_b = (a.probe & 2) != 0;
+    const unsigned b_bytes = contiguous_b ? (unsigned)S::kBChunk : __reduce_add_sync(0xffffffffu, my_bytes);
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[slot], S::kCoefChunk + b_bytes);
       bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk, &bars[slot]);
+      if (contiguous_b)
+        bulk_g2s(smem + S::kB + slot * S::kBChunk, a.b + ((size_t)c * (S::kBChunk / 8)) % ((size_t)a.nx * a.ny - S::kBChunk / 8),
+                 S::kBChunk, &bars[slot]);
     }
     __syncwarp();
-    if (jlo < jhi) {
+    if (jlo < jhi && !contiguous_b) {
       double* dst = reinterpret_cast<double*>(smem + S::kB + slot * S::kBChunk) + lane * kStR * kStBRow;
 #pragma unroll
       for (int r = 0; r < kStR; ++r) {
@@ -574,6 +579,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.ny = stencil.ny;
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
+  a.probe = opt.probe_flags;
   if (opt.probe_flags & 16) {
     if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, "probe buffer");

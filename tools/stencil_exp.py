@@ -34,10 +34,10 @@ def run(ny, precision="fast", nx=4096):
           flush=True)
 
 
-def clock(ny=64, precision="fast"):
+def clock(ny=64, precision="fast", extra=0):
     l = synth.lap2d(4096, ny)
     p = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
-                           probe_flags=16)
+                           probe_flags=16 | extra)
     b = np.ones(l.n)
     p.solve(b)
     p.solve(b)
@@ -53,14 +53,18 @@ def clock(ny=64, precision="fast"):
         "loader_handover": float(np.median(st[:, 5] - st[:, 4])),
         "loader_ahead_of_compute": float(np.median(st[:, 1] - st[:, 5])),
     }
-    print(json.dumps({"ny": ny, "precision": precision, "cycles": rec}), flush=True)
+    _, stt = p.solve(b)
+    print(json.dumps({"ny": ny, "precision": precision, "probe": extra, "kernel_ms": round(stt["kernel_ms"], 4),
+                      "cycles": rec}), flush=True)
     p.close()
 
 
 def main():
     if "--clock" in sys.argv:
         clock(64)
-        clock(256)
+        clock(64, extra=2)
+        clock(4096)
+        clock(4096, extra=2)
         return
     for ny in (64, 128, 256, 1024, 4096):
         run(ny)
