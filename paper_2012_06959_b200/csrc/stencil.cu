@@ -17,8 +17,8 @@
 // The compute warp is the critical path, so it only shuffles, multiplies and
 // writes shared memory. Two helper warps run beside it on other SM
 // sub-partitions, and every hand-over is per chunk of kStG steps:
-//   * loader: per chunk, one TMA bulk copy of the coefficient stream plus one
-//     bulk copy per grid row of b (both complete on the slot's mbarrier), then
+//   * loader: per chunk, one TMA bulk copy of the coefficient stream plus a
+//     16-byte cp.async gather of b (both complete on the slot's mbarrier), then
 //     the band-above mailbox values of the chunk's steps (polled), st_slots()
 //     chunks ahead — the compute warp never waits on global memory;
 //   * storer: writes the solved blocks from a shared-memory ring to x with
@@ -55,7 +55,10 @@ struct StArgs {
   int spin_initial, spin_max_ns;
   int nx, ny, n_tasks, steps;
   long long* dbg;  // diagnostics (probe_flags & 16): per-chunk clock stamps of task 0, chunks [64, 128)
-  int probe;       // diagnostics: bit 2 = fetch b as one contiguous bulk copy (timing only, wrong x)
+  int probe;       // diagnostics flags (probe_flags)
+  int nap;         // helper-warp sleep between control-word polls (ns)
+  int b_aligned;   // b is 16-byte aligned: gather it with 16-byte cp.async (else 8-byte)
+  int x_aligned;   // x is 16-byte aligned: 16-byte stores (else 8-byte)
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -65,7 +68,10 @@ __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, in
 }
 
 constexpr int kStBlkPairs = kStBlock / 2;
-constexpr int kStBRow = kStG * kStC;  // b doubles per lane-row per chunk
+// Shared-memory rings keep 16-byte pairs lane-innermost ([...][pair][lane]) so
+// every warp-wide 16-byte access touches 512 consecutive bytes (4 wavefronts,
+// no bank conflicts). b pair index of grid row r, chunk step k, column pair h:
+__host__ __device__ constexpr int st_b_pair(int r, int k, int h) { return (r * kStG + k) * (kStC / 2) + h; }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
@@ -88,6 +94,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// arrive on `bar` once all of this thread's earlier cp.async have landed
+__device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // chunk counters shared by the three warps of a CTA
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
@@ -131,11 +147,11 @@ struct StSmem {
   static constexpr int kSlots = st_slots(EXACT);
   static constexpr int kStep = st_step_bytes(EXACT);
   static constexpr int kCoefChunk = kStG * kStep;
-  static constexpr int kBChunk = kStLanes * kStR * kStBRow * 8;
+  static constexpr int kBChunk = kStLanes * kStR * kStG * kStC * 8;
   static constexpr int kCoef = 0;                                       // [kSlots][kStG][kStep]
-  static constexpr int kB = kCoef + kSlots * kCoefChunk;                // [kSlots][lane][r][kStBRow] f64
+  static constexpr int kB = kCoef + kSlots * kCoefChunk;                // [kSlots][r][k][pair][lane] f64x2
   static constexpr int kInbox = kB + kSlots * kBChunk;                  // [kSlots][kStG][kStC] f64
-  static constexpr int kOut = kInbox + kSlots * kStG * kStC * 8;        // [kStOutSlots][kStG][lane][kStBlock] f64
+  static constexpr int kOut = kInbox + kSlots * kStG * kStC * 8;        // [kStOutSlots][kStG][pair][lane] f64x2
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kCtl = kBars + 8 * kSlots;
@@ -144,11 +160,15 @@ struct StSmem {
 
 // Spin on a chunk counter; false when the task is being aborted or the
 // watchdog deadline passed (the caller then aborts the task).
-__device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, unsigned long long deadline) {
+// Helper warps pass nap > 0: they sleep between polls so their spinning does
+// not compete with the compute warp for the shared-memory pipe.
+__device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, unsigned long long deadline,
+                                         int nap = 0) {
   int polls = 0;
   while (ld_acquire_cta(ctl + which) < need) {
     if (ld_acquire_cta(ctl + kCtlAbort)) return false;
     if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
+    if (nap) __nanosleep(nap);
   }
   return true;
 }
@@ -188,12 +208,12 @@ struct StBlk {
         rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
       }
     }
-    const double* bb = reinterpret_cast<const double*>(smem + S::kB + slot * S::kBChunk) + lane * kStR * kStBRow;
+    const double2* bb = reinterpret_cast<const double2*>(smem + S::kB + slot * S::kBChunk) + lane;
 #pragma unroll
     for (int r = 0; r < kStR; ++r) {
 #pragma unroll
       for (int c = 0; c < kStC; c += 2) {
-        const double2 v = *reinterpret_cast<const double2*>(bb + r * kStBRow + k * kStC + c);
+        const double2 v = bb[st_b_pair(r, k, c / 2) * kStLanes];
         bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
       }
     }
@@ -218,34 +238,42 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   bool ok = true;
   // chunk c: its coefficient block and, per lane and grid row, the b segment of
   // column blocks [c*G - lane, c*G - lane + G) clipped to the grid
+  // The coefficient block is one TMA bulk copy (lane 0, expect_tx arrival);
+  // b is gathered by every lane with 16-byte cp.async (one warp instruction
+  // moves 512 B; a bulk copy per grid row would queue 64 small TMA operations
+  // per chunk), whose completion arrives on the same slot mbarrier (.noinc:
+  // the barrier counts 1 + 32 arrivals).
   auto issue = [&](int c) {
     const int slot = c % NB;
     const int j0 = c * kStG - lane;
-    const int jlo = max(j0, 0), jhi = min(j0 + kStG, nblk);
-    unsigned my_bytes = 0;
-    if (jlo < jhi)
-      for (int r = 0; r < kStR; ++r)
-        if (y0 + r < a.ny) my_bytes += (unsigned)(jhi - jlo) * kStC * 8;
-    const bool contiguous_b = (a.probe & 2) != 0;
-    const unsigned b_bytes = contiguous_b ? (unsigned)S::kBChunk : __reduce_add_sync(0xffffffffu, my_bytes);
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[slot], S::kCoefChunk + b_bytes);
+      mbar_expect_tx(&bars[slot], S::kCoefChunk);
       bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk, &bars[slot]);
-      if (contiguous_b)
-        bulk_g2s(smem + S::kB + slot * S::kBChunk, a.b + ((size_t)c * (S::kBChunk / 8)) % ((size_t)a.nx * a.ny - S::kBChunk / 8),
-                 S::kBChunk, &bars[slot]);
     }
-    __syncwarp();
-    if (jlo < jhi && !contiguous_b) {
-      double* dst = reinterpret_cast<double*>(smem + S::kB + slot * S::kBChunk) + lane * kStR * kStBRow;
+    double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk) + lane;
 #pragma unroll
-      for (int r = 0; r < kStR; ++r) {
-        if (y0 + r < a.ny)
-          bulk_g2s(dst + r * kStBRow + (jlo - j0) * kStC, a.b + (size_t)(y0 + r) * a.nx + jlo * kStC,
-                   (unsigned)(jhi - jlo) * kStC * 8, &bars[slot]);
+    for (int r = 0; r < kStR; ++r) {
+      if (y0 + r >= a.ny) continue;
+      const double* src = a.b + (size_t)(y0 + r) * a.nx;
+#pragma unroll
+      for (int k = 0; k < kStG; ++k) {
+        const int jb = j0 + k;
+        if (jb < 0 || jb >= nblk) continue;
+#pragma unroll
+        for (int h = 0; h < kStC / 2; ++h) {
+          double2* d = dst + st_b_pair(r, k, h) * kStLanes;
+          const double* s = src + jb * kStC + 2 * h;
+          if (a.b_aligned) {
+            cp_async16(d, s);
+          } else {
+            cp_async8(&d->x, s);
+            cp_async8(&d->y, s + 1);
+          }
+        }
       }
     }
+    cp_async_arrive_noinc(&bars[slot]);
   };
   auto settle = [&](int c) -> bool {
     const int slot = c % NB;
@@ -266,22 +294,22 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     const int done = ld_acquire_cta(ctl + kCtlInDone);
     while (issued < nchunks && issued < done + NB) issue(issued++);
     while (ok && issued <= c) {  // chunk c itself must be in flight: wait for its slot
-      ok = wait_ctl(ctl, kCtlInDone, issued - NB + 1, deadline);
+      ok = wait_ctl(ctl, kCtlInDone, issued - NB + 1, deadline, a.nap);
       if (ok) issue(issued++);
     }
     if (long long* p = st_stamp(a, t, c, lane, 3)) *p = clock64();
     if (ok) ok = settle(c);
     if (long long* p = st_stamp(a, t, c, lane, 4)) *p = clock64();
-    if (ok && lane < kStG && above) {  // lane k fetches step c*G+k's row above (lane 0's block)
-      const int j = c * kStG + lane;
+    if (ok && lane < kStG * kStC && above) {
+      // the chunk's row-above values (lane 0's blocks of steps c*G..c*G+G-1):
+      // one value per lane, so the chunk costs one L2 round trip
+      const int k = lane / kStC, q = lane % kStC;
+      const int j = c * kStG + k;
       if (j < nblk) {
-#pragma unroll
-        for (int q = 0; q < kStC; ++q) {
-          const unsigned long long u =
-              st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-          if (u == kNotReady) ok = false;
-          inbox[((c % NB) * kStG + lane) * kStC + q] = __longlong_as_double((long long)u);
-        }
+        const unsigned long long u =
+            st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+        if (u == kNotReady) ok = false;
+        inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
       }
     }
     ok = __all_sync(0xffffffffu, ok);
@@ -302,19 +330,29 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
   for (int c = 0; c < nchunks; ++c) {
-    if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline)) return abort_task(a, ctl, lane);
+    if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
     const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
 #pragma unroll
     for (int k = 0; k < kStG; ++k) {
       const int j = c * kStG + k - lane;
       if (j >= 0 && j < nblk) {
-        const double2* blk = src + (k * kStLanes + lane) * kStBlkPairs;
+        const double2* blk = src + k * kStBlkPairs * kStLanes + lane;
 #pragma unroll
         for (int r = 0; r < kStR; ++r) {
           if (y0 + r < a.ny) {
-            double2* dst = reinterpret_cast<double2*>(a.x + (size_t)(y0 + r) * a.nx + j * kStC);
+            double* row = a.x + (size_t)(y0 + r) * a.nx + j * kStC;
+            if (a.x_aligned) {
 #pragma unroll
-            for (int q = 0; q < kStC / 2; ++q) dst[q] = blk[r * (kStC / 2) + q];
+              for (int q = 0; q < kStC / 2; ++q)
+                reinterpret_cast<double2*>(row)[q] = blk[(r * (kStC / 2) + q) * kStLanes];
+            } else {
+#pragma unroll
+              for (int q = 0; q < kStC / 2; ++q) {
+                const double2 v = blk[(r * (kStC / 2) + q) * kStLanes];
+                row[2 * q] = v.x;
+                row[2 * q + 1] = v.y;
+              }
+            }
           }
         }
       }
@@ -379,11 +417,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       }
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
-                   (k * kStLanes + lane) * kStBlkPairs;
+                   k * kStBlkPairs * kStLanes + lane;
 #pragma unroll
     for (int r = 0; r < kStR; ++r)
 #pragma unroll
-      for (int q = 0; q < kStC; q += 2) dst[r * (kStC / 2) + q / 2] = make_double2(xb[r][q], xb[r][q + 1]);
+      for (int q = 0; q < kStC; q += 2)
+        dst[(r * (kStC / 2) + q / 2) * kStLanes] = make_double2(xb[r][q], xb[r][q + 1]);
     if (k + 1 < kStG) {
       nxt.load(smem, c % NB, k + 1, lane);
     } else {
@@ -425,7 +464,7 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1 + kStLanes);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned phase_bits = 0;
@@ -580,6 +619,9 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.n_tasks = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
   a.probe = opt.probe_flags;
+  a.b_aligned = ((uintptr_t)d_b & 15) == 0;
+  a.x_aligned = ((uintptr_t)d_x & 15) == 0;
+  a.nap = (opt.probe_flags & 4) ? (opt.probe_flags >> 8) & 1023 : 64;  // probe bit 4: override the nap
   if (opt.probe_flags & 16) {
     if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, "probe buffer");

@@ -182,6 +182,24 @@ def test_device_resident_solve_matches_host_path():
     assert dx.cpu().numpy().tobytes() == x_host.tobytes()
 
 
+@pytest.mark.parametrize("executor", ["stencil", "chains", "rows"])
+def test_device_resident_unaligned_vectors(executor):
+    """b and x only 8-byte aligned (views at an odd element offset)."""
+    torch = pytest.importorskip("torch")
+    l = _random_coefficients(synth.lap2d(128, 70), 5)
+    b = np.random.default_rng(4).uniform(-1, 1, l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor=executor)
+    db = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+    db[1:] = torch.from_numpy(b).cuda()
+    dx = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    plan.solve_device_async(db[1:].data_ptr(), dx[1:].data_ptr(), torch.cuda.current_stream().cuda_stream)
+    plan.synchronize()
+    assert dx[1:].cpu().numpy().tobytes() == ref.tobytes()
+    plan.close()
+
+
 def _random_coefficients(l, seed):
     """Same structure, random off-diagonals in [-1, 1], dominant diagonal."""
     rng = np.random.default_rng(seed)
