@@ -250,11 +250,21 @@ class NativePlan:
     def segment_ptr(self) -> int:
         return int(self._lib.sptrsv_plan_segment(self._h) or 0)
 
-    def probe_stamps(self, per_step: int = 5) -> np.ndarray:
-        out = np.zeros(per_step * 64, dtype=np.int64)
+    _PROBE_WORDS = 6 * 64 + 3 * 1024  # DevicePlan::kProbeWords
+
+    def _probe_raw(self) -> np.ndarray:
+        out = np.zeros(self._PROBE_WORDS, dtype=np.int64)
         rc = self._lib.sptrsv_plan_probe_read(self._h, _ptr(out, C.c_int64), out.size)
         raise_for_status(rc, _err(self._lib))
-        return out.reshape(64, per_step)
+        return out
+
+    def probe_stamps(self, per_step: int = 5) -> np.ndarray:
+        """Per-step (chains) or per-chunk (stencil) clock stamps, [64, per_step]."""
+        return self._probe_raw()[: per_step * 64].reshape(64, per_step)
+
+    def probe_tasks(self, n_tasks: int) -> np.ndarray:
+        """Stencil per-task globaltimer stamps [n_tasks, 3]: start, first chunk ready, end (ns)."""
+        return self._probe_raw()[6 * 64: 6 * 64 + 3 * min(n_tasks, 1024)].reshape(-1, 3)
 
     def in_degrees(self) -> np.ndarray:
         out = np.empty(self.n, dtype=np.int64)

@@ -427,7 +427,8 @@ int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count)
   if (!p || !out) return fail(SPTRSV_E_ARGUMENT, "null argument");
   if (!p->probe_buf) return fail(SPTRSV_E_ARGUMENT, "no probe data: set options.probe_flags");
   CUDA_TRY(cudaSetDevice(p->device));
-  CUDA_TRY(cudaMemcpy(out, p->probe_buf, sizeof(long long) * std::min(count, 6 * 64), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, p->probe_buf, sizeof(long long) * std::min<int>(count, DevicePlan::kProbeWords),
+                      cudaMemcpyDeviceToHost));
   return SPTRSV_OK;
 }
 

@@ -67,7 +67,10 @@ struct DevicePlan {
   int set_partition(const int32_t* owner, int pes, int my_pe);
   int solve_partitioned_rows(const double* d_b, double* d_x, cudaStream_t s);
   void release_partition();
-  long long* probe_buf = nullptr;  // diagnostics (probe_flags)
+  // diagnostics (probe_flags): kProbeWords int64 — per-step/chunk clock stamps
+  // [0, 384), then per-task globaltimer stamps [384, 384 + 3 * 1024)
+  static constexpr int kProbeWords = 6 * 64 + 3 * 1024;
+  long long* probe_buf = nullptr;
   int executor_used = SPTRSV_EXECUTOR_ROWS;
 
   double setup_ms = 0.0;

@@ -385,7 +385,8 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.spin_max_ns = opt.spin_max_ns;
   const bool probe = (opt.probe_flags & kProbeClock) != 0;
   if (probe) {
-    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * kProbeSteps) != cudaSuccess)
+    static_assert(6 * kProbeSteps <= kProbeWords, "probe buffer");
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * kProbeWords) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, "probe buffer");
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 5 * kProbeSteps, s);
     a.dbg = probe_buf;

@@ -62,7 +62,9 @@ struct StArgs {
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
-  return (a.dbg && t == 0 && lane == 0 && c >= kStProbeFirst && c < kStProbeFirst + kStProbeChunks)
+  // probe bit 64: stamp task 1 (a band with a band above) instead of task 0
+  return (a.dbg && t == ((a.probe & 64) ? 1 : 0) && lane == 0 && c >= kStProbeFirst &&
+          c < kStProbeFirst + kStProbeChunks)
              ? a.dbg + 6 * (c - kStProbeFirst) + slot
              : nullptr;
 }
@@ -100,6 +102,13 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// predicated relaxed store (no branch around it)
+__device__ __forceinline__ void st_relaxed_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.gpu.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v),
+      "r"((int)pred)
+      : "memory");
 }
 // arrive on `bar` once all of this thread's earlier cp.async have landed
 __device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
@@ -363,7 +372,10 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 }
 
 // ---- warp 0: the lockstep wavefront -----------------------------------------
-template <bool EXACT>
+// ABL: compile-time ablations for timing experiments only (0 in production):
+// 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
+// active/publish branch
+template <bool EXACT, int ABL>
 __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
@@ -371,6 +383,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   const bool has_above = t > 0;
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
+  const bool solo = (a.probe & 32) != 0;  // diagnostics: run without the helper warps
   double xleft[kStR];
 #pragma unroll
   for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
@@ -386,7 +399,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     double top[kStC];
 #pragma unroll
     for (int q = 0; q < kStC; ++q) {
-      const double up = __shfl_up_sync(0xffffffffu, bottom[q], 1);
+      const double up = (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
       top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
     }
     double xb[kStR][kStC];
@@ -406,15 +419,15 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
         }
       }
     }
-    if (active) {
+    // branch-free: a divergent branch here costs more than the whole FMA chain
 #pragma unroll
-      for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
+    for (int r = 0; r < kStR; ++r) xleft[r] = ((ABL & 8) || active) ? xb[r][kStC - 1] : xleft[r];
 #pragma unroll
-      for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
-      if (publish) {
+    for (int q = 0; q < kStC; ++q) bottom[q] = ((ABL & 8) || active) ? xb[kStR - 1][q] : bottom[q];
+    if (!(ABL & 8)) {
 #pragma unroll
-        for (int q = 0; q < kStC; ++q) st_relaxed_u64(below + j * kStC + q, publishable(bottom[q]));
-      }
+      for (int q = 0; q < kStC; ++q)
+        st_relaxed_u64_if(below + j * kStC + q, publishable(bottom[q]), publish && active);
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
                    k * kStBlkPairs * kStLanes + lane;
@@ -422,9 +435,9 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     for (int r = 0; r < kStR; ++r)
 #pragma unroll
       for (int q = 0; q < kStC; q += 2)
-        dst[(r * (kStC / 2) + q / 2) * kStLanes] = make_double2(xb[r][q], xb[r][q + 1]);
+        if (!(ABL & 1)) dst[(r * (kStC / 2) + q / 2) * kStLanes] = make_double2(xb[r][q], xb[r][q + 1]);
     if (k + 1 < kStG) {
-      nxt.load(smem, c % NB, k + 1, lane);
+      if (!(ABL & 2)) nxt.load(smem, c % NB, k + 1, lane);
     } else {
       // chunk boundary: hand over the outputs and the input slot, take the next chunk
       __syncwarp();
@@ -434,17 +447,22 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       }
       if (c + 1 < nchunks) {
         if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-        if (!wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
+        if (!solo && !wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
         if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
-        if (c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline)) return false;
+        if (!solo && c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline))
+          return false;
         nxt.load(smem, (c + 1) % NB, 0, lane);
       }
     }
     return true;
   };
 
+  // diagnostics: per-task globaltimer stamps (start, first chunk ready, end)
+  long long* tstamp = (a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
+  if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> A, B;
-  if (!wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
+  if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
+  if (tstamp) tstamp[1] = (long long)globaltimer_ns();
   A.load(smem, 0, 0, lane);
   for (int c = 0; c < nchunks; ++c) {
     static_assert(kStG % 2 == 0, "chunks hold an even number of steps");
@@ -454,9 +472,10 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       if (!step(c, k + 1, B, A)) return abort_task(a, ctl, lane);
     }
   }
+  if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
-template <bool EXACT>
+template <bool EXACT, int ABL>
 __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -477,25 +496,43 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
     __syncthreads();
     const int t = ctl[kCtlTask];
     if (t >= a.n_tasks) break;
-    if (warp == 0) compute<EXACT>(a, smem, ctl, t, lane, deadline);
-    else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
+    if (warp == 0) compute<EXACT, ABL>(a, smem, ctl, t, lane, deadline);
+    else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
+    } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
     else storer<EXACT>(a, smem, ctl, t, lane, deadline);
     __syncthreads();
     if (ctl[kCtlAbort]) break;
   }
 }
 
-template <bool EXACT>
-cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
+template <bool EXACT, int ABL>
+cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_stencil2d<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, StSmem<EXACT>::kTotal);
+    cudaError_t e = cudaFuncSetAttribute(k_stencil2d<EXACT, ABL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         StSmem<EXACT>::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stencil2d<EXACT><<<blocks, 96, StSmem<EXACT>::kTotal, s>>>(a);
+  k_stencil2d<EXACT, ABL><<<blocks, 96, StSmem<EXACT>::kTotal, s>>>(a);
   return cudaGetLastError();
+}
+
+// probe bits 12..15 select an ablation variant of the fast kernel (timing only)
+template <bool EXACT>
+cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
+  if (!EXACT) {
+    switch ((a.probe >> 12) & 15) {
+      case 1: return launch_stencil_v<EXACT, 1>(a, blocks, s);
+      case 2: return launch_stencil_v<EXACT, 2>(a, blocks, s);
+      case 3: return launch_stencil_v<EXACT, 3>(a, blocks, s);
+      case 4: return launch_stencil_v<EXACT, 4>(a, blocks, s);
+      case 8: return launch_stencil_v<EXACT, 8>(a, blocks, s);
+      case 15: return launch_stencil_v<EXACT, 15>(a, blocks, s);
+      default: break;
+    }
+  }
+  return launch_stencil_v<EXACT, 0>(a, blocks, s);
 }
 
 }  // namespace
@@ -623,9 +660,9 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
   a.nap = (opt.probe_flags & 4) ? (opt.probe_flags >> 8) & 1023 : 64;  // probe bit 4: override the nap
   if (opt.probe_flags & 16) {
-    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * 6 * 64) != cudaSuccess)
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * kProbeWords) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, "probe buffer");
-    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * 6 * 64, s);
+    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
     a.dbg = probe_buf;
   }
   const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));

@@ -59,12 +59,42 @@ def clock(ny=64, precision="fast", extra=0):
     p.close()
 
 
+def tasks(ny=4096, precision="fast"):
+    """Per-band timeline: start, first chunk ready, end (us from kernel start)."""
+    l = synth.lap2d(4096, ny)
+    p = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
+                           probe_flags=16)
+    b = np.ones(l.n)
+    p.solve(b)
+    _, st = p.solve(b)
+    nt = (ny + 63) // 64
+    ts = p.probe_tasks(nt).astype(np.float64)
+    t0 = ts[:, 0].min()
+    rel = (ts - t0) / 1e3
+    gaps = np.diff(rel[:, 2])
+    print(json.dumps({"ny": ny, "precision": precision, "kernel_ms": round(st["kernel_ms"], 4),
+                      "first_ready_us": [round(v, 1) for v in rel[:8, 1]],
+                      "end_us": [round(v, 1) for v in rel[::max(1, nt // 16), 2]],
+                      "band0_us": round(rel[0, 2] - rel[0, 1], 1),
+                      "end_gap_us_median": round(float(np.median(gaps)), 2) if gaps.size else None,
+                      "ready_gap_us_median": round(float(np.median(np.diff(rel[:, 1]))), 2) if nt > 1 else None}),
+          flush=True)
+    p.close()
+
+
 def main():
+    if "--tasks" in sys.argv:
+        for ny in (64, 256, 4096):
+            tasks(ny)
+        tasks(4096, "exact")
+        return
     if "--clock" in sys.argv:
-        # probe bit 4: helper nap = bits 8.. (ns)
-        for ny in (64, 4096):
-            clock(ny)
-        clock(4096, "exact")
+        # probe bit 4: helper nap = bits 8.. (ns); bit 32: compute warp alone;
+        # bits 12..15: compute ablation (1 no staging, 2 no loads, 4 no shfl, 8 no publish branch)
+        clock(64)
+        clock(256)
+        clock(256, extra=64)  # band 1
+        clock(4096, extra=64)
         return
     for ny in (64, 128, 256, 1024, 4096):
         run(ny)
