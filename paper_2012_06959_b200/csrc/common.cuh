@@ -67,6 +67,9 @@ __device__ __forceinline__ int exp_bits(double v) {
 // sequence; outside the safe exponent window the IEEE division runs instead.
 // Bit-identical to IEEE division — verified on 1e8 random operand pairs
 // (tests/test_oracle.py::test_markstein_division_is_ieee).
+// Operand-range guard of div_exact as one unsigned compare.
+__device__ __forceinline__ bool markstein_ok(double v) { return (unsigned)(exp_bits(v) - 101) < 1845u; }
+
 __device__ __forceinline__ double div_exact(double a, double d, double rd) {
   double q = __dmul_rn(a, rd);
   int eq = exp_bits(q), ea = exp_bits(a), ed = exp_bits(d);

@@ -70,6 +70,7 @@ __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, in
 }
 
 constexpr int kStBlkPairs = kStBlock / 2;
+constexpr int kStThreads = 4 * 32;  // compute, loader, storer, poller warps
 // Shared-memory rings keep 16-byte pairs lane-innermost ([...][pair][lane]) so
 // every warp-wide 16-byte access touches 512 consecutive bytes (4 wavefronts,
 // no bank conflicts). b pair index of grid row r, chunk step k, column pair h:
@@ -149,7 +150,7 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
 }
 
 // control words of one task (chunk counters)
-enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5 };
+enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5, kCtlMbReady = 6 };
 
 template <bool EXACT>
 struct StSmem {
@@ -239,11 +240,9 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-  double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
   const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
-  const unsigned long long* above = t > 0 ? a.mbox + (size_t)(t - 1) * a.nx : nullptr;
   bool ok = true;
   // chunk c: its coefficient block and, per lane and grid row, the b segment of
   // column blocks [c*G - lane, c*G - lane + G) clipped to the grid
@@ -309,18 +308,6 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     if (long long* p = st_stamp(a, t, c, lane, 3)) *p = clock64();
     if (ok) ok = settle(c);
     if (long long* p = st_stamp(a, t, c, lane, 4)) *p = clock64();
-    if (ok && lane < kStG * kStC && above) {
-      // the chunk's row-above values (lane 0's blocks of steps c*G..c*G+G-1):
-      // one value per lane, so the chunk costs one L2 round trip
-      const int k = lane / kStC, q = lane % kStC;
-      const int j = c * kStG + k;
-      if (j < nblk) {
-        const unsigned long long u =
-            st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
-        if (u == kNotReady) ok = false;
-        inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
-      }
-    }
     ok = __all_sync(0xffffffffu, ok);
     if (!ok) {
       abort_task(a, ctl, lane);
@@ -329,6 +316,36 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     }
     if (lane == 0) st_release_cta(ctl + kCtlInReady, c + 1);
     if (long long* p = st_stamp(a, t, c, lane, 5)) *p = clock64();
+  }
+}
+
+// ---- warp 3: the band above's bottom grid row -------------------------------
+// Per chunk, the row-above values of lane 0's blocks of steps c*G..c*G+G-1,
+// one value per lane (one L2 round trip per chunk), polled value-is-flag and
+// handed over through the inbox ring. Kept apart from the loader so the
+// round trip overlaps the loader's copies instead of adding to them.
+template <bool EXACT>
+__device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
+  using S = StSmem<EXACT>;
+  constexpr int NB = S::kSlots;
+  if (t == 0) return;
+  double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
+  const unsigned long long* above = a.mbox + (size_t)(t - 1) * a.nx;
+  const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
+  const int k = lane / kStC, q = lane % kStC;
+  for (int c = 0; c < nchunks; ++c) {
+    // inbox slot c % NB is free once the compute warp finished chunk c - NB
+    if (c >= NB && !wait_ctl(ctl, kCtlInDone, c - NB + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
+    bool ok = true;
+    const int j = c * kStG + k;
+    if (lane < kStG * kStC && j < nblk) {
+      const unsigned long long u =
+          st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+      if (u == kNotReady) ok = false;
+      inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
+    }
+    if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
+    if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
   }
 }
 
@@ -403,22 +420,38 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
     }
     double xb[kStR][kStC];
+    // exact: Markstein division for the whole block, with its operand-range
+    // guards folded into one flag; the rare lane whose guard fails (and the
+    // inactive edge steps, whose d is 0) redoes the block with IEEE division,
+    // so the block costs one branch instead of one per element
+    auto solve_block = [&](bool ieee) -> bool {
+      bool bad = false;
 #pragma unroll
-    for (int r = 0; r < kStR; ++r) {
+      for (int r = 0; r < kStR; ++r) {
 #pragma unroll
-      for (int q = 0; q < kStC; ++q) {
-        const int e = r * kStC + q;
-        const double up = r == 0 ? top[q] : xb[r - 1][q];
-        const double left = q == 0 ? xleft[r] : xb[r][q - 1];
-        if (EXACT) {
-          double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
-          acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
-          xb[r][q] = div_exact(__dsub_rn(cur.bv[e], acc), cur.dd[e], cur.rd[e]);
-        } else {
-          xb[r][q] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
+        for (int q = 0; q < kStC; ++q) {
+          const int e = r * kStC + q;
+          const double up = r == 0 ? top[q] : xb[r - 1][q];
+          const double left = q == 0 ? xleft[r] : xb[r][q - 1];
+          if (EXACT) {
+            double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
+            acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
+            const double num = __dsub_rn(cur.bv[e], acc);
+            if (ieee) {
+              xb[r][q] = __ddiv_rn(num, cur.dd[e]);
+            } else {
+              const double qv = __dmul_rn(num, cur.rd[e]);
+              bad |= !(markstein_ok(qv) && markstein_ok(num) && markstein_ok(cur.dd[e]));
+              xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
+            }
+          } else {
+            xb[r][q] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
+          }
         }
       }
-    }
+      return bad;
+    };
+    if (solve_block(false) && EXACT) solve_block(true);
     // branch-free: a divergent branch here costs more than the whole FMA chain
 #pragma unroll
     for (int r = 0; r < kStR; ++r) xleft[r] = ((ABL & 8) || active) ? xb[r][kStC - 1] : xleft[r];
@@ -448,6 +481,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       if (c + 1 < nchunks) {
         if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
         if (!solo && !wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
+        if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, c + 2, deadline)) return false;
         if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
         if (!solo && c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline))
           return false;
@@ -462,6 +496,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> A, B;
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
+  if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, 1, deadline)) return abort_task(a, ctl, lane);
   if (tstamp) tstamp[1] = (long long)globaltimer_ns();
   A.load(smem, 0, 0, lane);
   for (int c = 0; c < nchunks; ++c) {
@@ -476,7 +511,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 }
 
 template <bool EXACT, int ABL>
-__global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
+__global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(128) unsigned char smem[];
   int* ctl = reinterpret_cast<int*>(smem + S::kCtl);
@@ -492,6 +527,7 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
     if (threadIdx.x == 0) {
       ctl[kCtlTask] = atomicAdd(a.ticket, 1);
       ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
+      ctl[kCtlMbReady] = 0;
     }
     __syncthreads();
     const int t = ctl[kCtlTask];
@@ -499,7 +535,8 @@ __global__ void __launch_bounds__(96, 1) k_stencil2d(StArgs a) {
     if (warp == 0) compute<EXACT, ABL>(a, smem, ctl, t, lane, deadline);
     else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
     } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
-    else storer<EXACT>(a, smem, ctl, t, lane, deadline);
+    else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
+    else poller<EXACT>(a, smem, ctl, t, lane, deadline);
     __syncthreads();
     if (ctl[kCtlAbort]) break;
   }
@@ -514,7 +551,7 @@ cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stencil2d<EXACT, ABL><<<blocks, 96, StSmem<EXACT>::kTotal, s>>>(a);
+  k_stencil2d<EXACT, ABL><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -595,19 +632,24 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
       double* stepbuf = st.data() + ((size_t)t * stencil.steps_per_task + s) * (step_bytes / 8);
       for (int l = 0; l < kStLanes; ++l) {
         const int j = s - l;
-        if (j < 0 || j >= nblk) continue;
         for (int r = 0; r < kStR; ++r) {
           const long long y = (long long)t * kStBand + kStR * l + r;
-          if (y >= stencil.ny) continue;
           for (int c = 0; c < kStC; ++c) {
-            const long long i = y * nx + (long long)j * kStC + c;
             const int e_ = r * kStC + c;
             const int k = e_ / 2, half = e_ % 2;
+            double f[4];
+            if (j < 0 || j >= nblk || y >= stencil.ny) {
+              // padding element: no coefficients; exact mode divides by 1 so
+              // the block's Markstein guard stays on the fast path
+              f[0] = f[1] = 0.0, f[2] = exact ? 1.0 : 0.0, f[3] = exact ? 1.0 : 0.0;
+              for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
+              continue;
+            }
+            const long long i = y * nx + (long long)j * kStC + c;
             double fu = 0.0, fl = 0.0;
             int kk = h_rp[i];
             if (y > 0) fu = h_val[kk++];
             if (j * kStC + c > 0) fl = h_val[kk];
-            double f[4];
             if (exact) {
               f[0] = fu, f[1] = fl, f[2] = h_dg[i], f[3] = h_rdg[i];
             } else {
