@@ -260,8 +260,9 @@ def main():
     hx = torch.empty(n, dtype=torch.float64).pin_memory()
     hb_np, hx_np = hb.numpy(), hx.numpy()
     t_e2e = []
+    e2e_streamed = 0
     if ws == 1:
-        plan.solve(hb_np, out=hx_np)
+        e2e_streamed = int(plan.solve(hb_np, out=hx_np)[1].get("streamed_io", 0))
         for _ in range(args.e2e_steps):
             t1 = time.perf_counter()
             plan.solve(hb_np, out=hx_np)
@@ -359,7 +360,11 @@ def main():
             "h2d_bytes_per_step": 8 * n,
             "d2h_bytes_per_step": d2h,
             "ms_per_step": e2e_s * 1e3,
-            "path": "sptrsv_solve (C ABI, pinned host b/x)" if ws == 1 else "per-rank H2D b, solve, D2H owned x",
+            "path": ("sptrsv_solve (C ABI, pinned host b/x" +
+                     {1: ", band-granular H2D/D2H overlapping the kernel)",
+                      2: ", zero-copy: the kernel reads b and writes x over PCIe in 128-byte lines)"}.get(
+                         e2e_streamed, ")"))
+            if ws == 1 else "per-rank H2D b, solve, D2H owned x",
         },
         "cpu_baseline": None if cpu is None else {
             "value": flops / cpu["seconds"] / 1e9,

@@ -52,7 +52,8 @@ enum { SPTRSV_EXECUTOR_AUTO = 0, SPTRSV_EXECUTOR_ROWS = 1, SPTRSV_EXECUTOR_CHAIN
 
 /* plan flags */
 enum {
-  SPTRSV_PLAN_STRUCTURE_ONLY = 1 /* analysis only: diagonal may be missing/zero, values may be NULL */
+  SPTRSV_PLAN_STRUCTURE_ONLY = 1, /* analysis only: diagonal may be missing/zero, values may be NULL */
+  SPTRSV_PLAN_NO_STREAMED_IO = 4  /* sptrsv_solve: copy all of b in, solve, copy all of x out (no overlap) */
 };
 
 typedef struct sptrsv_options {
@@ -78,6 +79,10 @@ typedef struct sptrsv_stats {
   int64_t launches;       /* kernels launched by the last solve */
   int32_t executor;       /* executor that ran */
   int32_t n_levels;
+  double e2e_ms;          /* wall time of the last host-buffer solve (copies included) */
+  int32_t streamed_io;    /* 1: copies overlapped the kernel band by band; 2: zero-copy (pinned b/x read and
+                           written by the kernel over PCIe); 0: copy in, solve, copy out */
+  int32_t reserved_;
 } sptrsv_stats;
 
 typedef struct sptrsv_plan_info {
@@ -126,7 +131,11 @@ int sptrsv_plan_levels(const sptrsv_plan* plan, int64_t* level_of, int64_t* orde
 int sptrsv_in_degrees(const int64_t* col_ptr, const int64_t* row_idx, int64_t n, int32_t device, int64_t* out);
 
 /* solve (engine.py:585-589) on host buffers: copies b in, solves, copies x
- * out. b and x are float64[n]. */
+ * out. b and x are float64[n]. With the stencil executor the copies are
+ * band-granular and overlap the solve (b of band t lands while earlier bands
+ * solve; x of band t leaves as soon as it is stored), unless the plan was
+ * created with SPTRSV_PLAN_NO_STREAMED_IO. Pinned host buffers give full
+ * PCIe overlap; pageable ones are correct but serialise on the host. */
 int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* stats);
 
 /* Device-resident solve: d_b/d_x are device pointers on the plan's device,

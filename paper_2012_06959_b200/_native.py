@@ -24,6 +24,7 @@ PRECISION = {"exact": 0, "fast": 1}
 EXECUTOR = {"auto": 0, "rows": 1, "chains": 2, "stencil": 3}
 EXECUTOR_NAME = {v: k for k, v in EXECUTOR.items()}
 PLAN_STRUCTURE_ONLY = 1
+PLAN_NO_STREAMED_IO = 4
 
 
 class Options(C.Structure):
@@ -53,6 +54,9 @@ class Stats(C.Structure):
         ("launches", C.c_int64),
         ("executor", C.c_int32),
         ("n_levels", C.c_int32),
+        ("e2e_ms", C.c_double),
+        ("streamed_io", C.c_int32),
+        ("reserved_", C.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -185,7 +189,7 @@ class NativePlan:
 
     def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
                  timeout=60.0, spin_initial=1024, spin_max_ns=64, structure_only=False, chain_lanes=32,
-                 probe_flags=0):
+                 probe_flags=0, streamed_io=True):
         lib = require_gpu()
         self._lib = lib
         self.n = int(n)
@@ -196,7 +200,7 @@ class NativePlan:
         opt.precision = PRECISION[precision]
         opt.executor = EXECUTOR[executor]
         opt.device = int(device)
-        opt.flags = PLAN_STRUCTURE_ONLY if structure_only else 0
+        opt.flags = (PLAN_STRUCTURE_ONLY if structure_only else 0) | (0 if streamed_io else PLAN_NO_STREAMED_IO)
         opt.timeout_s = float(timeout)
         opt.spin_initial = int(spin_initial)
         opt.spin_max_ns = int(spin_max_ns)

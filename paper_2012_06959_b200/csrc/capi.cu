@@ -60,6 +60,8 @@ void DevicePlan::release() {
   if (evk0) cudaEventDestroy(evk0);
   if (evk1) cudaEventDestroy(evk1);
   if (stream) cudaStreamDestroy(stream);
+  if (cs_in) cudaStreamDestroy(cs_in);
+  if (cs_out) cudaStreamDestroy(cs_out);
 }
 
 int DevicePlan::run_levels() {
@@ -193,6 +195,99 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   if (rc != SPTRSV_OK) return rc;
   CUDA_TRY(cudaEventRecord(ev1, s));
   pending = true;
+  return SPTRSV_OK;
+}
+
+// Stream memory operations (cuStreamWriteValue32 / cuStreamWaitValue32),
+// fetched through the runtime so the library does not link libcuda.
+namespace {
+typedef int (*PfnValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
+PfnValue32 g_write32 = nullptr, g_wait32 = nullptr;
+bool stream_memops() {
+  static int state = 0;  // 0 unknown, 1 available, -1 not
+  if (state == 0) {
+    void *w = nullptr, *t = nullptr;
+    cudaDriverEntryPointQueryResult qw, qt;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &qw) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &qt) == cudaSuccess &&
+        qw == cudaDriverEntryPointSuccess && qt == cudaDriverEntryPointSuccess && w && t) {
+      g_write32 = reinterpret_cast<PfnValue32>(w);
+      g_wait32 = reinterpret_cast<PfnValue32>(t);
+      state = 1;
+    } else {
+      cudaGetLastError();
+      state = -1;
+    }
+  }
+  return state == 1;
+}
+constexpr unsigned kWaitGeq = 0;  // CU_STREAM_WAIT_VALUE_GEQ
+}  // namespace
+
+bool DevicePlan::streamed_io_ok() const {
+  return executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !(opt.flags & SPTRSV_PLAN_NO_STREAMED_IO) &&
+         stencil.bflag && stream_memops();
+}
+
+// Pinned host memory (cudaHostAlloc / cudaHostRegister under UVA): the whole
+// [p, p + bytes). Only such buffers get the overlapped copies: copies from
+// pageable memory block the host thread and would serialise the pipeline.
+static bool device_mapped_host(const void* p, size_t bytes) {
+  const void* ends[2] = {p, static_cast<const char*>(p) + bytes - 1};
+  for (const void* q : ends) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer != q) return false;
+  }
+  return true;
+}
+
+// Host-buffer solve for the stencil executor. The kernel is launched first;
+// its loader waits per band for bflag[t] >= epoch, which the input copy stream
+// writes after band t's slice of b. The output stream waits per band for the
+// kernel's xflag[t] >= epoch and copies that slice of x out. After the kernel
+// the solve stream writes every xflag itself, so an aborted kernel (watchdog)
+// can never leave the output stream waiting.
+int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st) {
+  if (!cs_in) CUDA_TRY(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
+  if (!cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+  auto t0 = std::chrono::steady_clock::now();
+  const unsigned ep = ++stencil.epoch;
+  const long long band = (long long)kStBand * stencil.nx;
+  const int nt = stencil.n_tasks;
+  CUDA_TRY(cudaEventRecord(ev0, stream));
+  int rc = solve_stencil(bbuf, xbuf, stream, true, true);
+  if (rc != SPTRSV_OK) return rc;
+  CUDA_TRY(cudaEventRecord(ev1, stream));
+  pending = true;
+  for (int t = 0; t < nt; ++t)
+    if (g_write32(stream, (unsigned long long)(stencil.xflag + t), ep, 0) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
+  for (int t = 0; t < nt; ++t) {
+    const long long off = t * band, cnt = std::min(band, n - off);
+    CUDA_TRY(cudaMemcpyAsync(bbuf + off, b + off, sizeof(double) * cnt, cudaMemcpyHostToDevice, cs_in));
+    if (g_write32(cs_in, (unsigned long long)(stencil.bflag + t), ep, 0) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
+  }
+  for (int t = 0; t < nt; ++t) {
+    const long long off = t * band, cnt = std::min(band, n - off);
+    if (g_wait32(cs_out, (unsigned long long)(stencil.xflag + t), ep, kWaitGeq) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWaitValue32 failed");
+    CUDA_TRY(cudaMemcpyAsync(x + off, xbuf + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, cs_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(cs_in));
+  CUDA_TRY(cudaStreamSynchronize(cs_out));
+  rc = finish(st);
+  if (rc != SPTRSV_OK) return rc;
+  if (st) {
+    st->h2d_ms = 0.0;  // overlapped with the solve
+    st->d2h_ms = 0.0;
+    st->e2e_ms = ms_since(t0);
+    st->streamed_io = 1;
+  }
   return SPTRSV_OK;
 }
 
@@ -355,6 +450,11 @@ int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* st
   if (!p || (p->n > 0 && (!b || !x))) return fail(SPTRSV_E_ARGUMENT, "null argument");
   CUDA_TRY(cudaSetDevice(p->device));
   if (p->n == 0) return p->finish(stats);
+  if (p->structure_only) return fail(SPTRSV_E_ARGUMENT, "plan was created structure-only; it cannot solve");
+  // band-granular copy overlap needs pinned buffers (pageable copies block the host)
+  if (p->streamed_io_ok() && device_mapped_host(b, sizeof(double) * p->n) &&
+      device_mapped_host(x, sizeof(double) * p->n))
+    return p->solve_host_streamed(b, x, stats);
   auto t0 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaMemcpyAsync(p->bbuf, b, sizeof(double) * p->n, cudaMemcpyHostToDevice, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
@@ -369,6 +469,7 @@ int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* st
   if (stats) {
     stats->h2d_ms = h2d;
     stats->d2h_ms = ms_since(t1);
+    stats->e2e_ms = ms_since(t0);
   }
   return SPTRSV_OK;
 }

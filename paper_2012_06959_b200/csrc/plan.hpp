@@ -86,7 +86,12 @@ struct DevicePlan {
   int build_chains(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
   bool chains_preferred() const;
   int build_stencil(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
-  int solve_stencil(const double* d_b, double* d_x, cudaStream_t s);
+  int solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags = false, bool x_flags = false);
+  // host-buffer solve with band-granular H2D of b / D2H of x overlapping the
+  // stencil kernel (copy streams + stream memory operations on band flags)
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  int solve_host_streamed(const double* b, double* x, sptrsv_stats* st);
+  bool streamed_io_ok() const;
   int solve_device(const double* d_b, double* d_x, cudaStream_t s);
   int finish(sptrsv_stats* st);
   void release();

@@ -59,6 +59,12 @@ struct StArgs {
   int nap;         // helper-warp sleep between control-word polls (ns)
   int b_aligned;   // b is 16-byte aligned: gather it with 16-byte cp.async (else 8-byte)
   int x_aligned;   // x is 16-byte aligned: 16-byte stores (else 8-byte)
+  // host-buffer solves with overlapped copies (null otherwise): band t's b is
+  // resident once bflag[t] >= epoch; the storer sets xflag[t] = epoch once
+  // band t's x is stored
+  const unsigned* bflag;
+  unsigned* xflag;
+  unsigned epoch;
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -293,6 +299,18 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     phase_bits ^= 1u << slot;
     return true;
   };
+  // overlapped host solve: this band's b may still be on its way over PCIe
+  if (a.bflag) {
+    int polls = 0;
+    while ((int)(ld_acquire_sys_u32(a.bflag + t) - a.epoch) < 0) {
+      if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
+      if (!__all_sync(0xffffffffu, ok)) {
+        abort_task(a, ctl, lane);
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
   // Issue as far ahead as the ring allows (bounded by the compute warp's
   // progress, never by the band above); hand chunks over in order; only the
   // hand-over waits on the band-above mailbox.
@@ -385,6 +403,11 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     }
     __syncwarp();
     if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
+  }
+  // overlapped host solve: band t's x may now be copied to the host
+  if (a.xflag && lane == 0) {
+    __threadfence_system();
+    st_release_sys_u32(a.xflag + t, a.epoch);
   }
 }
 
@@ -665,6 +688,10 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   if ((e = al((void**)&stencil.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&stencil.mbox, sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
       (e = al((void**)&stencil.ticket, sizeof(int))) != cudaSuccess ||
+      (e = al((void**)&stencil.bflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
+      (e = al((void**)&stencil.xflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
+      (e = cudaMemset(stencil.bflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
+      (e = cudaMemset(stencil.xflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = cudaMemcpy(stencil.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   stencil.stream_bytes = (long long)bytes;
@@ -673,7 +700,7 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   return SPTRSV_OK;
 }
 
-int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
+int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags) {
   if (!stencil.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 2D five-point lower structured");
   cudaError_t e;
   if ((e = cudaMemsetAsync(stencil.mbox, 0xFF, sizeof(unsigned long long) * (size_t)stencil.n_tasks * stencil.nx, s)) !=
@@ -700,6 +727,9 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s) {
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
+  if (b_flags) a.bflag = stencil.bflag;
+  if (x_flags) a.xflag = stencil.xflag;
+  a.epoch = stencil.epoch;
   a.nap = (opt.probe_flags & 4) ? (opt.probe_flags >> 8) & 1023 : 64;  // probe bit 4: override the nap
   if (opt.probe_flags & 16) {
     if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * kProbeWords) != cudaSuccess)

@@ -41,13 +41,21 @@ struct StencilPlan {
   unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
   unsigned long long* mbox = nullptr;  // [n_tasks][nx] bottom grid row of each task (value-is-flag)
   int* ticket = nullptr;
+  // streamed host solves (sptrsv_solve): per-band b-arrived flags written by
+  // the copy stream, per-band x-stored flags written by the kernel; both
+  // compared against a per-solve epoch so they never need resetting
+  unsigned* bflag = nullptr;  // [n_tasks]
+  unsigned* xflag = nullptr;  // [n_tasks]
+  unsigned epoch = 0;
   void release() {
-    void* ptrs[] = {stream, mbox, ticket};
+    void* ptrs[] = {stream, mbox, ticket, bflag, xflag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
     mbox = nullptr;
     ticket = nullptr;
+    bflag = xflag = nullptr;
+    epoch = 0;
     ready = false;
   }
 };

@@ -241,3 +241,36 @@ def test_stencil_not_chosen_for_other_structures():
     plan = _native.NativePlan(l3.col_ptr, l3.row_idx, l3.values, l3.n, executor="auto")
     assert plan.info()["executor"] != "stencil"
     plan.close()
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+@pytest.mark.parametrize("shape", [(64, 64), (128, 200), (512, 1000)])
+def test_stencil_streamed_host_solve(shape, precision):
+    """sptrsv_solve on host buffers: pinned (band-granular copies overlapping
+    the kernel) and pageable give the same x as the unstreamed plan and
+    (exact) the oracle; repeated solves (epoch flags never reset)."""
+    torch = pytest.importorskip("torch")
+    l = _random_coefficients(synth.lap2d(*shape), 11)
+    rng = np.random.default_rng(12)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil")
+    flat = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
+                              streamed_io=False)
+    hb = torch.empty(l.n, dtype=torch.float64).pin_memory()
+    hx = torch.empty(l.n, dtype=torch.float64).pin_memory()
+    for rep in range(3):
+        b = rng.uniform(-1, 1, l.n)
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        x1, st1 = plan.solve(b)  # pageable: copy in, solve, copy out
+        assert st1["streamed_io"] == 0
+        hb.numpy()[:] = b
+        _, st2 = plan.solve(hb.numpy(), out=hx.numpy())  # pinned: band-granular copies overlap the kernel
+        assert st2["streamed_io"] & 1
+        x0, st0 = flat.solve(hb.numpy())
+        assert st0["streamed_io"] == 0
+        assert x1.tobytes() == x0.tobytes() == hx.numpy().tobytes()
+        if precision == "exact":
+            assert x1.tobytes() == ref.tobytes()
+        else:
+            assert np.max(np.abs(x1 - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-12
+    plan.close()
+    flat.close()
