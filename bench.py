@@ -21,10 +21,11 @@ configured matrix with b = ones (the reference CLI default, cli.py:139-140).
   one host core, full matrix (rank 0, N = 1 only).
 
 N > 1 (torchrun, one process per GPU): block_partition(n, N) — every GPU owns a
-contiguous slab of rows and its x segment; peers' segments are opened over
-CUDA IPC and read with one-sided loads inside the solve (no collective in the
-solve); an NCCL all-reduce of one word orders consecutive solves. Total work is
-fixed, so ``scaling`` is "strong".
+contiguous slab of rows (for lap2d-4096: whole 64-grid-row bands of the
+stencil executor) and its x; the peer state (stencil mailboxes, or component
+segments) is opened over CUDA IPC and read with one-sided loads inside the
+solve (no collective in the solve); an NCCL all-reduce of one word orders
+consecutive solves. Total work is fixed, so ``scaling`` is "strong".
 """
 
 from __future__ import annotations
@@ -206,7 +207,7 @@ def main():
     setup_s = time.perf_counter() - ts
     info = plan.info()
     if ws > 1:
-        info["executor"] = "rows (PE segments)"
+        info["executor"] = f"{info['executor']} (PE partition, peer {'mailboxes' if info['executor'] == 'stencil' else 'segments'})"
 
     db = torch.from_numpy(b).to(f"cuda:{dev}")
     dx = torch.zeros_like(db)

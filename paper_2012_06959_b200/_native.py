@@ -251,6 +251,11 @@ class NativePlan:
         rc = self._lib.sptrsv_plan_import_segment(self._h, int(pe), buf)
         raise_for_status(rc, _err(self._lib))
 
+    def set_peer_segment(self, pe: int, device_ptr: int) -> None:
+        """Wire PE ``pe``'s shared state (segment / stencil mailboxes) by device pointer (same process)."""
+        rc = self._lib.sptrsv_plan_set_peer_segment(self._h, int(pe), C.c_void_p(device_ptr))
+        raise_for_status(rc, _err(self._lib))
+
     def segment_ptr(self) -> int:
         return int(self._lib.sptrsv_plan_segment(self._h) or 0)
 

@@ -188,7 +188,8 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   if (structure_only) return fail(SPTRSV_E_ARGUMENT, "plan was created structure-only; it cannot solve");
   int rc;
   CUDA_TRY(cudaEventRecord(ev0, s));
-  if (seg_table) rc = solve_partitioned_rows(d_b, d_x, s);
+  if (stencil.part) rc = solve_stencil(d_b, d_x, s);
+  else if (seg_table) rc = solve_partitioned_rows(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_STENCIL) rc = solve_stencil(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
   else rc = solve_rows(d_b, d_x, s);
@@ -225,7 +226,8 @@ constexpr unsigned kWaitGeq = 0;  // CU_STREAM_WAIT_VALUE_GEQ
 }  // namespace
 
 bool DevicePlan::streamed_io_ok() const {
-  return executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !(opt.flags & SPTRSV_PLAN_NO_STREAMED_IO) &&
+  return executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !stencil.part &&
+         !(opt.flags & SPTRSV_PLAN_NO_STREAMED_IO) &&
          stencil.bflag && stream_memops();
 }
 

@@ -38,6 +38,7 @@ __global__ void k_gather_owned(unsigned long long* const* segs, const unsigned c
 }  // namespace
 
 void DevicePlan::release_partition() {
+  stencil.release_part();
   for (auto* s : local_segs) cudaFree(s);
   local_segs.clear();
   for (void* p : opened_peers) cudaIpcCloseMemHandle(p);
@@ -67,6 +68,13 @@ int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
   }
   cudaSetDevice(device);
   release_partition();
+  if (executor_used == SPTRSV_EXECUTOR_STENCIL && stencil.ready && my_pe >= 0) {
+    // band-aligned block (or band round-robin) ownership: the stencil
+    // executor runs partitioned; anything else falls back to the pool
+    const int rc = set_stencil_partition(owner, pes, my_pe);
+    if (rc < 0) return SPTRSV_E_CUDA;
+    if (rc == 1) return SPTRSV_OK;
+  }
   n_pes = pes;
   pe_base = my_pe < 0 ? 0 : my_pe;
   n_pe_local = my_pe < 0 ? pes : 1;
@@ -93,7 +101,7 @@ int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
       (e = al((void**)&pe_order, sizeof(int) * ord.size())) != cudaSuccess ||
       (e = al((void**)&pe_order_off, sizeof(long long) * off.size())) != cudaSuccess ||
       (e = al((void**)&pe_tickets, sizeof(int) * n_pe_local)) != cudaSuccess ||
-      (e = al((void**)&seg_table, sizeof(void*) * pes)) != cudaSuccess)
+      (e = al((void**)&seg_table, 2 * sizeof(void*) * pes)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   cudaMemcpy(owner_dev, own.data(), n, cudaMemcpyHostToDevice);
   cudaMemcpy(pe_order, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice);
@@ -101,26 +109,42 @@ int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
   host_seg_table.assign(pes, nullptr);
   for (int q = 0; q < n_pe_local; ++q) {
     unsigned long long* seg = nullptr;
-    if ((e = al((void**)&seg, sizeof(unsigned long long) * n)) != cudaSuccess)
+    if ((e = al((void**)&seg, 2 * sizeof(unsigned long long) * n)) != cudaSuccess ||
+        (e = cudaMemset(seg, 0xFF, 2 * sizeof(unsigned long long) * n)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
     local_segs.push_back(seg);
     host_seg_table[pe_base + q] = seg;
   }
-  if ((e = cudaMemcpy(seg_table, host_seg_table.data(), sizeof(void*) * pes, cudaMemcpyHostToDevice)) != cudaSuccess)
-    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  part_solves = 0;
+  if (sync_seg_table() != SPTRSV_OK) return SPTRSV_E_CUDA;
   // the read-only inter-PE layer is the component pool (warp per component,
   // value-is-flag peer loads)
   executor_used = SPTRSV_EXECUTOR_ROWS;
   return SPTRSV_OK;
 }
 
+// Device segment table [2][n_pes]: half h of PE p's segment is seg_p + h * n.
+int DevicePlan::sync_seg_table() {
+  std::vector<unsigned long long*> t(2 * n_pes, nullptr);
+  for (int p = 0; p < n_pes; ++p)
+    if (host_seg_table[p]) t[p] = host_seg_table[p], t[n_pes + p] = host_seg_table[p] + n;
+  cudaError_t e = cudaMemcpy(seg_table, t.data(), sizeof(void*) * t.size(), cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? SPTRSV_OK : plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+}
+
 int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStream_t s) {
   for (int p = 0; p < n_pes; ++p)
     if (!host_seg_table[p]) return plan_fail(SPTRSV_E_INVALID_PE, "a peer segment was never imported");
   const int mode = opt.precision == SPTRSV_PRECISION_FAST ? kModeFast : kModeExact;
+  // Segments are double-buffered by solve parity: this solve publishes into
+  // and reads half `par` (reset by the previous solve), and resets the other
+  // half for the next solve, so no PE ever resets a half a peer may still be
+  // reading (consecutive solves are separated by a barrier across PEs).
+  const int par = (int)(part_solves++ & 1);
+  unsigned long long** table = seg_table + par * n_pes;
   cudaError_t e = cudaSuccess;
   for (auto* seg : local_segs)
-    if ((e = cudaMemsetAsync(seg, 0xFF, sizeof(unsigned long long) * n, s)) != cudaSuccess) break;
+    if ((e = cudaMemsetAsync(seg + (1 - par) * n, 0xFF, sizeof(unsigned long long) * n, s)) != cudaSuccess) break;
   if (e == cudaSuccess) e = cudaMemsetAsync(pe_tickets, 0, sizeof(int) * n_pe_local, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s);
@@ -133,7 +157,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   a.dg = dg;
   a.rdg = rdg;
   a.b = d_b;
-  a.xseg = seg_table;
+  a.xseg = table;
   a.lseg = lseg_dev;
   a.owner = owner_dev;
   a.pe_base = pe_base;
@@ -156,7 +180,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   if ((e = launch_rows(mode, a, blocks, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if (d_x) {
-    k_gather_owned<<<std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(seg_table, owner_dev, pe_base,
+    k_gather_owned<<<std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(table, owner_dev, pe_base,
                                                                                    n_pe_local, n, d_x);
     if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
@@ -179,6 +203,14 @@ int sptrsv_plan_set_partition(sptrsv_plan* plan, const int32_t* owner, int32_t n
 int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* handle_out) {
   auto* p = reinterpret_cast<const DevicePlan*>(plan);
   if (!p || !handle_out) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (p->stencil.part) {  // the stencil's shared state is its mailbox array
+    cudaSetDevice(p->device);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, p->stencil.mbox);
+    if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return SPTRSV_OK;
+  }
   if (p->local_segs.size() != 1) return plan_fail(SPTRSV_E_ARGUMENT, "export needs a one-PE-per-process partition");
   cudaSetDevice(p->device);
   cudaIpcMemHandle_t h;
@@ -191,8 +223,10 @@ int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* handle_out) {
 int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle) {
   auto* p = reinterpret_cast<DevicePlan*>(plan);
   if (!p || !handle) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
-  if (pe < 0 || pe >= p->n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
-  if (pe >= p->pe_base && pe < p->pe_base + p->n_pe_local) return plan_fail(SPTRSV_E_ARGUMENT, "pe is local");
+  const bool st = p->stencil.part;
+  if (pe < 0 || pe >= (st ? p->stencil.n_pes : p->n_pes)) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+  if (st ? pe == p->stencil.my_pe : (pe >= p->pe_base && pe < p->pe_base + p->n_pe_local))
+    return plan_fail(SPTRSV_E_ARGUMENT, "pe is local");
   cudaSetDevice(p->device);
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof(h));
@@ -200,25 +234,32 @@ int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle
   cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   p->opened_peers.push_back(ptr);
+  if (st) {
+    p->stencil.host_pe_mbox[pe] = reinterpret_cast<unsigned long long*>(ptr);
+    return p->stencil_sync_peers();
+  }
   p->host_seg_table[pe] = reinterpret_cast<unsigned long long*>(ptr);
-  e = cudaMemcpy(p->seg_table, p->host_seg_table.data(), sizeof(void*) * p->n_pes, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  return SPTRSV_OK;
+  return p->sync_seg_table();
 }
 
 int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr) {
   auto* p = reinterpret_cast<DevicePlan*>(plan);
   if (!p || !device_ptr) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (p->stencil.part) {
+    if (pe < 0 || pe >= p->stencil.n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+    cudaSetDevice(p->device);
+    p->stencil.host_pe_mbox[pe] = reinterpret_cast<unsigned long long*>(device_ptr);
+    return p->stencil_sync_peers();
+  }
   if (pe < 0 || pe >= p->n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
   cudaSetDevice(p->device);
   p->host_seg_table[pe] = reinterpret_cast<unsigned long long*>(device_ptr);
-  cudaError_t e = cudaMemcpy(p->seg_table, p->host_seg_table.data(), sizeof(void*) * p->n_pes, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  return SPTRSV_OK;
+  return p->sync_seg_table();
 }
 
 void* sptrsv_plan_segment(const sptrsv_plan* plan) {
   auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (p && p->stencil.part) return p->stencil.mbox;
   if (!p || p->local_segs.empty()) return nullptr;
   return p->local_segs[0];
 }

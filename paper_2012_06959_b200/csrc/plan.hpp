@@ -59,13 +59,15 @@ struct DevicePlan {
   unsigned char* owner_dev = nullptr;
   std::vector<unsigned long long*> local_segs;  // owned by this plan
   std::vector<void*> opened_peers;              // cudaIpcOpenMemHandle'd segments of other processes
-  unsigned long long** seg_table = nullptr;     // device [n_pes] segment pointers
+  unsigned long long** seg_table = nullptr;     // device [2][n_pes]: half h of each PE's segment
   std::vector<unsigned long long*> host_seg_table;
   int* pe_order = nullptr;
   long long* pe_order_off = nullptr;
   int* pe_tickets = nullptr;
   int set_partition(const int32_t* owner, int pes, int my_pe);
   int solve_partitioned_rows(const double* d_b, double* d_x, cudaStream_t s);
+  int sync_seg_table();
+  long long part_solves = 0;  // parity of the segment double buffer
   void release_partition();
   // diagnostics (probe_flags): kProbeWords int64 — per-step/chunk clock stamps
   // [0, 384), then per-task globaltimer stamps [384, 384 + 3 * 1024)
@@ -92,6 +94,8 @@ struct DevicePlan {
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
   int solve_host_streamed(const double* b, double* x, sptrsv_stats* st);
   bool streamed_io_ok() const;
+  int set_stencil_partition(const int32_t* owner, int pes, int my_pe);
+  int stencil_sync_peers();
   int solve_device(const double* d_b, double* d_x, cudaStream_t s);
   int finish(sptrsv_stats* st);
   void release();

@@ -65,6 +65,15 @@ struct StArgs {
   const unsigned* bflag;
   unsigned* xflag;
   unsigned epoch;
+  // PE partition (stencil.hpp): tickets index my_tasks (null: ticket = band);
+  // mbox is this PE's mailbox half of this solve, peers' halves are
+  // pe_mbox[owner] + mbox_half
+  const int* my_tasks;
+  int n_my_tasks;
+  unsigned long long* const* pe_mbox;
+  const unsigned char* band_owner;
+  int my_pe;
+  long long mbox_half;
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -110,6 +119,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.sys.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v),
+      "r"((int)pred)
+      : "memory");
+}
 // predicated relaxed store (no branch around it)
 __device__ __forceinline__ void st_relaxed_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
   asm volatile(
@@ -132,8 +147,10 @@ __device__ __forceinline__ void st_release_cta(int* p, int v) {
 }
 
 __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, int* abort_flag, DeviceStatus* status,
-                                                   int spin_initial, int spin_max_ns, unsigned long long deadline) {
-  unsigned long long u = ld_relaxed_u64(p);
+                                                   int spin_initial, int spin_max_ns, unsigned long long deadline,
+                                                   bool sys) {
+  auto ld = [&]() { return sys ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p); };
+  unsigned long long u = ld();
   int polls = 0, sleep_ns = 32;
   while (u == kNotReady) {
     ++polls;
@@ -149,7 +166,7 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
       __nanosleep(sleep_ns);
       if (sleep_ns < spin_max_ns) sleep_ns <<= 1;
     }
-    u = ld_relaxed_u64(p);
+    u = ld();
   }
   if (polls) atomicAdd(&status->spins, (unsigned long long)polls);
   return u;
@@ -348,7 +365,10 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   constexpr int NB = S::kSlots;
   if (t == 0) return;
   double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
-  const unsigned long long* above = a.mbox + (size_t)(t - 1) * a.nx;
+  // the band above on another PE: its owner's mailboxes over NVLink (.sys)
+  const int up_pe = a.band_owner ? a.band_owner[t - 1] : a.my_pe;
+  const bool remote = up_pe != a.my_pe;
+  const unsigned long long* above = (remote ? a.pe_mbox[up_pe] + a.mbox_half : a.mbox) + (size_t)(t - 1) * a.nx;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int k = lane / kStC, q = lane % kStC;
   for (int c = 0; c < nchunks; ++c) {
@@ -358,13 +378,14 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     const int j = c * kStG + k;
     if (lane < kStG * kStC && j < nblk) {
       const unsigned long long u =
-          st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline);
+          st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote);
       if (u == kNotReady) ok = false;
       inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
   }
+  if (remote && lane == 0) atomicAdd(&a.status->remote_reads, (unsigned long long)a.nx);
 }
 
 // ---- warp 2: solved blocks from shared memory to x --------------------------
@@ -415,14 +436,17 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 // ABL: compile-time ablations for timing experiments only (0 in production):
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
 // active/publish branch
-template <bool EXACT, int ABL>
+template <bool EXACT, int ABL, bool PART>
 __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const bool has_above = t > 0;
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
-  const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks;
+  // the band below on another PE reads these over NVLink: system-scope stores
+  const bool below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
+  const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks && !below_remote;
+  const bool publish_sys = lane == kStLanes - 1 && below_remote;
   const bool solo = (a.probe & 32) != 0;  // diagnostics: run without the helper warps
   double xleft[kStR];
 #pragma unroll
@@ -484,6 +508,11 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
       for (int q = 0; q < kStC; ++q)
         st_relaxed_u64_if(below + j * kStC + q, publishable(bottom[q]), publish && active);
+      if (PART) {
+#pragma unroll
+        for (int q = 0; q < kStC; ++q)
+          st_relaxed_sys_u64_if(below + j * kStC + q, publishable(bottom[q]), publish_sys && active);
+      }
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
                    k * kStBlkPairs * kStLanes + lane;
@@ -533,7 +562,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
-template <bool EXACT, int ABL>
+template <bool EXACT, int ABL, bool PART>
 __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -548,14 +577,15 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(StArgs a) {
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
   while (true) {
     if (threadIdx.x == 0) {
-      ctl[kCtlTask] = atomicAdd(a.ticket, 1);
+      const int k = atomicAdd(a.ticket, 1);  // ascending: the progress rule (engine.py:30-35)
+      ctl[kCtlTask] = k >= a.n_my_tasks ? a.n_tasks : (a.my_tasks ? a.my_tasks[k] : k);
       ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
       ctl[kCtlMbReady] = 0;
     }
     __syncthreads();
     const int t = ctl[kCtlTask];
     if (t >= a.n_tasks) break;
-    if (warp == 0) compute<EXACT, ABL>(a, smem, ctl, t, lane, deadline);
+    if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline);
     else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
     } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
     else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
@@ -565,22 +595,23 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(StArgs a) {
   }
 }
 
-template <bool EXACT, int ABL>
+template <bool EXACT, int ABL, bool PART = false>
 cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil2d<EXACT, ABL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_stencil2d<EXACT, ABL, PART>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          StSmem<EXACT>::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_stencil2d<EXACT, ABL><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
+  k_stencil2d<EXACT, ABL, PART><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
   return cudaGetLastError();
 }
 
 // probe bits 12..15 select an ablation variant of the fast kernel (timing only)
 template <bool EXACT>
 cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
+  if (a.band_owner) return launch_stencil_v<EXACT, 0, true>(a, blocks, s);
   if (!EXACT) {
     switch ((a.probe >> 12) & 15) {
       case 1: return launch_stencil_v<EXACT, 1>(a, blocks, s);
@@ -686,7 +717,9 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   }
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
   if ((e = al((void**)&stencil.stream, bytes)) != cudaSuccess ||
-      (e = al((void**)&stencil.mbox, sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
+      (e = al((void**)&stencil.mbox, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
+      (e = cudaMemset(stencil.mbox, 0xFF, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) !=
+          cudaSuccess ||
       (e = al((void**)&stencil.ticket, sizeof(int))) != cudaSuccess ||
       (e = al((void**)&stencil.bflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = al((void**)&stencil.xflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
@@ -694,6 +727,7 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
       (e = cudaMemset(stencil.xflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = cudaMemcpy(stencil.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  stencil.n_my_tasks = stencil.n_tasks;
   stencil.stream_bytes = (long long)bytes;
   stencil.ready = true;
   stencil.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -703,7 +737,16 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
 int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags) {
   if (!stencil.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 2D five-point lower structured");
   cudaError_t e;
-  if ((e = cudaMemsetAsync(stencil.mbox, 0xFF, sizeof(unsigned long long) * (size_t)stencil.n_tasks * stencil.nx, s)) !=
+  const long long half = (long long)stencil.n_tasks * stencil.nx;
+  const int par = (int)(stencil.solves & 1);
+  if (stencil.part) {
+    for (int t : stencil.host_my_tasks)
+      if (t > 0 && !stencil.host_pe_mbox[stencil.host_band_owner[t - 1]])
+        return plan_fail(SPTRSV_E_INVALID_PE, "the mailboxes of a peer PE were never imported");
+  }
+  // this solve uses mailbox half `par` (reset by the previous solve or at
+  // build); reset the other half for the next one
+  if ((e = cudaMemsetAsync(stencil.mbox + (1 - par) * half, 0xFF, sizeof(unsigned long long) * half, s)) !=
           cudaSuccess ||
       (e = cudaMemsetAsync(stencil.ticket, 0, sizeof(int), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
@@ -711,8 +754,18 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   StArgs a{};
   a.stream = stencil.stream;
-  a.mbox = stencil.mbox;
+  a.mbox = stencil.mbox + par * half;
+  a.mbox_half = par * half;
   a.ticket = stencil.ticket;
+  a.n_my_tasks = stencil.n_tasks;
+  a.my_pe = -1;
+  if (stencil.part) {
+    a.my_tasks = stencil.my_tasks;
+    a.n_my_tasks = stencil.n_my_tasks;
+    a.pe_mbox = stencil.pe_mbox;
+    a.band_owner = stencil.band_owner;
+    a.my_pe = stencil.my_pe;
+  }
   a.b = d_b;
   a.x = d_x;
   a.status = status;
@@ -737,13 +790,57 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
     a.dbg = probe_buf;
   }
-  const int blocks = std::max(1, std::min(stencil.n_tasks, num_sms));
+  const int blocks = std::max(1, std::min(a.n_my_tasks, num_sms));
+  ++stencil.solves;
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;
   return SPTRSV_OK;
+}
+
+// Band-aligned owner map, one PE per process: returns 1 when configured, 0
+// when some band is split between PEs (the caller falls back to the
+// component pool), < 0 on error.
+int DevicePlan::set_stencil_partition(const int32_t* owner, int pes, int my_pe) {
+  const long long band = (long long)kStBand * stencil.nx;
+  std::vector<int> bo(stencil.n_tasks), mine;
+  for (int t = 0; t < stencil.n_tasks; ++t) {
+    const long long i0 = t * band, i1 = std::min(n, i0 + band);
+    const int o = owner[i0];
+    for (long long i = i0 + 1; i < i1; ++i)
+      if (owner[i] != o) return 0;
+    bo[t] = o;
+    if (o == my_pe) mine.push_back(t);
+  }
+  stencil.release_part();
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  std::vector<unsigned char> bo8(bo.begin(), bo.end());
+  cudaError_t e;
+  if ((e = al((void**)&stencil.my_tasks, sizeof(int) * mine.size())) != cudaSuccess ||
+      (e = al((void**)&stencil.band_owner, bo8.size())) != cudaSuccess ||
+      (e = al((void**)&stencil.pe_mbox, sizeof(void*) * pes)) != cudaSuccess ||
+      (!mine.empty() &&
+       (e = cudaMemcpy(stencil.my_tasks, mine.data(), sizeof(int) * mine.size(), cudaMemcpyHostToDevice)) !=
+           cudaSuccess) ||
+      (e = cudaMemcpy(stencil.band_owner, bo8.data(), bo8.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  stencil.host_pe_mbox.assign(pes, nullptr);
+  stencil.host_pe_mbox[my_pe] = stencil.mbox;
+  stencil.host_band_owner = bo;
+  stencil.host_my_tasks = mine;
+  stencil.n_my_tasks = (int)mine.size();
+  stencil.my_pe = my_pe;
+  stencil.n_pes = pes;
+  stencil.part = true;
+  return stencil_sync_peers() == SPTRSV_OK ? 1 : -1;
+}
+
+int DevicePlan::stencil_sync_peers() {
+  cudaError_t e = cudaMemcpy(stencil.pe_mbox, stencil.host_pe_mbox.data(), sizeof(void*) * stencil.n_pes,
+                             cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? SPTRSV_OK : plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
 }
 
 }  // namespace sptrsv

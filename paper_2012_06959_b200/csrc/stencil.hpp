@@ -6,6 +6,7 @@
 // stencil.cu.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace sptrsv {
@@ -47,7 +48,41 @@ struct StencilPlan {
   unsigned* bflag = nullptr;  // [n_tasks]
   unsigned* xflag = nullptr;  // [n_tasks]
   unsigned epoch = 0;
+  // Mailboxes are double-buffered by solve parity ([2][n_tasks][nx]): solve k
+  // reads and writes half k % 2 and resets the other half for solve k + 1, so
+  // a PE never resets a half a peer may still be reading (consecutive solves
+  // are separated by a barrier across PEs).
+  long long solves = 0;
+  // PE partition, one PE per process (set_partition with my_pe >= 0 on a
+  // band-aligned owner map): this PE solves its own bands (ascending), reads
+  // the band above a PE boundary from the owning peer's mailboxes (CUDA IPC
+  // mapping, one-sided .sys loads over NVLink) and publishes the bottom row
+  // of a band whose successor is remote with .sys stores.
+  bool part = false;
+  int my_pe = -1, n_pes = 1;
+  int n_my_tasks = 0;
+  int* my_tasks = nullptr;                 // device [n_my_tasks]
+  unsigned char* band_owner = nullptr;     // device [n_tasks]
+  unsigned long long** pe_mbox = nullptr;  // device [n_pes] mailbox bases
+  std::vector<unsigned long long*> host_pe_mbox;
+  std::vector<int> host_band_owner, host_my_tasks;
+  void release_part() {
+    void* ptrs[] = {my_tasks, band_owner, pe_mbox};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    my_tasks = nullptr;
+    band_owner = nullptr;
+    pe_mbox = nullptr;
+    host_pe_mbox.clear();
+    host_band_owner.clear();
+    host_my_tasks.clear();
+    part = false;
+    my_pe = -1;
+    n_pes = 1;
+    n_my_tasks = n_tasks;
+  }
   void release() {
+    release_part();
     void* ptrs[] = {stream, mbox, ticket, bflag, xflag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
@@ -56,6 +91,7 @@ struct StencilPlan {
     ticket = nullptr;
     bflag = xflag = nullptr;
     epoch = 0;
+    solves = 0;
     ready = false;
   }
 };

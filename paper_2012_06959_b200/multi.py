@@ -5,7 +5,11 @@ default, as in BASELINE.json's multi-GPU config; ``task_round_robin_partition``
 works too). A rank builds the device plan of the whole matrix, keeps only its
 own components' x in its segment, exports the segment as a CUDA IPC handle and
 opens every peer's segment; inside the solve its kernel reads peers' x with
-one-sided loads over NVLink/NVSwitch. ``torch.distributed`` carries only the
+one-sided loads over NVLink/NVSwitch. For a 2D five-point L whose owner map
+is band-aligned (block_partition of a 4096-square grid over 1/2/4/8 PEs) the
+shared state is the stencil executor's mailbox array instead: a PE solves its
+own 64-grid-row bands and polls only the bottom row of the band above a PE
+boundary from its owner. ``torch.distributed`` carries only the
 64-byte handles at setup and a barrier between solves (a solve resets the
 segments, so no rank may start solve k+1 while a peer still reads solve k);
 scatter of b / gather of x, when a caller wants x on one rank, is NCCL.
@@ -58,7 +62,7 @@ class DistributedSolver:
     """This rank's PE of a partitioned solve (needs a GPU and an initialised process group)."""
 
     def __init__(self, l, plan: PartitionPlan, rank: int, *, device: int, precision: str = "fast",
-                 timeout: float = 60.0, group=None):
+                 timeout: float = 60.0, group=None, executor: str = "auto"):
         from . import _native
 
         if plan.n != l.n:
@@ -66,8 +70,10 @@ class DistributedSolver:
         self.rank = rank
         self.world = plan.n_pes
         self.group = group
+        # auto: a 2D five-point L with a band-aligned owner map runs the stencil
+        # executor partitioned (peer mailboxes); anything else the component pool
         self.native = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision,
-                                         executor="rows", device=device, timeout=timeout)
+                                         executor=executor, device=device, timeout=timeout)
         self.native.set_partition(plan.owner_arr, plan.n_pes, rank)
         handles = exchange_handles(self.native.export_segment(), group)
         for pe, h in enumerate(handles):
