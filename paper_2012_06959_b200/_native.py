@@ -152,11 +152,13 @@ def load_library() -> C.CDLL:
     global _lib
     with _lib_lock:
         if _lib is None:
-            if not LIB_PATH.exists():
+            # SPTRSV_LIB: an alternative in-tree build (tools/variants.sh), diagnostics only
+            path = Path(os.environ["SPTRSV_LIB"]) if os.environ.get("SPTRSV_LIB") else LIB_PATH
+            if not path.exists():
                 raise NativeUnavailable(
                     f"{LIB_PATH} is missing: run `python -m paper_2012_06959_b200.build` (there is no CPU fallback)"
                 )
-            lib = C.CDLL(str(LIB_PATH))
+            lib = C.CDLL(str(path))
             _bind(lib)
             _lib = lib
         return _lib

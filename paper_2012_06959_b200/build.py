@@ -34,7 +34,11 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
+def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] = (), lib: Path | None = None,
+          build_dir: Path | None = None) -> Path:
+    """Compile and link; ``defines``/``lib``/``build_dir`` build a variant (tools/variants.sh)."""
+    BUILD = build_dir or globals()["BUILD"]
+    LIB = lib or globals()["LIB"]
     BUILD.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [PKG.parent / "include" / "sptrsv_b200.h"]
     objs = []
@@ -43,7 +47,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+            cmd = [NVCC, *ARCH, *FLAGS, *defines, "-c", str(src), "-o", str(obj)]
             jobs.append(cmd)
 
     def run(cmd):
@@ -62,5 +66,13 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
-    print(LIB)
+    # python -m paper_2012_06959_b200.build [--force] [--variant NAME -DX=Y ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        defs = tuple(a for a in args if a.startswith("-D"))
+        print(build(verbose=True, force=True, defines=defs, lib=PKG / f"libsptrsv_b200_{name}.so",
+                    build_dir=PKG.parent / "build" / f"csrc_{name}"))
+    else:
+        build(verbose=True, force="--force" in args)
+        print(LIB)

@@ -34,6 +34,8 @@
 #include <vector>
 #include <chrono>
 #include <cstring>
+#include <cstdlib>
+#include <cuda.h>
 #include "plan.hpp"
 #include "kernels.cuh"
 
@@ -43,7 +45,19 @@ int plan_fail(int code, const char* msg);
 
 namespace {
 
-struct StArgs {
+// b of a chunk as ONE TMA copy (kStBTma): the band's rows seen through a
+// skewed 4-D tensor view of b, (q, l, r, band) with strides
+// (8, (2 nx - C) * 8, nx * 8, 64 nx * 8) bytes, so that element (q, l, r) is
+// b[64 band + 2 l + r][q - C l]: lane l's row pair lagging C columns per lane
+// is one rectangular box {G C, 32, R, 1} at q = c G C. Columns outside
+// [0, nx) of a lane read neighbouring rows of the same band (never outside
+// the band; padding steps discard them) or are zero-filled past the end.
+// 128-byte swizzle puts the 16-byte piece p of grid row R = 32 r + l at
+// p ^ (l & 7): the compute warp's 16-byte loads are conflict-free.
+constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
+
+struct alignas(64) StArgs {
+  CUtensorMap bmap;  // kStBTma and b 16-byte aligned and a full last band: b via TMA
   const unsigned char* stream;
   unsigned long long* mbox;
   int* ticket;
@@ -74,6 +88,7 @@ struct StArgs {
   const unsigned char* band_owner;
   int my_pe;
   long long mbox_half;
+  int b_tma_bands;  // bands [0, b_tma_bands) gather b with one TMA per chunk (0: cp.async everywhere)
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -89,7 +104,13 @@ constexpr int kStThreads = 4 * 32;  // compute, loader, storer, poller warps
 // Shared-memory rings keep 16-byte pairs lane-innermost ([...][pair][lane]) so
 // every warp-wide 16-byte access touches 512 consecutive bytes (4 wavefronts,
 // no bank conflicts). b pair index of grid row r, chunk step k, column pair h:
-__host__ __device__ constexpr int st_b_pair(int r, int k, int h) { return (r * kStG + k) * (kStC / 2) + h; }
+// b ring slot: [r][l][piece] 16-byte pieces, 128 bytes per grid row, piece
+// p = k * (kStC / 2) + h stored at p ^ (l & 7) (the TMA 128-byte swizzle;
+// the cp.async gather writes the same layout)
+__host__ __device__ constexpr int st_b_piece(int r, int l, int k, int h) {
+  return (r * kStLanes + l) * (kStG * kStC / 2) + ((k * (kStC / 2) + h) ^ (l & 7));
+}
+static_assert(kStG * kStC / 2 >= 8 || !kStBTma, "the swizzle spans eight 16-byte pieces");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
@@ -112,6 +133,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// 4-D tiled TMA load into shared memory, completing on `bar` (complete_tx)
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -188,7 +218,8 @@ struct StSmem {
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kCtl = kBars + 8 * kSlots;
-  static constexpr int kTotal = kCtl + 64;
+  static constexpr int kTotal = kCtl + 64 + 1024;  // + alignment slack of the ring base
+  static_assert(kB % 1024 == 0 && kBChunk % 1024 == 0, "b slots on 1024-byte boundaries (TMA swizzle)");
 };
 
 // Spin on a chunk counter; false when the task is being aborted or the
@@ -204,6 +235,21 @@ __device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, un
     if (nap) __nanosleep(nap);
   }
   return true;
+}
+
+// The compute warp's chunk-boundary wait: input slot, band-above inbox and
+// output slot in one polling loop (three independent shared loads per poll
+// instead of three sequential loops).
+__device__ __forceinline__ bool wait_chunk(const int* ctl, int in_need, int mb_need, int out_need,
+                                           unsigned long long deadline) {
+  int polls = 0;
+  while (true) {
+    const int i = ld_acquire_cta(ctl + kCtlInReady), m = ld_acquire_cta(ctl + kCtlMbReady),
+              o = ld_acquire_cta(ctl + kCtlOutDone);
+    if (i >= in_need && m >= mb_need && o >= out_need) return true;
+    if (ld_acquire_cta(ctl + kCtlAbort)) return false;
+    if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
+  }
 }
 
 // A wait failed (watchdog or a peer warp's abort): stop this task everywhere.
@@ -241,12 +287,12 @@ struct StBlk {
         rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
       }
     }
-    const double2* bb = reinterpret_cast<const double2*>(smem + S::kB + slot * S::kBChunk) + lane;
+    const double2* bb = reinterpret_cast<const double2*>(smem + S::kB + slot * S::kBChunk);
 #pragma unroll
     for (int r = 0; r < kStR; ++r) {
 #pragma unroll
       for (int c = 0; c < kStC; c += 2) {
-        const double2 v = bb[st_b_pair(r, k, c / 2) * kStLanes];
+        const double2 v = bb[st_b_piece(r, lane, k, c / 2)];
         bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
       }
     }
@@ -266,6 +312,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
   const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+  const bool b_tma = kStBTma && t < a.b_tma_bands;
   bool ok = true;
   // chunk c: its coefficient block and, per lane and grid row, the b segment of
   // column blocks [c*G - lane, c*G - lane + G) clipped to the grid
@@ -279,13 +326,14 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     const int j0 = c * kStG - lane;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[slot], S::kCoefChunk);
+      mbar_expect_tx(&bars[slot], S::kCoefChunk + (b_tma ? S::kBChunk : 0));
       bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk, &bars[slot]);
+      if (b_tma) tma_load_4d(smem + S::kB + slot * S::kBChunk, &a.bmap, c * kStG * kStC, 0, 0, t, &bars[slot]);
     }
-    double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk) + lane;
+    double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk);
 #pragma unroll
     for (int r = 0; r < kStR; ++r) {
-      if (y0 + r >= a.ny) continue;
+      if (b_tma || y0 + r >= a.ny) continue;
       const double* src = a.b + (size_t)(y0 + r) * a.nx;
 #pragma unroll
       for (int k = 0; k < kStG; ++k) {
@@ -293,7 +341,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
         if (jb < 0 || jb >= nblk) continue;
 #pragma unroll
         for (int h = 0; h < kStC / 2; ++h) {
-          double2* d = dst + st_b_pair(r, k, h) * kStLanes;
+          double2* d = dst + st_b_piece(r, lane, k, h);
           const double* s = src + jb * kStC + 2 * h;
           if (a.b_aligned) {
             cp_async16(d, s);
@@ -456,7 +504,17 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   for (int q = 0; q < kStC; ++q) bottom[q] = 0.0;
 
   // step k of chunk c; `nxt` receives the next step's inputs
-  auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt) -> bool {
+  // step k of chunk c computes from `cur` (loaded two steps earlier) and
+  // loads step k + 2 into `nxt2`: a full step of slack hides the shared-memory
+  // latency that a one-step lookahead leaves exposed
+  auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt2) -> bool {
+    // the first step that loads from chunk c + 1: make sure it is ready
+    if (k == kStG - 2 && c + 1 < nchunks && !solo) {
+      if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
+      if (!wait_chunk(ctl, c + 2, has_above ? c + 2 : 0, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0, deadline))
+        return false;
+      if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
+    }
     const int s = c * kStG + k;
     const int j = s - lane;
     const bool active = j >= 0 && j < nblk;
@@ -491,6 +549,10 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
               bad |= !(markstein_ok(qv) && markstein_ok(num) && markstein_ok(cur.dd[e]));
               xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
             }
+          } else if (q == 0) {
+            // left comes from the previous step (early): the late operand
+            // (up, possibly straight off the shuffle) goes in the outer FMA
+            xb[r][q] = __fma_rn(cur.wu[e], up, __fma_rn(cur.wl[e], left, __dmul_rn(cur.bv[e], cur.rd[e])));
           } else {
             xb[r][q] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
           }
@@ -521,23 +583,17 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
       for (int q = 0; q < kStC; q += 2)
         if (!(ABL & 1)) dst[(r * (kStC / 2) + q / 2) * kStLanes] = make_double2(xb[r][q], xb[r][q + 1]);
-    if (k + 1 < kStG) {
-      if (!(ABL & 2)) nxt.load(smem, c % NB, k + 1, lane);
-    } else {
-      // chunk boundary: hand over the outputs and the input slot, take the next chunk
+    if (k + 2 < kStG) {
+      if (!(ABL & 2)) nxt2.load(smem, c % NB, k + 2, lane);
+    } else if (c + 1 < nchunks) {
+      nxt2.load(smem, (c + 1) % NB, k + 2 - kStG, lane);
+    }
+    if (k == kStG - 1) {
+      // chunk boundary: hand over the outputs and the input slot
       __syncwarp();
       if (lane == 0) {
         st_release_cta(ctl + kCtlOutReady, c + 1);
         st_release_cta(ctl + kCtlInDone, c + 1);
-      }
-      if (c + 1 < nchunks) {
-        if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-        if (!solo && !wait_ctl(ctl, kCtlInReady, c + 2, deadline)) return false;
-        if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, c + 2, deadline)) return false;
-        if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
-        if (!solo && c + 1 >= kStOutSlots && !wait_ctl(ctl, kCtlOutDone, c + 2 - kStOutSlots, deadline))
-          return false;
-        nxt.load(smem, (c + 1) % NB, 0, lane);
       }
     }
     return true;
@@ -546,26 +602,33 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   // diagnostics: per-task globaltimer stamps (start, first chunk ready, end)
   long long* tstamp = (a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
-  StBlk<EXACT> A, B;
+  StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
   if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, 1, deadline)) return abort_task(a, ctl, lane);
   if (tstamp) tstamp[1] = (long long)globaltimer_ns();
-  A.load(smem, 0, 0, lane);
-  for (int c = 0; c < nchunks; ++c) {
-    static_assert(kStG % 2 == 0, "chunks hold an even number of steps");
+  static_assert(kStG >= 3, "the two-step lookahead stays within one chunk boundary");
+  buf[0].load(smem, 0, 0, lane);
+  buf[1].load(smem, 0, 1, lane);
+  // three chunks per iteration so that s % 3 is a compile-time constant
+  for (int c0 = 0; c0 < nchunks; c0 += 3) {
 #pragma unroll
-    for (int k = 0; k < kStG; k += 2) {
-      if (!step(c, k, A, B)) return abort_task(a, ctl, lane);
-      if (!step(c, k + 1, B, A)) return abort_task(a, ctl, lane);
+    for (int u = 0; u < 3; ++u) {
+      const int c = c0 + u;
+      if (c >= nchunks) break;
+#pragma unroll
+      for (int k = 0; k < kStG; ++k)
+        if (!step(c, k, buf[(u * kStG + k) % 3], buf[(u * kStG + k + 2) % 3])) return abort_task(a, ctl, lane);
     }
   }
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
 template <bool EXACT, int ABL, bool PART>
-__global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(StArgs a) {
+__global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_constant__ StArgs a) {
   using S = StSmem<EXACT>;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // the 128-byte TMA swizzle repeats every 1024 bytes: align the rings to it
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int* ctl = reinterpret_cast<int*>(smem + S::kCtl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -627,6 +690,38 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
 }
 
 }  // namespace
+
+// The skewed tensor view of b (see kStBTma); returns the number of bands it
+// covers (the full ones), 0 when the driver entry point or the encode fails.
+static int encode_b_map(CUtensorMap* map, const double* b, int nx, int ny) {
+  typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<Encode>(f);
+  }();
+  static const bool disabled = std::getenv("SPTRSV_NO_B_TMA") != nullptr;  // A/B diagnostics
+  const int bands = ny / kStBand;
+  if (!encode || disabled || bands < 1 || nx < kStLanes * kStC) return 0;
+  const cuuint64_t dims[4] = {(cuuint64_t)nx + (kStLanes - 1) * kStC, (cuuint64_t)kStLanes, (cuuint64_t)kStR,
+                              (cuuint64_t)bands};
+  const cuuint64_t strides[3] = {(cuuint64_t)(kStR * nx - kStC) * 8, (cuuint64_t)nx * 8,
+                                 (cuuint64_t)kStBand * nx * 8};
+  const cuuint32_t box[4] = {kStG * kStC, kStLanes, kStR, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(b), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 0;
+  return bands;
+}
 
 // Detect the 2D five-point lower structure on the host CSR; returns nx or 0.
 static int detect_stencil2d(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
@@ -779,6 +874,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.steps = stencil.steps_per_task;
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
+  a.b_tma_bands = (kStBTma && a.b_aligned) ? encode_b_map(&a.bmap, d_b, stencil.nx, stencil.ny) : 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
   if (b_flags) a.bflag = stencil.bflag;
   if (x_flags) a.xflag = stencil.xflag;

@@ -12,12 +12,21 @@
 namespace sptrsv {
 
 // Block of one lane per lockstep step: kStR grid rows x kStC grid columns.
-constexpr int kStR = 2;
-constexpr int kStC = 4;
+#ifndef SPTRSV_ST_R
+#define SPTRSV_ST_R 2
+#endif
+#ifndef SPTRSV_ST_C
+#define SPTRSV_ST_C 2
+#endif
+constexpr int kStR = SPTRSV_ST_R;
+constexpr int kStC = SPTRSV_ST_C;
 constexpr int kStLanes = 32;
 constexpr int kStBand = kStLanes * kStR;  // grid rows per task (one CTA)
 constexpr int kStBlock = kStR * kStC;     // elements per lane per step
-constexpr int kStG = 4;                   // steps per ring slot ("chunk"): the unit of every hand-over
+#ifndef SPTRSV_ST_G
+#define SPTRSV_ST_G 8
+#endif
+constexpr int kStG = SPTRSV_ST_G;         // steps per ring slot ("chunk"): the unit of every hand-over
 constexpr int kStOutSlots = 3;            // output ring (chunks) between the compute and the store warp
 
 // Per step, per lane: kStBlock elements; per element NF doubles:
@@ -29,7 +38,13 @@ __host__ __device__ constexpr int st_fields(bool exact) { return exact ? 4 : 3; 
 __host__ __device__ constexpr int st_step_bytes(bool exact) { return st_fields(exact) * kStBlock * kStLanes * 8; }
 // Input ring depth in chunks: (slots - 1) * kStG steps of copies stay in flight
 // (~20 steps at ~0.1 us per step covers the ~1.5 us DRAM latency).
-__host__ __device__ constexpr int st_slots(bool exact) { return exact ? 4 : 5; }
+#ifndef SPTRSV_ST_SLOTS_FAST
+#define SPTRSV_ST_SLOTS_FAST 5
+#endif
+#ifndef SPTRSV_ST_SLOTS_EXACT
+#define SPTRSV_ST_SLOTS_EXACT 4
+#endif
+__host__ __device__ constexpr int st_slots(bool exact) { return exact ? SPTRSV_ST_SLOTS_EXACT : SPTRSV_ST_SLOTS_FAST; }
 
 struct StencilPlan {
   bool ready = false;

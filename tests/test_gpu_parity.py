@@ -231,7 +231,7 @@ def test_stencil_executor_matches_oracle(shape, precision):
 
 
 def test_stencil_not_chosen_for_other_structures():
-    l = synth.lap2d(30, 10)  # nx not a multiple of the column block: general executors
+    l = synth.lap2d(31, 10)  # nx not a multiple of the column block: general executors
     plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="auto")
     assert plan.info()["executor"] != "stencil"
     plan.close()
