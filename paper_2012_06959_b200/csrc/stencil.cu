@@ -56,6 +56,13 @@ namespace {
 // p ^ (l & 7): the compute warp's 16-byte loads are conflict-free.
 constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
 
+// Mailbox sentinel: a signalling NaN. FP64 arithmetic propagates NaN
+// payloads but always quiets them (tools/microbench/nan_bits.cu), so no
+// solved value can alias it and values are published without conversion.
+// 32-bit periodic, so it is reset with one cuMemsetD32Async.
+constexpr unsigned kStNotReady32 = 0xFFF40000u;
+constexpr unsigned long long kStNotReady = 0xFFF40000FFF40000ull;
+
 struct alignas(64) StArgs {
   CUtensorMap bmap;  // kStBTma and b 16-byte aligned and a full last band: b via TMA
   const unsigned char* stream;
@@ -182,7 +189,7 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
   auto ld = [&]() { return sys ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p); };
   unsigned long long u = ld();
   int polls = 0, sleep_ns = 32;
-  while (u == kNotReady) {
+  while (u == kStNotReady) {
     ++polls;
     if (polls > spin_initial) {
       if ((polls & 63) == 0) {
@@ -390,6 +397,18 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     }
     if (long long* p = st_stamp(a, t, c, lane, 3)) *p = clock64();
     if (ok) ok = settle(c);
+    if (ok && c * kStG < kStLanes) {
+      // steps before this lane's first block: b must read as exact zeros
+      // (the TMA view put neighbouring rows there, the gather left them stale)
+      double2* dst = reinterpret_cast<double2*>(smem + S::kB + (c % NB) * S::kBChunk);
+#pragma unroll
+      for (int r = 0; r < kStR; ++r)
+#pragma unroll
+        for (int k = 0; k < kStG; ++k)
+          if (c * kStG - lane + k < 0)
+#pragma unroll
+            for (int h = 0; h < kStC / 2; ++h) dst[st_b_piece(r, lane, k, h)] = make_double2(0.0, 0.0);
+    }
     if (long long* p = st_stamp(a, t, c, lane, 4)) *p = clock64();
     ok = __all_sync(0xffffffffu, ok);
     if (!ok) {
@@ -427,7 +446,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     if (lane < kStG * kStC && j < nblk) {
       const unsigned long long u =
           st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote);
-      if (u == kNotReady) ok = false;
+      if (u == kStNotReady) ok = false;
       inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
@@ -546,7 +565,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
               xb[r][q] = __ddiv_rn(num, cur.dd[e]);
             } else {
               const double qv = __dmul_rn(num, cur.rd[e]);
-              bad |= !(markstein_ok(qv) && markstein_ok(num) && markstein_ok(cur.dd[e]));
+              // a zero numerator is exact too (x = +-0 with the IEEE sign):
+              // the zero-filled steps before a lane's first block stay fast
+              // (bitwise, not short-circuit: no branch per element)
+              const int ok = (int)markstein_ok(cur.dd[e]) &
+                             ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+              bad |= !ok;
               xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
             }
           } else if (q == 0) {
@@ -560,20 +584,27 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       }
       return bad;
     };
-    if (solve_block(false) && EXACT) solve_block(true);
-    // branch-free: a divergent branch here costs more than the whole FMA chain
+    if (solve_block(false) && EXACT) {
+      if (a.probe & 128) atomicAdd(&a.status->remote_reads, 1ull);  // diagnostics: count IEEE fallbacks
+      solve_block(true);
+    }
+    // No select on `active`: steps before a lane's first block see zero
+    // coefficients, zero b (the loader zero-fills it) and zero neighbours, so
+    // they compute exact zeros -- the boundary values the first block needs;
+    // steps past the last block compute garbage that only ever reaches
+    // other past-the-end steps (never published, never stored).
 #pragma unroll
-    for (int r = 0; r < kStR; ++r) xleft[r] = ((ABL & 8) || active) ? xb[r][kStC - 1] : xleft[r];
+    for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
 #pragma unroll
-    for (int q = 0; q < kStC; ++q) bottom[q] = ((ABL & 8) || active) ? xb[kStR - 1][q] : bottom[q];
+    for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
     if (!(ABL & 8)) {
 #pragma unroll
       for (int q = 0; q < kStC; ++q)
-        st_relaxed_u64_if(below + j * kStC + q, publishable(bottom[q]), publish && active);
+        st_relaxed_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish && active);
       if (PART) {
 #pragma unroll
         for (int q = 0; q < kStC; ++q)
-          st_relaxed_sys_u64_if(below + j * kStC + q, publishable(bottom[q]), publish_sys && active);
+          st_relaxed_sys_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish_sys && active);
       }
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
@@ -690,6 +721,26 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Reset `count` mailbox words to kStNotReady (cuMemsetD32Async through the
+// runtime's driver entry point).
+static cudaError_t fill_not_ready(unsigned long long* p, long long count, cudaStream_t s) {
+  typedef CUresult (*MemsetD32)(CUdeviceptr, unsigned int, size_t, CUstream);
+  static MemsetD32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemsetD32Async", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<MemsetD32>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  if (count <= 0) return cudaSuccess;
+  return fn((CUdeviceptr)p, kStNotReady32, (size_t)count * 2, (CUstream)s) == CUDA_SUCCESS ? cudaSuccess
+                                                                                          : cudaErrorUnknown;
+}
 
 // The skewed tensor view of b (see kStBTma); returns the number of bands it
 // covers (the full ones), 0 when the driver entry point or the encode fails.
@@ -813,8 +864,8 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
   if ((e = al((void**)&stencil.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&stencil.mbox, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
-      (e = cudaMemset(stencil.mbox, 0xFF, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) !=
-          cudaSuccess ||
+      (e = fill_not_ready(stencil.mbox, 2ll * stencil.n_tasks * nx, 0)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess ||
       (e = al((void**)&stencil.ticket, sizeof(int))) != cudaSuccess ||
       (e = al((void**)&stencil.bflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = al((void**)&stencil.xflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
@@ -841,8 +892,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   }
   // this solve uses mailbox half `par` (reset by the previous solve or at
   // build); reset the other half for the next one
-  if ((e = cudaMemsetAsync(stencil.mbox + (1 - par) * half, 0xFF, sizeof(unsigned long long) * half, s)) !=
-          cudaSuccess ||
+  if ((e = fill_not_ready(stencil.mbox + (1 - par) * half, half, s)) != cudaSuccess ||
       (e = cudaMemsetAsync(stencil.ticket, 0, sizeof(int), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
       (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
