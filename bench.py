@@ -2,7 +2,7 @@
 """Benchmark: fp64 SpTRSV on B200 — µs/solve and GFLOP/s (2·nnz/t), % of the HBM roofline.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config lap2d-4096]
-                    [--precision fast|exact] [--executor auto|rows|chains|stencil]
+                    [--precision fast|exact] [--executor auto|rows|chains|stencil|push]
     python bench.py --impl reference ...      # the reference's CPU path (oracle port)
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   # column-block over N GPUs
 
@@ -158,7 +158,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="lap2d-4096")
     ap.add_argument("--precision", choices=["fast", "exact"], default="fast")
-    ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil"], default="auto")
+    ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil", "push"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -48,7 +48,14 @@ enum { SPTRSV_PRECISION_EXACT = 0, SPTRSV_PRECISION_FAST = 1 };
  * with 2D five-point lower structure (detected; any coefficients). AUTO:
  * STENCIL when the structure is detected, else CHAINS when most dependencies
  * stay inside a warp task, else ROWS. */
-enum { SPTRSV_EXECUTOR_AUTO = 0, SPTRSV_EXECUTOR_ROWS = 1, SPTRSV_EXECUTOR_CHAINS = 2, SPTRSV_EXECUTOR_STENCIL = 3 };
+enum {
+  SPTRSV_EXECUTOR_AUTO = 0,
+  SPTRSV_EXECUTOR_ROWS = 1,
+  SPTRSV_EXECUTOR_CHAINS = 2,
+  SPTRSV_EXECUTOR_STENCIL = 3,
+  SPTRSV_EXECUTOR_PUSH = 4 /* paper Alg. 2 / solve_shared_atomics (engine.py:324-431): warp per column, fp64
+                              atomics on shared left sums + in-degree counters; rounding-level nondeterministic */
+};
 
 /* plan flags */
 enum {

@@ -138,6 +138,12 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   if (rc != SPTRSV_OK) return rc;
 
   executor_used = SPTRSV_EXECUTOR_ROWS;
+  if (!structure_only && opt.executor == SPTRSV_EXECUTOR_PUSH) {
+    rc = build_push();
+    if (rc != SPTRSV_OK) return rc;
+    executor_used = SPTRSV_EXECUTOR_PUSH;
+    return SPTRSV_OK;
+  }
   if (!structure_only && opt.executor != SPTRSV_EXECUTOR_ROWS) {
     // host copy of the CSR structure for the schedulers
     std::vector<int> h_rp(n + 1), h_ci(noff);

@@ -50,6 +50,24 @@ struct DevicePlan {
 
   ChainPlan chains;
   StencilPlan stencil;
+  // push executor (solve_push.cu): CSC of the off-diagonals + shared counters
+  struct PushPlan {
+    bool ready = false;
+    int* cp = nullptr;
+    int* ri = nullptr;
+    double* v_exact = nullptr;
+    double* v_fast = nullptr;
+    double* left = nullptr;
+    int* count = nullptr;
+    void release() {
+      void* ptrs[] = {cp, ri, v_exact, v_fast, left, count};
+      for (void* p : ptrs)
+        if (p) cudaFree(p);
+      *this = PushPlan();
+    }
+  } push;
+  int build_push();
+  int solve_push(const double* d_b, double* d_x, cudaStream_t s);
 
   // PE partition (partition.cu): each PE owns components (PartitionPlan.owner_arr)
   // and publishes their x only into its own segment; other PEs read it.
