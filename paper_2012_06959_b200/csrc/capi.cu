@@ -54,6 +54,7 @@ void DevicePlan::release() {
     if (p) cudaFree(p);
   chains.release();
   stencil.release();
+  stencil3.release();
   push.release();
   release_partition();
   if (ev0) cudaEventDestroy(ev0);
@@ -191,7 +192,8 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   CUDA_TRY(cudaEventRecord(ev0, s));
   if (stencil.part) rc = solve_stencil(d_b, d_x, s);
   else if (seg_table) rc = solve_partitioned_rows(d_b, d_x, s);
-  else if (executor_used == SPTRSV_EXECUTOR_STENCIL) rc = solve_stencil(d_b, d_x, s);
+  else if (executor_used == SPTRSV_EXECUTOR_STENCIL)
+    rc = stencil3.ready ? solve_stencil3d(d_b, d_x, s) : solve_stencil(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_PUSH) rc = solve_push(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
   else rc = solve_rows(d_b, d_x, s);

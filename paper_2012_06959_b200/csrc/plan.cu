@@ -156,8 +156,16 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
         executor_used = SPTRSV_EXECUTOR_STENCIL;
         return SPTRSV_OK;
       }
+      rc = build_stencil3d(h_rp, h_ci);
+      if (rc != SPTRSV_OK) return rc;
+      if (stencil3.ready) {
+        executor_used = SPTRSV_EXECUTOR_STENCIL;
+        return SPTRSV_OK;
+      }
       if (opt.executor == SPTRSV_EXECUTOR_STENCIL)
-        return plan_fail(SPTRSV_E_UNSUPPORTED, "stencil executor requested but L is not 2D five-point lower structured");
+        return plan_fail(SPTRSV_E_UNSUPPORTED,
+                         "stencil executor requested but L is neither 2D five-point nor 3D seven-point lower "
+                         "structured");
     }
     rc = build_chains(h_rp, h_ci);
     if (rc != SPTRSV_OK) return rc;

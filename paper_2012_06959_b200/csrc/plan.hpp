@@ -50,6 +50,9 @@ struct DevicePlan {
 
   ChainPlan chains;
   StencilPlan stencil;
+  Stencil3Plan stencil3;
+  int build_stencil3d(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
+  int solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s);
   // push executor (solve_push.cu): CSC of the off-diagonals + shared counters
   struct PushPlan {
     bool ready = false;

@@ -38,6 +38,7 @@
 #include <cuda.h>
 #include "plan.hpp"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace sptrsv {
 
@@ -119,73 +120,10 @@ __host__ __device__ constexpr int st_b_piece(int r, int l, int k, int h) {
 }
 static_assert(kStG * kStC / 2 >= 8 || !kStBTma, "the swizzle spans eight 16-byte pieces");
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned phase) {
-  unsigned ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-// 4-D tiled TMA load into shared memory, completing on `bar` (complete_tx)
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-      "[%6];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void st_relaxed_sys_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.sys.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v),
-      "r"((int)pred)
-      : "memory");
-}
-// predicated relaxed store (no branch around it)
-__device__ __forceinline__ void st_relaxed_u64_if(unsigned long long* p, unsigned long long v, bool pred) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.relaxed.gpu.global.b64 [%0], %1;\n\t}" ::"l"(p), "l"(v),
-      "r"((int)pred)
-      : "memory");
-}
-// arrive on `bar` once all of this thread's earlier cp.async have landed
-__device__ __forceinline__ void cp_async_arrive_noinc(unsigned long long* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// chunk counters shared by the three warps of a CTA
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
 
 __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, int* abort_flag, DeviceStatus* status,
                                                    int spin_initial, int spin_max_ns, unsigned long long deadline,
-                                                   bool sys) {
+                                                   bool sys, unsigned long long& spins) {
   auto ld = [&]() { return sys ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p); };
   unsigned long long u = ld();
   int polls = 0, sleep_ns = 32;
@@ -205,7 +143,7 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
     }
     u = ld();
   }
-  if (polls) atomicAdd(&status->spins, (unsigned long long)polls);
+  spins += polls;  // added to status->spins once per task (no per-miss global atomic)
   return u;
 }
 
@@ -438,6 +376,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const unsigned long long* above = (remote ? a.pe_mbox[up_pe] + a.mbox_half : a.mbox) + (size_t)(t - 1) * a.nx;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int k = lane / kStC, q = lane % kStC;
+  unsigned long long spins = 0;
   for (int c = 0; c < nchunks; ++c) {
     // inbox slot c % NB is free once the compute warp finished chunk c - NB
     if (c >= NB && !wait_ctl(ctl, kCtlInDone, c - NB + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
@@ -445,13 +384,17 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     const int j = c * kStG + k;
     if (lane < kStG * kStC && j < nblk) {
       const unsigned long long u =
-          st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote);
+          st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote,
+                  spins);
       if (u == kStNotReady) ok = false;
       inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
+  if (lane == 0 && spins) atomicAdd(&a.status->spins, spins);
   if (remote && lane == 0) atomicAdd(&a.status->remote_reads, (unsigned long long)a.nx);
 }
 

@@ -111,4 +111,25 @@ struct StencilPlan {
   }
 };
 
+// 3D seven-point lower structure (stencil3d.cu): tiles of 32 y-rows x 4
+// z-planes, one CTA each, dispatched in ascending (Z, Y) order.
+struct Stencil3Plan {
+  bool ready = false;
+  bool exact = true;
+  int nx = 0, ny = 0, nz = 0, nyt = 0, nzt = 0, n_tasks = 0, steps = 0;
+  long long stream_bytes = 0;
+  double build_ms = 0.0;
+  long long solves = 0;  // mailbox parity
+  unsigned char* stream = nullptr;
+  unsigned long long* ymail = nullptr;  // [2][tasks][4][nx]
+  unsigned long long* zmail = nullptr;  // [2][tasks][32][nx]
+  int* ticket = nullptr;
+  void release() {
+    void* ptrs[] = {stream, ymail, zmail, ticket};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    *this = Stencil3Plan();
+  }
+};
+
 }  // namespace sptrsv

@@ -1,0 +1,683 @@
+// Register-blocked, warp-specialised wavefront executor for 3D seven-point
+// lower structure (lap3d-128, BASELINE configs[1]).
+//
+// Structure: row i = (z*ny + y)*nx + x stores (i, i - nx*ny) iff z > 0,
+// (i, i - nx) iff y > 0 and (i, i - 1) iff x > 0 (plus the diagonal), any
+// coefficients — detected from the CSR at plan time. The DAG is the 3D
+// wavefront: nx + ny + nz - 2 levels (382 for 128^3).
+//
+// Tiling: a task (one CTA) owns a tile of 32 grid rows in y (one per lane)
+// by k3R = 4 planes in z, all nx columns. Lane l at lockstep step s solves,
+// for its k3R rows (z0 + r, y0 + l), the k3C = 2 columns of block j = s - l:
+//   * the y-neighbour of every row comes from lane l - 1's block of the
+//     previous step (k3R * k3C values per step by __shfl_up_sync; lane 0
+//     takes them from the tile above in y, polled from its y-mailbox);
+//   * the z-neighbour of row r > 0 is the lane's own row r - 1 of this
+//     block (registers); row 0's comes from the tile behind in z (its last
+//     plane, polled from its z-mailbox);
+//   * the x-neighbour is the lane's previous block.
+// Tiles are dispatched in ascending (Z, Y) order, each depending only on the
+// tiles at (Y-1, Z) and (Y, Z-1) — the reference's progress rule. A tile
+// trails the one behind it in z by one chunk plus a mailbox round trip (not
+// by the 32-step lane skew, which only separates tiles in y), so the
+// critical path is ~3 y-hops + nz/k3R z-hops + nx/k3C steps.
+//
+// Warps: 0 compute (the only one on the critical path), 1 loader (TMA bulk
+// copy of the pre-packed coefficient stream + cp.async of b), 2 storer (x
+// from a shared-memory ring), 3 poller (both mailboxes into shared-memory
+// inboxes). Hand-overs are monotone chunk counters at CTA scope, as in
+// stencil.cu; mailboxes are value-is-flag with a signalling-NaN sentinel and
+// double-buffered by solve parity.
+//
+// Arithmetic: fast: x = wy*y + (wz*z + (wx*left + b/d)) with pre-scaled
+// coefficients; exact: s = 0 + lz*z, s += ly*y, s += lx*left, x = (b - s)/d —
+// the serial oracle's ascending-column order with separate IEEE operations
+// (absent boundary terms contribute +0 and leave every partial sum unchanged),
+// Markstein division with a branch-free guard and an IEEE fallback.
+#include <vector>
+#include <chrono>
+#include <cstring>
+#include <algorithm>
+#include "plan.hpp"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace sptrsv {
+
+int plan_fail(int code, const char* msg);
+
+namespace {
+
+constexpr int k3R = 4, k3C = 2, k3G = 4, k3Lanes = 32;
+constexpr int k3Blk = k3R * k3C;
+constexpr int k3Pairs = k3Blk / 2;
+constexpr int k3OutSlots = 3;
+constexpr int k3Threads = 4 * 32;
+constexpr unsigned k3NotReady32 = 0xFFF40000u;  // signalling NaN, as in stencil.cu
+constexpr unsigned long long k3NotReady = 0xFFF40000FFF40000ull;
+static_assert(k3R * k3C * k3G == 32, "the poller fetches the y-inbox of a chunk with one value per lane");
+
+__host__ __device__ constexpr int s3_fields(bool exact) { return exact ? 5 : 4; }  // wz wy wx [d] rd
+__host__ __device__ constexpr int s3_step_bytes(bool exact) { return s3_fields(exact) * k3Pairs * k3Lanes * 16; }
+__host__ __device__ constexpr int s3_slots(bool exact) { return exact ? 3 : 4; }
+
+struct S3Args {
+  const unsigned char* stream;  // [task][step][field][pair][lane] f64x2
+  unsigned long long* ymail;    // this solve's half: [task][k3R][nx] (lane 31's rows)
+  unsigned long long* zmail;    // this solve's half: [task][32][nx] (plane z0 + k3R - 1)
+  int* ticket;
+  const double* b;
+  double* x;
+  DeviceStatus* status;
+  int* abort_flag;
+  unsigned long long timeout_ns;
+  int spin_initial, spin_max_ns;
+  int nx, ny, nz, nyt, nzt, n_tasks, steps;
+  int b_aligned, x_aligned;  // 16-byte vector paths (else 8-byte halves)
+  long long* dbg;            // diagnostics (probe_flags & 16): per-task globaltimer [start, ready, end]
+};
+
+template <bool EXACT>
+struct S3Smem {
+  static constexpr int kSlots = s3_slots(EXACT);
+  static constexpr int kStep = s3_step_bytes(EXACT);
+  static constexpr int kCoefChunk = k3G * kStep;
+  static constexpr int kBChunk = k3R * k3G * k3Lanes * 16;     // [r][k][lane] f64x2
+  static constexpr int kZChunk = k3G * k3Lanes * 16;           // [k][lane] f64x2
+  static constexpr int kYChunk = k3G * k3R * k3C * 8;          // [k][r][q] f64
+  static constexpr int kOutChunk = k3G * k3Pairs * k3Lanes * 16;  // [k][pair][lane] f64x2
+  static constexpr int kCoef = 0;
+  static constexpr int kB = kCoef + kSlots * kCoefChunk;
+  static constexpr int kZ = kB + kSlots * kBChunk;
+  static constexpr int kY = kZ + kSlots * kZChunk;
+  static constexpr int kOut = kY + kSlots * kYChunk;
+  static constexpr int kBars = kOut + k3OutSlots * kOutChunk;
+  static constexpr int kCtl = kBars + 8 * kSlots;
+  static constexpr int kTotal = kCtl + 64;
+};
+
+enum { kC3Task = 0, kC3InReady = 1, kC3InDone = 2, kC3OutReady = 3, kC3OutDone = 4, kC3Abort = 5, kC3MbReady = 6 };
+
+__device__ __forceinline__ bool s3_wait(const int* ctl, int which, int need, unsigned long long deadline, int nap) {
+  int polls = 0;
+  while (ld_acquire_cta(ctl + which) < need) {
+    if (ld_acquire_cta(ctl + kC3Abort)) return false;
+    if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
+    if (nap) __nanosleep(nap);
+  }
+  return true;
+}
+
+__device__ __forceinline__ void s3_abort(const S3Args& a, int* ctl, int lane) {
+  if (lane == 0) {
+    atomicExch(&a.status->code, 5);
+    atomicExch(a.abort_flag, 1);
+    st_release_cta(ctl + kC3Abort, 1);
+  }
+}
+
+// ---- warp 1: coefficient stream (TMA bulk) and b (cp.async) ----------------
+template <bool EXACT>
+__device__ void s3_loader(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane, unsigned& phase_bits,
+                          unsigned long long deadline) {
+  using S = S3Smem<EXACT>;
+  constexpr int NB = S::kSlots;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
+  const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
+  const int Y = t % a.nyt, Z = t / a.nyt;
+  const int y = Y * k3Lanes + lane;
+  const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+  auto issue = [&](int c) {
+    const int slot = c % NB;
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[slot], S::kCoefChunk);
+      bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk,
+               &bars[slot]);
+    }
+    double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk) + lane;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      const int z = Z * k3R + r;
+#pragma unroll
+      for (int k = 0; k < k3G; ++k) {
+        const int j = c * k3G + k - lane;
+        double2* d = dst + (r * k3G + k) * k3Lanes;
+        if (j >= 0 && j < nblk && y < a.ny && z < a.nz) {
+          const double* src = a.b + ((size_t)z * a.ny + y) * a.nx + (size_t)j * k3C;
+          if (a.b_aligned) {
+            cp_async16(d, src);
+          } else {
+            cp_async8(&d->x, src);
+            cp_async8(&d->y, src + 1);
+          }
+        } else {
+          *d = make_double2(0.0, 0.0);  // padding computes exact zeros
+        }
+      }
+    }
+    cp_async_arrive_noinc(&bars[slot]);
+  };
+  int issued = 0;
+  bool ok = true;
+  for (int c = 0; c < nchunks; ++c) {
+    const int done = ld_acquire_cta(ctl + kC3InDone);
+    while (issued < nchunks && issued < done + NB) issue(issued++);
+    while (ok && issued <= c) {
+      ok = s3_wait(ctl, kC3InDone, issued - NB + 1, deadline, 64);
+      if (ok) issue(issued++);
+    }
+    if (ok) {
+      const int slot = c % NB;
+      const unsigned ph = (phase_bits >> slot) & 1u;
+      int polls = 0;
+      while (!mbar_try_wait(&bars[slot], ph)) {
+        if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) {
+          ok = false;
+          break;
+        }
+      }
+      if (ok) phase_bits ^= 1u << slot;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) {
+      s3_abort(a, ctl, lane);
+      return;
+    }
+    if (lane == 0) st_release_cta(ctl + kC3InReady, c + 1);
+  }
+}
+
+// ---- warp 3: both mailboxes into the chunk's inboxes -----------------------
+template <bool EXACT>
+__device__ void s3_poller(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane,
+                          unsigned long long deadline) {
+  using S = S3Smem<EXACT>;
+  constexpr int NB = S::kSlots;
+  const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
+  const int Y = t % a.nyt, Z = t / a.nyt;
+  // z-inbox: lane l's row-0 z-neighbours = plane z0 - 1, lane l, of the tile behind
+  const unsigned long long* zsrc = Z > 0 ? a.zmail + ((size_t)(t - a.nyt) * k3Lanes + lane) * a.nx : nullptr;
+  // y-inbox: lane 0's y-neighbours = lane 31's rows of the tile above; value
+  // (k, r, q) of the chunk is polled by lane k * R * C + r * C + q
+  const int yk = lane / (k3R * k3C), yr = (lane / k3C) % k3R, yq = lane % k3C;
+  const unsigned long long* ysrc = Y > 0 ? a.ymail + ((size_t)(t - 1) * k3R + yr) * a.nx : nullptr;
+  unsigned long long spins = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    if (c >= NB && !s3_wait(ctl, kC3InDone, c - NB + 1, deadline, 64)) return s3_abort(a, ctl, lane);
+    const int slot = c % NB;
+    bool ok = true;
+    // the chunk's words are polled all at once: every round re-issues the
+    // loads of the words still not ready as independent requests, so a
+    // round costs one L2 round trip however many words it covers
+    unsigned long long zw[k3G][k3C], yw = 0;
+    const int jy = c * k3G + yk;  // lane 0's block at step c*G + yk
+    bool zneed[k3G][k3C], yneed = ysrc && jy < nblk;
+#pragma unroll
+    for (int k = 0; k < k3G; ++k) {
+      const int j = c * k3G + k - lane;
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) {
+        zneed[k][q] = zsrc && j >= 0 && j < nblk;
+        zw[k][q] = 0ull;
+      }
+    }
+    int polls = 0, sleep_ns = 32;
+    while (true) {
+      bool pending = false;
+#pragma unroll
+      for (int k = 0; k < k3G; ++k) {
+        const int j = c * k3G + k - lane;
+#pragma unroll
+        for (int q = 0; q < k3C; ++q)
+          if (zneed[k][q]) zw[k][q] = ld_relaxed_u64(zsrc + (size_t)j * k3C + q);
+      }
+      if (yneed) yw = ld_relaxed_u64(ysrc + (size_t)jy * k3C + yq);
+#pragma unroll
+      for (int k = 0; k < k3G; ++k)
+#pragma unroll
+        for (int q = 0; q < k3C; ++q) {
+          zneed[k][q] = zneed[k][q] && zw[k][q] == k3NotReady;
+          pending |= zneed[k][q];
+        }
+      yneed = yneed && yw == k3NotReady;
+      pending |= yneed;
+      if (!pending) break;
+      ++spins;
+      if (++polls > a.spin_initial) {
+        if ((polls & 63) == 0 &&
+            (ld_relaxed_s32(a.abort_flag) || (deadline && globaltimer_ns() > deadline))) {
+          ok = false;
+          break;
+        }
+        __nanosleep(sleep_ns);
+        if (sleep_ns < a.spin_max_ns) sleep_ns <<= 1;
+      }
+    }
+    double2* zin = reinterpret_cast<double2*>(smem + S::kZ + slot * S::kZChunk);
+#pragma unroll
+    for (int k = 0; k < k3G; ++k) zin[k * k3Lanes + lane] = make_double2(as_f64(zw[k][0]), as_f64(zw[k][1]));
+    double* yin = reinterpret_cast<double*>(smem + S::kY + slot * S::kYChunk);
+    yin[(yk * k3R + yr) * k3C + yq] = as_f64(yw);
+    if (!__all_sync(0xffffffffu, ok)) return s3_abort(a, ctl, lane);
+    if (lane == 0) st_release_cta(ctl + kC3MbReady, c + 1);
+    if (a.dbg && lane == 0 && c == 0 && t < 192) a.dbg[2 * t] = (long long)globaltimer_ns();  // diagnostics
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
+  if (lane == 0 && spins) atomicAdd(&a.status->spins, spins);
+}
+
+// ---- warp 2: solved blocks to x ---------------------------------------------
+template <bool EXACT>
+__device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane,
+                          unsigned long long deadline) {
+  using S = S3Smem<EXACT>;
+  const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
+  const int Y = t % a.nyt, Z = t / a.nyt;
+  const int y = Y * k3Lanes + lane;
+  for (int c = 0; c < nchunks; ++c) {
+    if (!s3_wait(ctl, kC3OutReady, c + 1, deadline, 64)) return s3_abort(a, ctl, lane);
+    const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk);
+#pragma unroll
+    for (int k = 0; k < k3G; ++k) {
+      const int j = c * k3G + k - lane;
+      if (j < 0 || j >= nblk || y >= a.ny) continue;
+#pragma unroll
+      for (int r = 0; r < k3R; ++r) {
+        const int z = Z * k3R + r;
+        if (z >= a.nz) continue;
+        double* row = a.x + ((size_t)z * a.ny + y) * a.nx + (size_t)j * k3C;
+        const double2 v = src[(k * k3Pairs + r) * k3Lanes + lane];
+        if (a.x_aligned) {
+          *reinterpret_cast<double2*>(row) = v;
+        } else {
+          row[0] = v.x;
+          row[1] = v.y;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kC3OutDone, c + 1);
+  }
+}
+
+// ---- warp 0: the lockstep wavefront -----------------------------------------
+template <bool EXACT>
+struct S3Blk {
+  double wz[k3Blk], wy[k3Blk], wx[k3Blk], dd[k3Blk], rd[k3Blk], bv[k3Blk];
+  double zin[k3C], yin[k3R][k3C];
+  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int k, int lane) {
+    using S = S3Smem<EXACT>;
+    const double2* cs = reinterpret_cast<const double2*>(smem + S::kCoef + slot * S::kCoefChunk + k * S::kStep);
+#pragma unroll
+    for (int p = 0; p < k3Pairs; ++p) {
+      const double2 fz = cs[(0 * k3Pairs + p) * k3Lanes + lane];
+      const double2 fy = cs[(1 * k3Pairs + p) * k3Lanes + lane];
+      const double2 fx = cs[(2 * k3Pairs + p) * k3Lanes + lane];
+      wz[2 * p] = fz.x, wz[2 * p + 1] = fz.y;
+      wy[2 * p] = fy.x, wy[2 * p + 1] = fy.y;
+      wx[2 * p] = fx.x, wx[2 * p + 1] = fx.y;
+      if (EXACT) {
+        const double2 d = cs[(3 * k3Pairs + p) * k3Lanes + lane];
+        const double2 r = cs[(4 * k3Pairs + p) * k3Lanes + lane];
+        dd[2 * p] = d.x, dd[2 * p + 1] = d.y;
+        rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
+      } else {
+        const double2 r = cs[(3 * k3Pairs + p) * k3Lanes + lane];
+        rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
+      }
+    }
+    const double2* bb = reinterpret_cast<const double2*>(smem + S::kB + slot * S::kBChunk) + lane;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      const double2 v = bb[(r * k3G + k) * k3Lanes];
+      bv[r * k3C] = v.x, bv[r * k3C + 1] = v.y;
+    }
+    const double2 zz = reinterpret_cast<const double2*>(smem + S::kZ + slot * S::kZChunk)[k * k3Lanes + lane];
+    zin[0] = zz.x, zin[1] = zz.y;
+    const double* yy = reinterpret_cast<const double*>(smem + S::kY + slot * S::kYChunk) + k * k3R * k3C;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r)
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) yin[r][q] = yy[r * k3C + q];
+  }
+};
+
+template <bool EXACT>
+__device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane,
+                           unsigned long long deadline) {
+  using S = S3Smem<EXACT>;
+  constexpr int NB = S::kSlots;
+  const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
+  const int Y = t % a.nyt, Z = t / a.nyt;
+  // publish: lane 31's rows for the tile below in y, every lane's last plane
+  // for the tile in front in z
+  unsigned long long* ypub = a.ymail + (size_t)t * k3R * a.nx;
+  unsigned long long* zpub = a.zmail + ((size_t)t * k3Lanes + lane) * a.nx;
+  const bool pub_y = lane == k3Lanes - 1 && Y + 1 < a.nyt;
+  const bool pub_z = Z + 1 < a.nzt;
+  double xleft[k3R], prev[k3R][k3C];
+#pragma unroll
+  for (int r = 0; r < k3R; ++r) {
+    xleft[r] = 0.0;
+#pragma unroll
+    for (int q = 0; q < k3C; ++q) prev[r][q] = 0.0;
+  }
+  auto step = [&](int c, int k, const S3Blk<EXACT>& cur, S3Blk<EXACT>& nxt) -> bool {
+    const int s = c * k3G + k;
+    const int j = s - lane;
+    const bool active = j >= 0 && j < nblk;
+    double yn[k3R][k3C];
+#pragma unroll
+    for (int r = 0; r < k3R; ++r)
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) {
+        const double up = __shfl_up_sync(0xffffffffu, prev[r][q], 1);
+        yn[r][q] = lane == 0 ? cur.yin[r][q] : up;
+      }
+    double xb[k3R][k3C];
+    auto solve_block = [&](bool ieee) -> bool {
+      bool bad = false;
+#pragma unroll
+      for (int r = 0; r < k3R; ++r) {
+#pragma unroll
+        for (int q = 0; q < k3C; ++q) {
+          const int e = r * k3C + q;
+          const double zn = r == 0 ? cur.zin[q] : xb[r - 1][q];
+          const double left = q == 0 ? xleft[r] : xb[r][q - 1];
+          if (EXACT) {
+            double acc = __dadd_rn(0.0, __dmul_rn(cur.wz[e], zn));
+            acc = __dadd_rn(acc, __dmul_rn(cur.wy[e], yn[r][q]));
+            acc = __dadd_rn(acc, __dmul_rn(cur.wx[e], left));
+            const double num = __dsub_rn(cur.bv[e], acc);
+            if (ieee) {
+              xb[r][q] = __ddiv_rn(num, cur.dd[e]);
+            } else {
+              const double qv = __dmul_rn(num, cur.rd[e]);
+              const int ok = (int)markstein_ok(cur.dd[e]) &
+                             ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+              bad |= !ok;
+              xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
+            }
+          } else {
+            const double inner = __fma_rn(cur.wz[e], zn, __fma_rn(cur.wx[e], left, __dmul_rn(cur.bv[e], cur.rd[e])));
+            xb[r][q] = __fma_rn(cur.wy[e], yn[r][q], inner);
+          }
+        }
+      }
+      return bad;
+    };
+    if (solve_block(false) && EXACT) solve_block(true);
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      xleft[r] = xb[r][k3C - 1];
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) prev[r][q] = xb[r][q];
+    }
+#pragma unroll
+    for (int r = 0; r < k3R; ++r)
+#pragma unroll
+      for (int q = 0; q < k3C; ++q)
+        st_relaxed_u64_if(ypub + (size_t)r * a.nx + (size_t)j * k3C + q, as_u64(xb[r][q]), pub_y && active);
+#pragma unroll
+    for (int q = 0; q < k3C; ++q)
+      st_relaxed_u64_if(zpub + (size_t)j * k3C + q, as_u64(xb[k3R - 1][q]), pub_z && active);
+    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk) + k * k3Pairs * k3Lanes +
+                   lane;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) dst[r * k3Lanes] = make_double2(xb[r][0], xb[r][1]);
+    if (a.dbg && lane == 0 && c == 0 && k == k3G - 1 && t < 192) a.dbg[2 * t + 1] = (long long)globaltimer_ns();
+    if (k + 1 < k3G) {
+      nxt.load(smem, c % NB, k + 1, lane);
+    } else {
+      __syncwarp();
+      if (lane == 0) {
+        st_release_cta(ctl + kC3OutReady, c + 1);
+        st_release_cta(ctl + kC3InDone, c + 1);
+      }
+      if (c + 1 < nchunks) {
+        if (!s3_wait(ctl, kC3InReady, c + 2, deadline, 0)) return false;
+        if (!s3_wait(ctl, kC3MbReady, c + 2, deadline, 0)) return false;
+        if (c + 1 >= k3OutSlots && !s3_wait(ctl, kC3OutDone, c + 2 - k3OutSlots, deadline, 0)) return false;
+        nxt.load(smem, (c + 1) % NB, 0, lane);
+      }
+    }
+    return true;
+  };
+  long long* ts = (a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * 64 + 3 * t : nullptr;
+  if (ts) ts[0] = (long long)globaltimer_ns();
+  S3Blk<EXACT> A, B;
+  if (!s3_wait(ctl, kC3InReady, 1, deadline, 0) || !s3_wait(ctl, kC3MbReady, 1, deadline, 0))
+    return s3_abort(a, ctl, lane);
+  if (ts) ts[1] = (long long)globaltimer_ns();
+  A.load(smem, 0, 0, lane);
+  for (int c = 0; c < nchunks; ++c) {
+    static_assert(k3G % 2 == 0, "chunks hold an even number of steps");
+#pragma unroll
+    for (int k = 0; k < k3G; k += 2) {
+      if (!step(c, k, A, B)) return s3_abort(a, ctl, lane);
+      if (!step(c, k + 1, B, A)) return s3_abort(a, ctl, lane);
+    }
+  }
+  if (ts) ts[2] = (long long)globaltimer_ns();
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(k3Threads, 1) k_stencil3d(const __grid_constant__ S3Args a) {
+  using S = S3Smem<EXACT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  int* ctl = reinterpret_cast<int*>(smem + S::kCtl);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
+    for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1 + k3Lanes);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned phase_bits = 0;
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      ctl[kC3Task] = atomicAdd(a.ticket, 1);  // ascending (Z, Y): the progress rule
+      ctl[kC3InReady] = ctl[kC3InDone] = ctl[kC3OutReady] = ctl[kC3OutDone] = ctl[kC3Abort] = 0;
+      ctl[kC3MbReady] = 0;
+    }
+    __syncthreads();
+    const int t = ctl[kC3Task];
+    if (t >= a.n_tasks) break;
+    if (warp == 0) s3_compute<EXACT>(a, smem, ctl, t, lane, deadline);
+    else if (warp == 1) s3_loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
+    else if (warp == 2) s3_storer<EXACT>(a, smem, ctl, t, lane, deadline);
+    else s3_poller<EXACT>(a, smem, ctl, t, lane, deadline);
+    __syncthreads();
+    if (ctl[kC3Abort]) break;
+  }
+}
+
+template <bool EXACT>
+cudaError_t launch_s3(const S3Args& a, int blocks, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_stencil3d<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         S3Smem<EXACT>::kTotal);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_stencil3d<EXACT><<<blocks, k3Threads, S3Smem<EXACT>::kTotal, s>>>(a);
+  return cudaGetLastError();
+}
+
+static cudaError_t s3_fill_not_ready(unsigned long long* p, long long words, cudaStream_t s) {
+  typedef CUresult (*MemsetD32)(CUdeviceptr, unsigned int, size_t, CUstream);
+  static MemsetD32 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemsetD32Async", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<MemsetD32>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  if (words <= 0) return cudaSuccess;
+  return fn((CUdeviceptr)p, k3NotReady32, (size_t)words * 2, (CUstream)s) == CUDA_SUCCESS ? cudaSuccess
+                                                                                         : cudaErrorUnknown;
+}
+
+}  // namespace
+
+// 3D seven-point lower structure on the host CSR: returns true and (nx, ny, nz).
+static bool detect_stencil3d(long long n, const std::vector<int>& rp, const std::vector<int>& ci, int* dims) {
+  if (n < 8) return false;
+  long long nx = 0, nxy = 0;
+  for (long long i = 1; i < n && (!nx || !nxy); ++i)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const long long d = i - ci[k];
+      if (d > 1 && !nx) nx = d;
+      else if (nx && d > nx && !nxy) nxy = d;
+    }
+  if (nx < 2 || nxy < 2 * nx || nxy % nx || n % nxy || nx % k3C || nx > (1 << 24)) return false;
+  const long long ny = nxy / nx, nz = n / nxy;
+  if (nz < 2 || ny < 2) return false;
+  for (long long i = 0; i < n; ++i) {
+    const long long x = i % nx, y = (i / nx) % ny, z = i / nxy;
+    int k = rp[i];
+    if (z > 0) {
+      if (k >= rp[i + 1] || ci[k] != i - nxy) return false;
+      ++k;
+    }
+    if (y > 0) {
+      if (k >= rp[i + 1] || ci[k] != i - nx) return false;
+      ++k;
+    }
+    if (x > 0) {
+      if (k >= rp[i + 1] || ci[k] != i - 1) return false;
+      ++k;
+    }
+    if (k != rp[i + 1]) return false;
+  }
+  dims[0] = (int)nx, dims[1] = (int)ny, dims[2] = (int)nz;
+  return true;
+}
+
+int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<int>& h_ci) {
+  auto t0 = std::chrono::steady_clock::now();
+  stencil3.release();
+  int dims[3];
+  if (!detect_stencil3d(n, h_rp, h_ci, dims)) return SPTRSV_OK;
+  const bool exact = opt.precision != SPTRSV_PRECISION_FAST;
+  Stencil3Plan& P = stencil3;
+  P.exact = exact;
+  P.nx = dims[0], P.ny = dims[1], P.nz = dims[2];
+  P.nyt = (P.ny + k3Lanes - 1) / k3Lanes;
+  P.nzt = (P.nz + k3R - 1) / k3R;
+  P.n_tasks = P.nyt * P.nzt;
+  const int nblk = P.nx / k3C;
+  P.steps = (nblk + k3Lanes - 1 + k3G - 1) / k3G * k3G;
+  const int NF = s3_fields(exact);
+  const size_t step_doubles = s3_step_bytes(exact) / 8;
+  const size_t bytes = s3_step_bytes(exact) * (size_t)P.steps * P.n_tasks;
+  std::vector<double> h_val(noff), h_dg(n), h_rdg(n);
+  cudaError_t e;
+  if ((noff && (e = cudaMemcpy(h_val.data(), exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
+                   cudaSuccess) ||
+      (e = cudaMemcpy(h_dg.data(), dg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(h_rdg.data(), rdg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  std::vector<double> st(bytes / 8, 0.0);
+  for (int t = 0; t < P.n_tasks; ++t) {
+    const int Y = t % P.nyt, Z = t / P.nyt;
+    for (int s = 0; s < P.steps; ++s) {
+      double* sb = st.data() + ((size_t)t * P.steps + s) * step_doubles;
+      for (int l = 0; l < k3Lanes; ++l) {
+        const int j = s - l;
+        const long long y = (long long)Y * k3Lanes + l;
+        for (int r = 0; r < k3R; ++r) {
+          const long long z = (long long)Z * k3R + r;
+          for (int q = 0; q < k3C; ++q) {
+            const int e_ = r * k3C + q, pair = e_ / 2, half = e_ % 2;
+            double f[5] = {0.0, 0.0, 0.0, exact ? 1.0 : 0.0, exact ? 1.0 : 0.0};
+            if (!exact) f[3] = 0.0;  // fast: fields wz wy wx rd (rd of padding 0)
+            if (j >= 0 && j < nblk && y < P.ny && z < P.nz) {
+              const long long x = (long long)j * k3C + q;
+              const long long i = (z * P.ny + y) * P.nx + x;
+              int kk = h_rp[i];
+              const double fz = z > 0 ? h_val[kk++] : 0.0;
+              const double fy = y > 0 ? h_val[kk++] : 0.0;
+              const double fx = x > 0 ? h_val[kk] : 0.0;
+              if (exact) {
+                f[0] = fz, f[1] = fy, f[2] = fx, f[3] = h_dg[i], f[4] = h_rdg[i];
+              } else {
+                f[0] = fz, f[1] = fy, f[2] = fx, f[3] = h_rdg[i];
+              }
+            }
+            for (int fld = 0; fld < NF; ++fld) sb[((fld * k3Pairs + pair) * k3Lanes + l) * 2 + half] = f[fld];
+          }
+        }
+      }
+    }
+  }
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
+  if ((e = al((void**)&P.stream, bytes)) != cudaSuccess ||
+      (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
+      (e = al((void**)&P.zmail, 2 * sizeof(unsigned long long) * zw)) != cudaSuccess ||
+      (e = al((void**)&P.ticket, sizeof(int))) != cudaSuccess ||
+      (e = cudaMemcpy(P.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = s3_fill_not_ready(P.ymail, 2 * yw, 0)) != cudaSuccess ||
+      (e = s3_fill_not_ready(P.zmail, 2 * zw, 0)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  P.stream_bytes = (long long)bytes;
+  P.ready = true;
+  P.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s) {
+  Stencil3Plan& P = stencil3;
+  if (!P.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 3D seven-point lower structured");
+  const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
+  const int par = (int)(P.solves & 1);
+  cudaError_t e;
+  // this solve uses mailbox half `par`; reset the other half for the next one
+  if ((e = s3_fill_not_ready(P.ymail + (1 - par) * yw, yw, s)) != cudaSuccess ||
+      (e = s3_fill_not_ready(P.zmail + (1 - par) * zw, zw, s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(P.ticket, 0, sizeof(int), s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  S3Args a{};
+  a.stream = P.stream;
+  a.ymail = P.ymail + par * yw;
+  a.zmail = P.zmail + par * zw;
+  a.ticket = P.ticket;
+  a.b = d_b;
+  a.x = d_x;
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.spin_initial = opt.spin_initial;
+  a.spin_max_ns = opt.spin_max_ns;
+  a.nx = P.nx, a.ny = P.ny, a.nz = P.nz, a.nyt = P.nyt, a.nzt = P.nzt;
+  a.n_tasks = P.n_tasks;
+  a.steps = P.steps;
+  a.b_aligned = ((uintptr_t)d_b & 15) == 0;
+  a.x_aligned = ((uintptr_t)d_x & 15) == 0;
+  if (opt.probe_flags & 16) {
+    if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * kProbeWords) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, "probe buffer");
+    cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
+    a.dbg = probe_buf;
+  }
+  const int blocks = std::max(1, std::min(P.n_tasks, num_sms));
+  ++P.solves;
+  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  e = P.exact ? launch_s3<true>(a, blocks, s) : launch_s3<false>(a, blocks, s);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  launches = 1;
+  return SPTRSV_OK;
+}
+
+}  // namespace sptrsv

@@ -81,13 +81,16 @@ def lap2d(nx: int, ny: int | None = None) -> CscMatrix:
     return _stencil_lower(n, 4.0, [(1, x > 0), (nx, y > 0)])
 
 
-def lap3d(nx: int) -> CscMatrix:
-    n = nx ** 3
+def lap3d(nx: int, ny: int | None = None, nz: int | None = None) -> CscMatrix:
+    """Lower triangle of the 7-point 3D Laplacian, natural order i = (z*ny + y)*nx + x."""
+    ny = nx if ny is None else ny
+    nz = nx if nz is None else nz
+    n = nx * ny * nz
     i = np.arange(n, dtype=np.int64)
     x = i % nx
-    y = (i // nx) % nx
-    z = i // (nx * nx)
-    return _stencil_lower(n, 6.0, [(1, x > 0), (nx, y > 0), (nx * nx, z > 0)])
+    y = (i // nx) % ny
+    z = i // (nx * ny)
+    return _stencil_lower(n, 6.0, [(1, x > 0), (nx, y > 0), (nx * ny, z > 0)])
 
 
 def _dominant_diag(n: int, rows: np.ndarray, vals: np.ndarray, rng: np.random.Generator) -> np.ndarray:

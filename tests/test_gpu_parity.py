@@ -237,9 +237,48 @@ def test_stencil_not_chosen_for_other_structures():
     plan.close()
     with pytest.raises(sp.errors.SptrsvError if hasattr(sp, "errors") else Exception):
         _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="stencil")
-    l3 = synth.lap3d(8)
+    l3 = synth.lap3d(9)  # odd nx: not a whole number of 2-column blocks
     plan = _native.NativePlan(l3.col_ptr, l3.row_idx, l3.values, l3.n, executor="auto")
     assert plan.info()["executor"] != "stencil"
+    plan.close()
+    lr = synth.random_lower(500, 0.02, 3, dominant=True)
+    plan = _native.NativePlan(lr.col_ptr, lr.row_idx, lr.values, lr.n, executor="auto")
+    assert plan.info()["executor"] != "stencil"
+    plan.close()
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 8), (16, 33, 5), (64, 32, 9), (128, 70, 13), (24, 96, 40)])
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_stencil3d_executor_matches_oracle(shape, precision):
+    """3D seven-point structure: the tile wavefront (stencil3d.cu) is chosen
+    automatically; random coefficients; partial y-tiles and z-tiles."""
+    l = _random_coefficients(synth.lap3d(*shape), 13)
+    b = np.random.default_rng(14).uniform(-1, 1, l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="auto")
+    assert plan.info()["executor"] == "stencil"
+    for _ in range(3):  # repeated solves: mailbox parity halves
+        x, _ = plan.solve(b)
+        if precision == "exact":
+            assert x.tobytes() == ref.tobytes()
+        else:
+            assert sp.compare_solutions(x, ref, FAST_TOL).within_tol
+    plan.close()
+
+
+def test_stencil3d_unaligned_and_device_resident():
+    torch = pytest.importorskip("torch")
+    l = _random_coefficients(synth.lap3d(32, 40, 7), 15)
+    b = np.random.default_rng(16).uniform(-1, 1, l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor="stencil")
+    db = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+    db[1:] = torch.from_numpy(b).cuda()
+    dx = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    plan.solve_device_async(db[1:].data_ptr(), dx[1:].data_ptr(), torch.cuda.current_stream().cuda_stream)
+    plan.synchronize()
+    assert dx[1:].cpu().numpy().tobytes() == ref.tobytes()
     plan.close()
 
 
