@@ -48,8 +48,8 @@ namespace sptrsv {
 
 void DevicePlan::release() {
   cudaSetDevice(device);
-  void* ptrs[] = {rp, ci, cv, wv, dg, rdg, indeg, level, by_level, level_ptr, order, xbuf, bbuf, ticket, status,
-                  abort_flag, xseg_dev, lseg_dev, probe_buf};
+  void* ptrs[] = {rp, ci, cv, wv, dg, rdg, indeg, level, by_level, level_ptr, order, xbuf, bbuf, ctlblk,
+                  xseg_dev, lseg_dev, probe_buf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   chains.release();
@@ -70,9 +70,7 @@ int DevicePlan::run_levels() {
   // K6: level_i = 1 + max(level_j) over dependencies, 0 without any; the
   // component pool in (max,+1) arithmetic over the natural (topological) order.
   CUDA_TRY(cudaMemsetAsync(level, 0xFF, sizeof(int) * (size_t)n, stream));
-  CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(int), stream));
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(DeviceStatus), stream));
-  CUDA_TRY(cudaMemsetAsync(abort_flag, 0, sizeof(int), stream));
+  CUDA_TRY(reset_control(stream));
   RowsArgs a{};
   a.n = (int)n;
   a.rp = rp;
@@ -154,9 +152,7 @@ int DevicePlan::rows_grid(int mode) const {
 int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
   const int mode = opt.precision == SPTRSV_PRECISION_FAST ? kModeFast : kModeExact;
   CUDA_TRY(cudaMemsetAsync(d_x, 0xFF, sizeof(double) * (size_t)n, s));
-  CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(int), s));
-  CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s));
-  CUDA_TRY(cudaMemsetAsync(abort_flag, 0, sizeof(int), s));
+  CUDA_TRY(reset_control(s));
   unsigned long long* xs = reinterpret_cast<unsigned long long*>(d_x);
   CUDA_TRY(cudaMemcpyAsync(xseg_dev, &xs, sizeof(xs), cudaMemcpyHostToDevice, s));
   RowsArgs a{};

@@ -146,8 +146,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   for (auto* seg : local_segs)
     if ((e = cudaMemsetAsync(seg + (1 - par) * n, 0xFF, sizeof(unsigned long long) * n, s)) != cudaSuccess) break;
   if (e == cudaSuccess) e = cudaMemsetAsync(pe_tickets, 0, sizeof(int) * n_pe_local, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s);
+  if (e == cudaSuccess) e = reset_control(s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   RowsArgs a{};
   a.n = (int)n;

@@ -121,9 +121,11 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   // solve scratch
   P_TRY(dal(&xbuf, n));
   P_TRY(dal(&bbuf, n));
-  P_TRY(dal(&ticket, 1));
-  P_TRY(dal(&status, 1));
-  P_TRY(dal(&abort_flag, 1));
+  // per-solve control words in one block: one memset resets them all
+  P_TRY(dal(&ctlblk, kCtlBlockBytes));
+  status = reinterpret_cast<DeviceStatus*>(ctlblk);
+  ticket = reinterpret_cast<int*>(ctlblk + 32);
+  abort_flag = reinterpret_cast<int*>(ctlblk + 36);
   P_TRY(dal(&xseg_dev, 1));
   P_TRY(dal(&lseg_dev, 1));
   P_TRY(dal(&level, n));

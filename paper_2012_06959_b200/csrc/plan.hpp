@@ -42,9 +42,12 @@ struct DevicePlan {
   // solve scratch
   double* xbuf = nullptr;
   double* bbuf = nullptr;
-  int* ticket = nullptr;
+  static constexpr int kCtlBlockBytes = 64;
+  unsigned char* ctlblk = nullptr;   // [0,24) status, [32] ticket, [36] abort flag
+  int* ticket = nullptr;             // the executors' task pool (every executor uses this one)
   DeviceStatus* status = nullptr;
   int* abort_flag = nullptr;
+  cudaError_t reset_control(cudaStream_t s) { return cudaMemsetAsync(ctlblk, 0, kCtlBlockBytes, s); }
   unsigned long long** xseg_dev = nullptr;  // [1] for a single-PE plan
   int** lseg_dev = nullptr;
 

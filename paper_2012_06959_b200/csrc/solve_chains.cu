@@ -360,9 +360,7 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   if (!chains.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "chains schedule not built");
   cudaError_t e;
   if ((e = cudaMemsetAsync(chains.mbox, 0xFF, 16 * (size_t)std::max(chains.n_mbox, 1ll), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(chains.ticket, 0, sizeof(int), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+      (e = reset_control(s)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   ChainArgs a{};
   a.stream = chains.stream;
@@ -375,7 +373,7 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   a.mbox = chains.mbox;
   a.ovf_src = chains.ovf_src;
   a.ovf_val = chains.ovf_val;
-  a.ticket = chains.ticket;
+  a.ticket = ticket;
   a.b = d_b;
   a.x = d_x;
   a.status = status;

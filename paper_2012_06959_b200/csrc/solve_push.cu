@@ -195,9 +195,7 @@ int DevicePlan::solve_push(const double* d_b, double* d_x, cudaStream_t s) {
   cudaError_t e;
   if ((e = cudaMemsetAsync(push.left, 0, sizeof(double) * n, s)) != cudaSuccess ||
       (e = cudaMemsetAsync(push.count, 0, sizeof(int) * n, s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(ticket, 0, sizeof(int), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+      (e = reset_control(s)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   PushArgs a{};
   a.n = (int)n;

@@ -97,6 +97,7 @@ struct alignas(64) StArgs {
   int my_pe;
   long long mbox_half;
   int b_tma_bands;  // bands [0, b_tma_bands) gather b with one TMA per chunk (0: cp.async everywhere)
+  unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -404,6 +405,13 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   using S = StSmem<EXACT>;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
+  // this band's row of the other mailbox half (last read by the previous
+  // solve, which is complete) is reset here for the next solve: no memset
+  // node between solves
+  {
+    ulonglong2* row = reinterpret_cast<ulonglong2*>(a.mbox_next + (size_t)t * a.nx);
+    for (int w = lane; w < a.nx / 2; w += kStLanes) row[w] = make_ulonglong2(kStNotReady, kStNotReady);
+  }
   for (int c = 0; c < nchunks; ++c) {
     if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
     const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
@@ -809,7 +817,6 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
       (e = al((void**)&stencil.mbox, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
       (e = fill_not_ready(stencil.mbox, 2ll * stencil.n_tasks * nx, 0)) != cudaSuccess ||
       (e = cudaDeviceSynchronize()) != cudaSuccess ||
-      (e = al((void**)&stencil.ticket, sizeof(int))) != cudaSuccess ||
       (e = al((void**)&stencil.bflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = al((void**)&stencil.xflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = cudaMemset(stencil.bflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
@@ -835,16 +842,14 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   }
   // this solve uses mailbox half `par` (reset by the previous solve or at
   // build); reset the other half for the next one
-  if ((e = fill_not_ready(stencil.mbox + (1 - par) * half, half, s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(stencil.ticket, 0, sizeof(int), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+  if ((e = reset_control(s)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   StArgs a{};
   a.stream = stencil.stream;
   a.mbox = stencil.mbox + par * half;
+  a.mbox_next = stencil.mbox + (1 - par) * half;
   a.mbox_half = par * half;
-  a.ticket = stencil.ticket;
+  a.ticket = ticket;
   a.n_my_tasks = stencil.n_tasks;
   a.my_pe = -1;
   if (stencil.part) {

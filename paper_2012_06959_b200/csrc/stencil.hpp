@@ -56,7 +56,6 @@ struct StencilPlan {
   double build_ms = 0.0;
   unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
   unsigned long long* mbox = nullptr;  // [n_tasks][nx] bottom grid row of each task (value-is-flag)
-  int* ticket = nullptr;
   // streamed host solves (sptrsv_solve): per-band b-arrived flags written by
   // the copy stream, per-band x-stored flags written by the kernel; both
   // compared against a per-solve epoch so they never need resetting
@@ -98,12 +97,11 @@ struct StencilPlan {
   }
   void release() {
     release_part();
-    void* ptrs[] = {stream, mbox, ticket, bflag, xflag};
+    void* ptrs[] = {stream, mbox, bflag, xflag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
     mbox = nullptr;
-    ticket = nullptr;
     bflag = xflag = nullptr;
     epoch = 0;
     solves = 0;
@@ -123,9 +121,8 @@ struct Stencil3Plan {
   unsigned char* stream = nullptr;
   unsigned long long* ymail = nullptr;  // [2][tasks][4][nx]
   unsigned long long* zmail = nullptr;  // [2][tasks][32][nx]
-  int* ticket = nullptr;
   void release() {
-    void* ptrs[] = {stream, ymail, zmail, ticket};
+    void* ptrs[] = {stream, ymail, zmail};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     *this = Stencil3Plan();

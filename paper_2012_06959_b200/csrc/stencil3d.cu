@@ -75,6 +75,8 @@ struct S3Args {
   int nx, ny, nz, nyt, nzt, n_tasks, steps;
   int b_aligned, x_aligned;  // 16-byte vector paths (else 8-byte halves)
   long long* dbg;            // diagnostics (probe_flags & 16): per-task globaltimer [start, ready, end]
+  unsigned long long* ymail_next;  // the other mailbox halves: the storer resets each tile's part
+  unsigned long long* zmail_next;  // for the next solve
 };
 
 template <bool EXACT>
@@ -276,6 +278,13 @@ __device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t,
   const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
   const int Y = t % a.nyt, Z = t / a.nyt;
   const int y = Y * k3Lanes + lane;
+  {  // reset this tile's mailboxes in the other half for the next solve
+    const ulonglong2 nr = make_ulonglong2(k3NotReady, k3NotReady);
+    ulonglong2* ym = reinterpret_cast<ulonglong2*>(a.ymail_next + (size_t)t * k3R * a.nx);
+    ulonglong2* zm = reinterpret_cast<ulonglong2*>(a.zmail_next + (size_t)t * k3Lanes * a.nx);
+    for (int w = lane; w < k3R * a.nx / 2; w += k3Lanes) ym[w] = nr;
+    for (int w = lane; w < k3Lanes * a.nx / 2; w += k3Lanes) zm[w] = nr;
+  }
   for (int c = 0; c < nchunks; ++c) {
     if (!s3_wait(ctl, kC3OutReady, c + 1, deadline, 64)) return s3_abort(a, ctl, lane);
     const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk);
@@ -623,7 +632,6 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
   if ((e = al((void**)&P.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
       (e = al((void**)&P.zmail, 2 * sizeof(unsigned long long) * zw)) != cudaSuccess ||
-      (e = al((void**)&P.ticket, sizeof(int))) != cudaSuccess ||
       (e = cudaMemcpy(P.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = s3_fill_not_ready(P.ymail, 2 * yw, 0)) != cudaSuccess ||
       (e = s3_fill_not_ready(P.zmail, 2 * zw, 0)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess)
@@ -641,17 +649,15 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s) 
   const int par = (int)(P.solves & 1);
   cudaError_t e;
   // this solve uses mailbox half `par`; reset the other half for the next one
-  if ((e = s3_fill_not_ready(P.ymail + (1 - par) * yw, yw, s)) != cudaSuccess ||
-      (e = s3_fill_not_ready(P.zmail + (1 - par) * zw, zw, s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(P.ticket, 0, sizeof(int), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(status, 0, sizeof(DeviceStatus), s)) != cudaSuccess ||
-      (e = cudaMemsetAsync(abort_flag, 0, sizeof(int), s)) != cudaSuccess)
+  if ((e = reset_control(s)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   S3Args a{};
   a.stream = P.stream;
   a.ymail = P.ymail + par * yw;
   a.zmail = P.zmail + par * zw;
-  a.ticket = P.ticket;
+  a.ymail_next = P.ymail + (1 - par) * yw;
+  a.zmail_next = P.zmail + (1 - par) * zw;
+  a.ticket = ticket;
   a.b = d_b;
   a.x = d_x;
   a.status = status;
