@@ -119,7 +119,45 @@ int DevicePlan::run_levels() {
   CUDA_TRY(cudaMemcpyAsync(&total_tickets, tb + n_levels, sizeof(int), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
   long long padded = 32ll * total_tickets;
-  if (n > 0 && padded <= 2 * n) {
+  // Rows with more than kLongDeps dependencies are solved warp-wide; each gets
+  // a ticket of its own (after the level's short rows, packed 32 per ticket),
+  // so the long rows of one level run on different warps in parallel instead
+  // of one after another in the warp that drew them (power-law in-degrees:
+  // rmat-4M has 2,759 rows with > 1024 dependencies in 721 levels).
+  std::vector<int> h_order;
+  if (n > 0 && !structure_only) {
+    std::vector<int> h_by(n), h_lp(n_levels + 1), h_rp(n + 1);
+    CUDA_TRY(cudaMemcpy(h_by.data(), by_level, sizeof(int) * n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(h_lp.data(), level_ptr, sizeof(int) * (n_levels + 1), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
+    h_order.reserve(padded);
+    std::vector<int> longs;
+    for (int L = 0; L < n_levels; ++L) {
+      longs.clear();
+      size_t in_ticket = 0;
+      for (int k = h_lp[L]; k < h_lp[L + 1]; ++k) {
+        const int r = h_by[k];
+        if (h_rp[r + 1] - h_rp[r] > kLongDeps) {
+          longs.push_back(r);
+        } else {
+          h_order.push_back(r);
+          in_ticket = (in_ticket + 1) % 32;
+        }
+      }
+      if (in_ticket) h_order.resize(h_order.size() + (32 - in_ticket), -1);
+      for (int r : longs) {
+        h_order.push_back(r);
+        h_order.resize(h_order.size() + 31, -1);
+      }
+    }
+    padded = (long long)h_order.size();
+  }
+  if (n > 0 && !structure_only && padded <= 8 * n) {
+    CUDA_TRY(dalloc(&order, padded));
+    CUDA_TRY(cudaMemcpy(order, h_order.data(), sizeof(int) * padded, cudaMemcpyHostToDevice));
+    order_len = padded;
+    coop_long = 1;
+  } else if (n > 0 && padded <= 2 * n) {
     CUDA_TRY(dalloc(&order, padded));
     CUDA_TRY(cudaMemsetAsync(order, 0xFF, sizeof(int) * padded, stream));
     CUDA_TRY(launch_pad_order(by_level, level, level_ptr, tb, (int)n, order, stream));
@@ -174,7 +212,7 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = coop_long;
-  a.long_deps = 32;
+  a.long_deps = kLongDeps;
   CUDA_TRY(cudaEventRecord(evk0, s));
   CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
   CUDA_TRY(cudaEventRecord(evk1, s));

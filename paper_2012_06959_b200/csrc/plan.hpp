@@ -38,6 +38,7 @@ struct DevicePlan {
   int* order = nullptr;
   long long order_len = 0;
   int coop_long = 0;
+  static constexpr int kLongDeps = 32;  // rows with more dependencies are solved warp-wide
 
   // solve scratch
   double* xbuf = nullptr;

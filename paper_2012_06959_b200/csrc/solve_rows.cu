@@ -201,7 +201,39 @@ __device__ bool solve_row_warp(const RowsArgs& a, Poller& poll, int i, int lane)
   const int beg = a.rp[i], end = a.rp[i + 1];
   double s = (MODE == kModeFast) ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
   double part = 0.0;  // fast mode: per-lane partial
-  for (int base = beg; base < end; base += kWarp) {
+  int base = beg;
+  if (MODE == kModeFast) {
+    // Very long rows (power-law in-degrees: 29,079 in rmat-4M): kLongUnroll
+    // dependencies per lane per round, all loads in flight before any wait,
+    // so a round costs one memory round trip for 32 * kLongUnroll entries.
+    constexpr int kLongUnroll = 8;
+    for (; base + kWarp * kLongUnroll <= end; base += kWarp * kLongUnroll) {
+      int j[kLongUnroll];
+      double v[kLongUnroll];
+      unsigned long long u[kLongUnroll];
+      const unsigned long long* p[kLongUnroll];
+      bool rem[kLongUnroll];
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q) {
+        j[q] = __ldg(a.ci + base + q * kWarp + lane);
+        v[q] = __ldg(a.val + base + q * kWarp + lane);
+      }
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q) {
+        p[q] = slot_u64<MODE>(a, j[q], rem[q]);
+        u[q] = rem[q] ? ld_relaxed_sys_u64(p[q]) : ld_relaxed_u64(p[q]);
+        if (rem[q]) ++poll.remote;
+      }
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q) {
+        ok = ok && poll.wait_u64(p[q], rem[q], u[q]);
+        part = __fma_rn(v[q], as_f64(u[q]), part);
+      }
+      if (__any_sync(0xffffffffu, !ok)) return false;
+    }
+  }
+  for (; base < end; base += kWarp) {
     int k = base + lane;
     double prod = 0.0;
     bool ok = true;

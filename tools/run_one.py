@@ -25,13 +25,16 @@ def main():
     ap.add_argument("--executor", default="auto")
     ap.add_argument("--precision", default="fast")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--spin-initial", type=int, default=1024)
+    ap.add_argument("--spin-max-ns", type=int, default=64)
     args = ap.parse_args()
     if args.lap2d:
         l = synth.lap2d(*args.lap2d)
     else:
         l = synth.config_matrix(args.config or "lap2d-4096")
     t0 = time.perf_counter()
-    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=args.precision, executor=args.executor)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=args.precision, executor=args.executor,
+                              spin_initial=args.spin_initial, spin_max_ns=args.spin_max_ns)
     print("setup_s", round(time.perf_counter() - t0, 2), plan.info(), flush=True)
     b = np.ones(l.n)
     for _ in range(args.reps):
