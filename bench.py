@@ -158,7 +158,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="lap2d-4096")
     ap.add_argument("--precision", choices=["fast", "exact"], default="fast")
-    ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil", "push"], default="auto")
+    ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil", "push", "band"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -53,8 +53,10 @@ enum {
   SPTRSV_EXECUTOR_ROWS = 1,
   SPTRSV_EXECUTOR_CHAINS = 2,
   SPTRSV_EXECUTOR_STENCIL = 3,
-  SPTRSV_EXECUTOR_PUSH = 4 /* paper Alg. 2 / solve_shared_atomics (engine.py:324-431): warp per column, fp64
-                              atomics on shared left sums + in-degree counters; rounding-level nondeterministic */
+  SPTRSV_EXECUTOR_PUSH = 4, /* paper Alg. 2 / solve_shared_atomics (engine.py:324-431): warp per column, fp64
+                               atomics on shared left sums + in-degree counters; rounding-level nondeterministic */
+  SPTRSV_EXECUTOR_BAND = 5  /* one warp, sliding 64-row window of accumulators, column (push) order: for narrow
+                               bands with little parallelism (banded-8M); exact mode bit-identical */
 };
 
 /* plan flags */

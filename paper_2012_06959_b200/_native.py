@@ -21,7 +21,7 @@ from .errors import NativeUnavailable, raise_for_status
 LIB_PATH = Path(__file__).resolve().parent / "libsptrsv_b200.so"
 
 PRECISION = {"exact": 0, "fast": 1}
-EXECUTOR = {"auto": 0, "rows": 1, "chains": 2, "stencil": 3, "push": 4}
+EXECUTOR = {"auto": 0, "rows": 1, "chains": 2, "stencil": 3, "push": 4, "band": 5}
 EXECUTOR_NAME = {v: k for k, v in EXECUTOR.items()}
 PLAN_STRUCTURE_ONLY = 1
 PLAN_NO_STREAMED_IO = 4

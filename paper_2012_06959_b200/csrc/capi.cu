@@ -56,6 +56,7 @@ void DevicePlan::release() {
   stencil.release();
   stencil3.release();
   push.release();
+  band.release();
   release_partition();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -229,6 +230,7 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   else if (executor_used == SPTRSV_EXECUTOR_STENCIL)
     rc = stencil3.ready ? solve_stencil3d(d_b, d_x, s) : solve_stencil(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_PUSH) rc = solve_push(d_b, d_x, s);
+  else if (executor_used == SPTRSV_EXECUTOR_BAND) rc = solve_band(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
   else rc = solve_rows(d_b, d_x, s);
   if (rc != SPTRSV_OK) return rc;

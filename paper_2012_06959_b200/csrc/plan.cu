@@ -169,6 +169,18 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
                          "stencil executor requested but L is neither 2D five-point nor 3D seven-point lower "
                          "structured");
     }
+    if (opt.executor == SPTRSV_EXECUTOR_BAND || (opt.executor == SPTRSV_EXECUTOR_AUTO && band_candidate(h_rp, h_ci))) {
+      if (opt.executor == SPTRSV_EXECUTOR_BAND && !band_candidate(h_rp, h_ci)) {
+        bool narrow = n >= 128;
+        for (long long i = 0; i < n && narrow; ++i)
+          if (h_rp[i] < h_rp[i + 1] && i - h_ci[h_rp[i]] > 64) narrow = false;
+        if (!narrow) return plan_fail(SPTRSV_E_UNSUPPORTED, "band executor needs every dependency within 64 rows");
+      }
+      rc = build_band();
+      if (rc != SPTRSV_OK) return rc;
+      executor_used = SPTRSV_EXECUTOR_BAND;
+      return SPTRSV_OK;
+    }
     rc = build_chains(h_rp, h_ci);
     if (rc != SPTRSV_OK) return rc;
     if (chains.ready && (opt.executor == SPTRSV_EXECUTOR_CHAINS || chains_preferred()))

@@ -74,6 +74,21 @@ struct DevicePlan {
     }
   } push;
   int build_push();
+  // band executor (solve_band.cu): dense 64-wide band columns + presence masks
+  struct BandPlan {
+    bool ready = false;
+    double* coef = nullptr;
+    unsigned long long* mask = nullptr;
+    int nchunks = 0;
+    void release() {
+      if (coef) cudaFree(coef);
+      if (mask) cudaFree(mask);
+      *this = BandPlan();
+    }
+  } band;
+  bool band_candidate(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const;
+  int build_band();
+  int solve_band(const double* d_b, double* d_x, cudaStream_t s);
   int solve_push(const double* d_b, double* d_x, cudaStream_t s);
 
   // PE partition (partition.cu): each PE owns components (PartitionPlan.owner_arr)
