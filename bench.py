@@ -183,12 +183,18 @@ def main():
 
     from paper_2012_06959_b200 import _native
 
-    dev = local
+    # SPTRSV_BENCH_SAME_DEVICE=1 + SPTRSV_BENCH_BACKEND=gloo: every rank on
+    # cuda:0 (exercises the N > 1 path on a one-GPU box; NCCL refuses that)
+    dev = 0 if os.environ.get("SPTRSV_BENCH_SAME_DEVICE") == "1" else local
     torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        backend = os.environ.get("SPTRSV_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.Stream(dev)  # solves, events and the inter-solve all-reduce share it
     sh = stream.cuda_stream
 
@@ -272,16 +278,23 @@ def main():
         d2h = 8 * n
     else:
         rows = solver.rows
+        # a rank reads b and writes x of its own rows only: with a contiguous
+        # (block) slab each GPU moves 1/N of b and x over its own PCIe link
+        if rows.size and rows[-1] - rows[0] + 1 == rows.size:
+            sl = slice(int(rows[0]), int(rows[-1]) + 1)
+        else:
+            sl = slice(0, n)
         for _ in range(args.e2e_steps + 1):
             torch.distributed.barrier()
             t1 = time.perf_counter()
-            db.copy_(hb, non_blocking=True)
+            db[sl].copy_(hb[sl], non_blocking=True)
             one_solve()
             plan.synchronize()
-            hx.copy_(dx, non_blocking=False)
+            hx[sl].copy_(dx[sl], non_blocking=False)
             t_e2e.append(time.perf_counter() - t1)
         t_e2e = t_e2e[1:]
-        d2h = 8 * int(rows.size)
+        h2d_rank = 8 * (sl.stop - sl.start)
+        d2h = 8 * (sl.stop - sl.start)
     e2e_s = statistics.mean(t_e2e)
     if ws > 1:
         t = torch.tensor([e2e_s], device=f"cuda:{dev}")
@@ -358,14 +371,14 @@ def main():
         "e2e": {
             "value": flops / e2e_s / 1e9,
             "unit": UNIT,
-            "h2d_bytes_per_step": 8 * n,
-            "d2h_bytes_per_step": d2h,
+            "h2d_bytes_per_step": 8 * n if ws == 1 else h2d_rank * ws,
+            "d2h_bytes_per_step": d2h if ws == 1 else d2h * ws,
             "ms_per_step": e2e_s * 1e3,
             "path": ("sptrsv_solve (C ABI, pinned host b/x" +
                      {1: ", band-granular H2D/D2H overlapping the kernel)",
                       2: ", zero-copy: the kernel reads b and writes x over PCIe in 128-byte lines)"}.get(
                          e2e_streamed, ")"))
-            if ws == 1 else "per-rank H2D b, solve, D2H owned x",
+            if ws == 1 else "per rank: H2D of its rows of b, solve, D2H of its rows of x (pinned)",
         },
         "cpu_baseline": None if cpu is None else {
             "value": flops / cpu["seconds"] / 1e9,
