@@ -94,9 +94,8 @@ struct ChainPlan {
   unsigned long long* mbox = nullptr;  // [n_mbox] cross-task mailboxes (value-is-flag, 16-byte slots)
   int* ovf_src = nullptr;              // overflow dependency lists (rows wider than kInlineDeps)
   double* ovf_val = nullptr;
-  int* ticket = nullptr;
   void release() {
-    void* ptrs[] = {stream, chunk_off, chunk_steps, chunk_width, task_chunk, mbox, ovf_src, ovf_val, ticket};
+    void* ptrs[] = {stream, chunk_off, chunk_steps, chunk_width, task_chunk, mbox, ovf_src, ovf_val};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
@@ -107,7 +106,6 @@ struct ChainPlan {
     mbox = nullptr;
     ovf_src = nullptr;
     ovf_val = nullptr;
-    ticket = nullptr;
     ready = false;
   }
   double in_task_fraction() const { return deps_total ? double(deps_in_task) / double(deps_total) : 1.0; }

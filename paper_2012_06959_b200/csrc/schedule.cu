@@ -343,8 +343,7 @@ int DevicePlan::build_chains(const std::vector<int>& h_rp, const std::vector<int
       (e = al((void**)&chains.task_chunk, sizeof(int) * out.task_chunk.size())) != cudaSuccess ||
       (e = al((void**)&chains.mbox, 16 * (size_t)out.n_mbox)) != cudaSuccess ||  // 16-byte slots
       (e = al((void**)&chains.ovf_src, sizeof(int) * out.ovf_src.size())) != cudaSuccess ||
-      (e = al((void**)&chains.ovf_val, sizeof(double) * out.ovf_val.size())) != cudaSuccess ||
-      (e = al((void**)&chains.ticket, sizeof(int))) != cudaSuccess)
+      (e = al((void**)&chains.ovf_val, sizeof(double) * out.ovf_val.size())) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   cudaMemcpy(chains.stream, out.stream.data(), out.stream.size(), cudaMemcpyHostToDevice);
   cudaMemcpy(chains.chunk_off, out.chunk_off.data(), sizeof(long long) * out.chunk_off.size(), cudaMemcpyHostToDevice);

@@ -21,6 +21,10 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#ifndef SPTRSV_LONG_UNROLL
+#define SPTRSV_LONG_UNROLL 8
+#endif
+
 namespace sptrsv {
 
 namespace {
@@ -206,7 +210,7 @@ __device__ bool solve_row_warp(const RowsArgs& a, Poller& poll, int i, int lane)
     // Very long rows (power-law in-degrees: 29,079 in rmat-4M): kLongUnroll
     // dependencies per lane per round, all loads in flight before any wait,
     // so a round costs one memory round trip for 32 * kLongUnroll entries.
-    constexpr int kLongUnroll = 8;
+    constexpr int kLongUnroll = SPTRSV_LONG_UNROLL;
     for (; base + kWarp * kLongUnroll <= end; base += kWarp * kLongUnroll) {
       int j[kLongUnroll];
       double v[kLongUnroll];
