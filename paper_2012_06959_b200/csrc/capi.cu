@@ -57,6 +57,7 @@ void DevicePlan::release() {
   stencil3.release();
   push.release();
   band.release();
+  split_rows.release();
   release_partition();
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
@@ -132,6 +133,13 @@ int DevicePlan::run_levels() {
     CUDA_TRY(cudaMemcpy(h_lp.data(), level_ptr, sizeof(int) * (n_levels + 1), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
     h_order.reserve(padded);
+    // fast mode splits rows with > kSplitDeps dependencies into partial tasks
+    // of kSplitDeps entries, one warp each, placed before the level's long
+    // rows: the level then costs ~one memory round trip per warp however
+    // heavy its heaviest row (rmat-4M: 29,079 dependencies)
+    const bool split = opt.precision == SPTRSV_PRECISION_FAST;
+    std::vector<int> hv_idx, hv_parts, pt_beg, pt_end, pt_heavy;
+    if (split) hv_idx.assign(n, -1);
     std::vector<int> longs;
     for (int L = 0; L < n_levels; ++L) {
       longs.clear();
@@ -147,11 +155,44 @@ int DevicePlan::run_levels() {
       }
       if (in_ticket) h_order.resize(h_order.size() + (32 - in_ticket), -1);
       for (int r : longs) {
+        const int deg = h_rp[r + 1] - h_rp[r];
+        if (!split || deg <= kSplitDeps) continue;
+        const int h = (int)hv_parts.size();
+        hv_idx[r] = h;
+        hv_parts.push_back((deg + kSplitDeps - 1) / kSplitDeps);
+        for (int b0 = h_rp[r]; b0 < h_rp[r + 1]; b0 += kSplitDeps) {
+          h_order.push_back((int)n + (int)pt_beg.size());
+          h_order.resize(h_order.size() + 31, -1);
+          pt_beg.push_back(b0);
+          pt_end.push_back(std::min(b0 + kSplitDeps, h_rp[r + 1]));
+          pt_heavy.push_back(h);
+        }
+      }
+      for (int r : longs) {
         h_order.push_back(r);
         h_order.resize(h_order.size() + 31, -1);
       }
     }
     padded = (long long)h_order.size();
+    if (!hv_parts.empty() && (long long)n + (long long)pt_beg.size() < (1ll << 31)) {
+      auto up = [&](int** d, const std::vector<int>& h) -> cudaError_t {
+        cudaError_t e = dalloc(d, h.size());
+        return e != cudaSuccess ? e : cudaMemcpy(*d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice);
+      };
+      CUDA_TRY(up(&split_rows.heavy_idx, hv_idx));
+      CUDA_TRY(up(&split_rows.heavy_parts, hv_parts));
+      CUDA_TRY(up(&split_rows.part_beg, pt_beg));
+      CUDA_TRY(up(&split_rows.part_end, pt_end));
+      CUDA_TRY(up(&split_rows.part_heavy, pt_heavy));
+      CUDA_TRY(dalloc(&split_rows.part_sum, hv_parts.size()));
+      CUDA_TRY(dalloc(&split_rows.part_done, hv_parts.size()));
+      split_rows.n_heavy = (int)hv_parts.size();
+    } else if (!hv_parts.empty()) {
+      // (cannot encode the partial tasks in int32: keep whole rows)
+      h_order.erase(std::remove_if(h_order.begin(), h_order.end(), [&](int v) { return v >= (int)n; }),
+                    h_order.end());
+      padded = (long long)h_order.size();
+    }
   }
   if (n > 0 && !structure_only && padded <= 8 * n) {
     CUDA_TRY(dalloc(&order, padded));
@@ -214,6 +255,17 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = coop_long;
   a.long_deps = kLongDeps;
+  if (mode == kModeFast && split_rows.n_heavy) {
+    CUDA_TRY(cudaMemsetAsync(split_rows.part_sum, 0, sizeof(double) * split_rows.n_heavy, s));
+    CUDA_TRY(cudaMemsetAsync(split_rows.part_done, 0, sizeof(int) * split_rows.n_heavy, s));
+    a.heavy_idx = split_rows.heavy_idx;
+    a.heavy_parts = split_rows.heavy_parts;
+    a.part_beg = split_rows.part_beg;
+    a.part_end = split_rows.part_end;
+    a.part_heavy = split_rows.part_heavy;
+    a.part_sum = split_rows.part_sum;
+    a.part_done = split_rows.part_done;
+  }
   CUDA_TRY(cudaEventRecord(evk0, s));
   CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
   CUDA_TRY(cudaEventRecord(evk1, s));

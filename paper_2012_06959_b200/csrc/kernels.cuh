@@ -60,6 +60,17 @@ struct RowsArgs {
   int spin_max_ns;          // largest __nanosleep (Backoff.max_pause)
   int coop_long;            // 1: tickets are single-level, rows with > long_deps deps go warp-wide
   int long_deps;
+  // split rows (fast mode, one PE): an order entry n + p is partial task p —
+  // a slice [part_beg[p], part_end[p]) of heavy row part_heavy[p]'s entries,
+  // summed by one warp and added into part_sum[h] (then part_done[h] += 1);
+  // the heavy row's own ticket waits for part_done[h] == heavy_parts[h]
+  const int* part_beg;
+  const int* part_end;
+  const int* part_heavy;
+  const int* heavy_idx;     // [n]: heavy index of a split row, -1 otherwise (nullptr: no split rows)
+  const int* heavy_parts;
+  double* part_sum;
+  int* part_done;
 };
 
 cudaError_t launch_rows(int mode, const RowsArgs& a, int blocks, cudaStream_t s);

@@ -38,7 +38,20 @@ struct DevicePlan {
   int* order = nullptr;
   long long order_len = 0;
   int coop_long = 0;
-  static constexpr int kLongDeps = 32;  // rows with more dependencies are solved warp-wide
+  static constexpr int kLongDeps = 32;    // rows with more dependencies are solved warp-wide
+  static constexpr int kSplitDeps = 256;  // fast mode: rows with more are split into partial tasks
+  struct SplitRows {
+    int n_heavy = 0;
+    int *heavy_idx = nullptr, *heavy_parts = nullptr, *part_beg = nullptr, *part_end = nullptr,
+        *part_heavy = nullptr, *part_done = nullptr;
+    double* part_sum = nullptr;
+    void release() {
+      void* ptrs[] = {heavy_idx, heavy_parts, part_beg, part_end, part_heavy, part_done, part_sum};
+      for (void* p : ptrs)
+        if (p) cudaFree(p);
+      *this = SplitRows();
+    }
+  } split_rows;
 
   // solve scratch
   double* xbuf = nullptr;

@@ -200,11 +200,103 @@ __device__ bool level_row_thread(const RowsArgs& a, Poller& poll, int i) {
 
 // Whole warp, one long row. Exact mode keeps the ascending-column fold by
 // letting lane 0 add the 32 products of each chunk in order.
+// Warp-wide dot product of entries [beg, end) with x (fast mode), all loads
+// of a round in flight before any wait. Returns false when aborting.
+__device__ bool warp_dot_fast(const RowsArgs& a, Poller& poll, int beg, int end, int lane, double& part) {
+  constexpr int kU = SPTRSV_LONG_UNROLL;
+  for (int base = beg; base < end; base += kWarp * kU) {
+    int j[kU];
+    double v[kU];
+    unsigned long long u[kU];
+    const unsigned long long* p[kU];
+    bool rem[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int k = base + q * kWarp + lane;
+      j[q] = k < end ? __ldg(a.ci + k) : -1;
+      v[q] = k < end ? __ldg(a.val + k) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      if (j[q] >= 0) {
+        p[q] = slot_u64<kModeFast>(a, j[q], rem[q]);
+        u[q] = rem[q] ? ld_relaxed_sys_u64(p[q]) : ld_relaxed_u64(p[q]);
+        if (rem[q]) ++poll.remote;
+      }
+    }
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < kU; ++q)
+      if (j[q] >= 0) {
+        ok = ok && poll.wait_u64(p[q], rem[q], u[q]);
+        part = __fma_rn(v[q], as_f64(u[q]), part);
+      }
+    if (__any_sync(0xffffffffu, !ok)) return false;
+  }
+  return true;
+}
+
+// Partial task p of a split row: its slice of the row's dot product, added to
+// the row's shared partial sum; then the row's done-count is bumped.
+__device__ bool solve_part_warp(const RowsArgs& a, Poller& poll, int p, int lane) {
+  double part = 0.0;
+  if (!warp_dot_fast(a, poll, a.part_beg[p], a.part_end[p], lane, part)) return false;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+  if (lane == 0) {
+    const int h = a.part_heavy[p];
+    atomicAdd(a.part_sum + h, part);
+    __threadfence();  // the sum before the count
+    atomicAdd(a.part_done + h, 1);
+  }
+  return true;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu_s32_rows(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int MODE>
 __device__ bool solve_row_warp(const RowsArgs& a, Poller& poll, int i, int lane) {
   const int beg = a.rp[i], end = a.rp[i + 1];
   double s = (MODE == kModeFast) ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
   double part = 0.0;  // fast mode: per-lane partial
+  if (MODE == kModeFast && a.heavy_idx) {
+    const int h = a.heavy_idx[i];
+    if (h >= 0) {
+      // a split row: its partial tasks (earlier tickets of the same level)
+      // hold the whole dot product
+      int ok = 1;
+      double sum = 0.0;
+      if (lane == 0) {
+        const int need = a.heavy_parts[h];
+        int polls = 0, sleep_ns = 32;
+        while (ld_acquire_gpu_s32_rows(a.part_done + h) < need) {
+          ++poll.spins;
+          if (++polls > a.spin_initial) {
+            if ((polls & 63) == 0) {
+              if (ld_relaxed_s32(a.abort_flag)) { ok = 0; break; }
+              if (poll.deadline && globaltimer_ns() > poll.deadline) {
+                atomicExch(&a.status->code, 5);
+                atomicExch(a.abort_flag, 1);
+                ok = 0;
+                break;
+              }
+            }
+            __nanosleep(sleep_ns);
+            if (sleep_ns < a.spin_max_ns) sleep_ns <<= 1;
+          }
+        }
+        if (ok) {
+          sum = __ldcg(a.part_sum + h);
+          publish_u64(a, i, s + sum);
+        }
+      }
+      return __shfl_sync(0xffffffffu, ok, 0) != 0;
+    }
+  }
   int base = beg;
   if (MODE == kModeFast) {
     // Very long rows (power-law in-degrees: 29,079 in rmat-4M): kLongUnroll
@@ -314,7 +406,8 @@ __global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
     int i = -1;
     if (slot < a.order_len) i = a.order ? a.order[slot] : (int)slot;
     bool is_long = false;
-    if (i >= 0 && a.coop_long) is_long = (a.rp[i + 1] - a.rp[i]) > a.long_deps;
+    if (i >= a.n) is_long = true;  // a partial task of a split row (fast mode)
+    else if (i >= 0 && a.coop_long) is_long = (a.rp[i + 1] - a.rp[i]) > a.long_deps;
     bool ok = true;
     if (i >= 0 && !is_long) {
       if constexpr (MODE == kModeLevel) ok = level_row_thread(a, poll, i);
@@ -327,6 +420,7 @@ __global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
       int r = __shfl_sync(0xffffffffu, i, src);
       bool wok;
       if constexpr (MODE == kModeLevel) wok = level_row_warp(a, poll, r, lane);
+      else if (MODE == kModeFast && r >= a.n) wok = solve_part_warp(a, poll, r - a.n, lane);
       else wok = solve_row_warp<MODE>(a, poll, r, lane);
       ok = ok && wok;
     }

@@ -358,3 +358,30 @@ def test_band_executor_special_values_and_errors():
     wide = synth.random_lower(500, 0.05, 8, dominant=True)  # dependencies farther than 64 rows
     with pytest.raises(sp.errors.SptrsvError if hasattr(sp, "errors") else Exception):
         _native.NativePlan(wide.col_ptr, wide.row_idx, wide.values, wide.n, executor="band")
+
+
+def test_split_heavy_rows_fast_mode():
+    """Fast mode splits rows with > 256 dependencies into partial tasks (one
+    warp per 256 entries, summed with atomics); exact mode keeps them whole.
+    Power-law rows of every size around the split threshold."""
+    rng = np.random.default_rng(31)
+    n = 6000
+    entries = {}
+    for i in range(n):
+        entries[(i, i)] = 4.0 + rng.random()
+    for i in range(1, n):
+        k = int(min(i, rng.choice([1, 3, 30, 255, 256, 257, 600, 2500, 5000], p=[.3, .3, .2, .04, .04, .04, .04, .02, .02])))
+        for j in rng.choice(i, size=k, replace=False):
+            entries[(i, int(j))] = rng.uniform(-1, 1) / k
+    l = sp.CscMatrix.from_entries(n, entries)
+    b = rng.uniform(-1, 1, n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    for precision in ("fast", "exact"):
+        plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="rows")
+        for _ in range(2):
+            x, _ = plan.solve(b)
+            if precision == "exact":
+                assert x.tobytes() == ref.tobytes()
+            else:
+                assert sp.compare_solutions(x, ref, FAST_TOL).within_tol
+        plan.close()
