@@ -385,3 +385,45 @@ def test_split_heavy_rows_fast_mode():
             else:
                 assert sp.compare_solutions(x, ref, FAST_TOL).within_tol
         plan.close()
+
+
+def _serial_backward(u, b):
+    """Backward substitution with the serial oracle's rounding: x_i = (b_i - sum_{j>i} u_ij x_j) / u_ii,
+    terms added in descending column order (the reversed lower solve's ascending order)."""
+    n = u.n
+    x = np.zeros(n)
+    left = np.zeros(n)
+    for j in range(n - 1, -1, -1):
+        rows = u.row_idx[u.col_ptr[j]:u.col_ptr[j + 1]]
+        vals = u.values[u.col_ptr[j]:u.col_ptr[j + 1]]
+        x[j] = (b[j] - left[j]) / vals[-1]  # diagonal is the last entry of an upper column
+        for r, v in zip(rows[:-1], vals[:-1]):
+            left[r] += v * x[j]
+    return x
+
+
+@pytest.mark.parametrize("shape", ["lap2d", "random", "banded"])
+def test_upper_triangular_solve(shape):
+    """Row f4: U x = b through the index reversal, exact mode equal to serial backward substitution."""
+    low = {"lap2d": lambda: synth.lap2d(40, 30), "random": lambda: synth.random_lower(700, 0.02, 4, dominant=True),
+           "banded": lambda: synth.banded(900, 16, 0.5, 2)}[shape]()
+    import scipy.sparse as ssp
+
+    dense_l = ssp.csc_matrix((low.values, low.row_idx, low.col_ptr), shape=(low.n, low.n))
+    ut = dense_l.T.tocsc()
+    ut.sort_indices()
+    u = sp.CscMatrix(n=low.n, col_ptr=ut.indptr.astype(np.int64), row_idx=ut.indices.astype(np.int64),
+                     values=ut.data.copy())
+    b = np.random.default_rng(5).uniform(-1, 1, u.n)
+    x = sp.solve_upper(u, b, precision="exact")
+    assert x.tobytes() == _serial_backward(u, b).tobytes()
+    xf = sp.solve_upper(u, b, precision="fast")
+    assert sp.compare_solutions(xf, x, FAST_TOL).within_tol
+
+
+def test_solve_many_columns():
+    l = synth.lap3d(12)
+    bs = np.random.default_rng(6).uniform(-1, 1, (l.n, 5))
+    xs = sp.solve_many(l, bs, precision="exact")
+    for k in range(5):
+        assert xs[:, k].tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, bs[:, k].copy()).tobytes()

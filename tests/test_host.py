@@ -154,3 +154,26 @@ def test_no_gpu_means_loud_failure():
         pytest.skip("a GPU is visible")
     with pytest.raises(errors.NativeUnavailable):
         sp.solve_serial(synth.diagonal(3), np.ones(3))
+
+
+def test_reverse_upper_is_a_relabelling():
+    """P U P is lower triangular, diagonal first per column, same values."""
+    import scipy.sparse as ssp
+
+    rng = np.random.default_rng(3)
+    n = 300
+    dense = np.triu(rng.uniform(-1, 1, (n, n)) * (rng.random((n, n)) < 0.05))
+    dense[np.arange(n), np.arange(n)] = rng.uniform(1, 2, n)
+    csc = ssp.csc_matrix(dense)
+    csc.sort_indices()
+    u = sp.CscMatrix(n=n, col_ptr=csc.indptr.astype(np.int64), row_idx=csc.indices.astype(np.int64),
+                     values=csc.data.copy())
+    lr = sp.reverse_upper(u)
+    rebuilt = np.zeros((n, n))
+    cols = np.repeat(np.arange(n), np.diff(lr.col_ptr))
+    rebuilt[lr.row_idx, cols] = lr.values
+    np.testing.assert_array_equal(rebuilt, dense[::-1, ::-1])
+    assert np.all(lr.row_idx[lr.col_ptr[:-1]] == np.arange(n))  # diagonal first
+    with pytest.raises(sp.errors.MatrixStructureError if hasattr(sp, "errors") else Exception):
+        sp.reverse_upper(sp.CscMatrix(n=2, col_ptr=np.array([0, 2, 3]), row_idx=np.array([0, 1, 1]),
+                                      values=np.ones(3)))
