@@ -142,7 +142,8 @@ def reference_arm(args, l, b, n, nnz):
         "steps": r["reps"], "warmup": args.warmup, "ms_per_step": r["seconds"] * 1e3,
         "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "n": n, "nnz": nnz, "rhs": "ones"},
+        "config": {"workload": args.config, "n": n, "nnz": nnz, "rhs": "ones", "precision": "exact (serial)",
+                   "executor": "solve_serial (C port of reference.py:20-35)", "parallelism": "1 CPU core"},
         "cpu_baseline": {"value": gflops, "unit": UNIT, "cores": 1, "kind": "port",
                          "sample": f"full {args.config} solve_serial (C port of reference.py:20-35, "
                                    f"-ffp-contract=off), {r['reps']} reps"},
