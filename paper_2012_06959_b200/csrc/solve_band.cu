@@ -146,10 +146,13 @@ __device__ void band_compute(const BandArgs& a, unsigned char* smem, int* ctl, i
     const double* coef = reinterpret_cast<const double*>(smem + BSmem::kCoef + slot * BSmem::kCoefChunk);
     const unsigned long long* msk = reinterpret_cast<const unsigned long long*>(smem + BSmem::kMask) + slot * kBK;
     const double* rowd = reinterpret_cast<const double*>(smem + BSmem::kRow + slot * BSmem::kRowChunk);
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < kBK; ++k) {
       const long long j = (long long)c * kBK + k;
-      const int p = (int)(j & (kBW - 1)), owner = p >> 1, os = p & 1;
+      // chunks are window-aligned (kBK == kBW), so row j's window position is
+      // k itself: owner lane and slot are compile-time after unrolling
+      static_assert(kBK == kBW, "window position = column index within the chunk");
+      const int p = k, owner = p >> 1, os = p & 1;
       const double mine = os ? acc[1] : acc[0];
       double xj;
       if (EXACT) {
