@@ -168,7 +168,14 @@ int sptrsv_plan_destroy(sptrsv_plan* plan);
  *               segments are attached with sptrsv_plan_import_segment (CUDA
  *               IPC) or sptrsv_plan_set_peer_segment (same-process peer
  *               pointer). The caller must order consecutive solves across
- *               processes (a barrier) because each solve resets the segments. */
+ *               processes (a barrier): each solve resets the half of the
+ *               parity double buffer the next solve uses, and every PE must
+ *               run the same sequence of solves.
+ * With the 2D stencil executor and a band-aligned owner map (whole 64-row
+ * bands per PE, e.g. block_partition of lap2d-4096 over 1/2/4/8 GPUs) the
+ * shared state is the stencil's mailbox array (the bottom grid row of every
+ * band) instead of x segments; export/import/segment then refer to it. Other
+ * owner maps fall back to the component pool. */
 int sptrsv_plan_set_partition(sptrsv_plan* plan, const int32_t* owner, int32_t n_pes, int32_t my_pe);
 int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* ipc_handle_out);
 int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* ipc_handle);
