@@ -66,6 +66,7 @@ constexpr unsigned long long kStNotReady = 0xFFF40000FFF40000ull;
 
 struct alignas(64) StArgs {
   CUtensorMap bmap;  // kStBTma and b 16-byte aligned and a full last band: b via TMA
+  CUtensorMap xmap;  // the same skewed view of x: interior chunks leave by one TMA store
   const unsigned char* stream;
   unsigned long long* mbox;
   int* ticket;
@@ -97,6 +98,7 @@ struct alignas(64) StArgs {
   int my_pe;
   long long mbox_half;
   int b_tma_bands;  // bands [0, b_tma_bands) gather b with one TMA per chunk (0: cp.async everywhere)
+  int x_tma_bands;  // bands [0, x_tma_bands) store interior chunks of x with one TMA store
   unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
@@ -160,7 +162,9 @@ struct StSmem {
   static constexpr int kCoef = 0;                                       // [kSlots][kStG][kStep]
   static constexpr int kB = kCoef + kSlots * kCoefChunk;                // [kSlots][r][k][pair][lane] f64x2
   static constexpr int kInbox = kB + kSlots * kBChunk;                  // [kSlots][kStG][kStC] f64
-  static constexpr int kOut = kInbox + kSlots * kStG * kStC * 8;        // [kStOutSlots][kStG][pair][lane] f64x2
+  // out ring: the b slot layout ([r][l][piece], 128-byte swizzled), so a
+  // whole chunk leaves with one TMA tensor store through the skewed view of x
+  static constexpr int kOut = (kInbox + kSlots * kStG * kStC * 8 + 1023) / 1024 * 1024;
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kCtl = kBars + 8 * kSlots;
@@ -412,28 +416,39 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     ulonglong2* row = reinterpret_cast<ulonglong2*>(a.mbox_next + (size_t)t * a.nx);
     for (int w = lane; w < a.nx / 2; w += kStLanes) row[w] = make_ulonglong2(kStNotReady, kStNotReady);
   }
+  const bool x_tma = kStBTma && t < a.x_tma_bands;
   for (int c = 0; c < nchunks; ++c) {
     if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
-    const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
+    unsigned char* slot = smem + S::kOut + (c % kStOutSlots) * S::kOutChunk;
+    const double2* src = reinterpret_cast<const double2*>(slot);
+    // interior chunk (every lane's blocks inside the row): one TMA store of
+    // the whole slot; edge chunks element by element (the skewed box would
+    // write padding into neighbouring rows there)
+    if (x_tma && c * kStG >= kStLanes - 1 && (c + 1) * kStG <= nblk) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compute warp's STS -> async proxy
+        tma_store_4d(&a.xmap, c * kStG * kStC, 0, 0, t, slot);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slot reusable once read
+      }
+    } else {
 #pragma unroll
-    for (int k = 0; k < kStG; ++k) {
-      const int j = c * kStG + k - lane;
-      if (j >= 0 && j < nblk) {
-        const double2* blk = src + k * kStBlkPairs * kStLanes + lane;
+      for (int k = 0; k < kStG; ++k) {
+        const int j = c * kStG + k - lane;
+        if (j >= 0 && j < nblk) {
 #pragma unroll
-        for (int r = 0; r < kStR; ++r) {
-          if (y0 + r < a.ny) {
-            double* row = a.x + (size_t)(y0 + r) * a.nx + j * kStC;
-            if (a.x_aligned) {
-#pragma unroll
-              for (int q = 0; q < kStC / 2; ++q)
-                reinterpret_cast<double2*>(row)[q] = blk[(r * (kStC / 2) + q) * kStLanes];
-            } else {
+          for (int r = 0; r < kStR; ++r) {
+            if (y0 + r < a.ny) {
+              double* row = a.x + (size_t)(y0 + r) * a.nx + j * kStC;
 #pragma unroll
               for (int q = 0; q < kStC / 2; ++q) {
-                const double2 v = blk[(r * (kStC / 2) + q) * kStLanes];
-                row[2 * q] = v.x;
-                row[2 * q + 1] = v.y;
+                const double2 v = src[st_b_piece(r, lane, k, q)];
+                if (a.x_aligned) {
+                  reinterpret_cast<double2*>(row)[q] = v;
+                } else {
+                  row[2 * q] = v.x;
+                  row[2 * q + 1] = v.y;
+                }
               }
             }
           }
@@ -443,6 +458,7 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     __syncwarp();
     if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
   }
+  if (x_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   // overlapped host solve: band t's x may now be copied to the host
   if (a.xflag && lane == 0) {
     __threadfence_system();
@@ -558,13 +574,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
           st_relaxed_sys_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish_sys && active);
       }
     }
-    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk) +
-                   k * kStBlkPairs * kStLanes + lane;
+    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
 #pragma unroll
     for (int r = 0; r < kStR; ++r)
 #pragma unroll
       for (int q = 0; q < kStC; q += 2)
-        if (!(ABL & 1)) dst[(r * (kStC / 2) + q / 2) * kStLanes] = make_double2(xb[r][q], xb[r][q + 1]);
+        if (!(ABL & 1)) dst[st_b_piece(r, lane, k, q / 2)] = make_double2(xb[r][q], xb[r][q + 1]);
     if (k + 2 < kStG) {
       if (!(ABL & 2)) nxt2.load(smem, c % NB, k + 2, lane);
     } else if (c + 1 < nchunks) {
@@ -873,6 +888,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
   a.b_tma_bands = (kStBTma && a.b_aligned) ? encode_b_map(&a.bmap, d_b, stencil.nx, stencil.ny) : 0;
+  a.x_tma_bands = (kStBTma && a.x_aligned) ? encode_b_map(&a.xmap, d_x, stencil.nx, stencil.ny) : 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
   if (b_flags) a.bflag = stencil.bflag;
   if (x_flags) a.xflag = stencil.xflag;
