@@ -68,9 +68,17 @@ void DevicePlan::release() {
   if (cs_out) cudaStreamDestroy(cs_out);
 }
 
-int DevicePlan::run_levels() {
+int DevicePlan::run_levels(const int* grid, bool precomputed) {
   // K6: level_i = 1 + max(level_j) over dependencies, 0 without any; the
-  // component pool in (max,+1) arithmetic over the natural (topological) order.
+  // component pool in (max,+1) arithmetic over the natural (topological) order
+  // — or, for a verified 2D / 3D lower stencil, its closed form: row
+  // (x, y[, z]) depends exactly on (x-1, ...), (x, y-1, ...)[, (x, y, z-1)],
+  // so its earliest level is x + y (+ z), the same integers.
+  if (precomputed) {
+    // `level` already holds the levels (the band window kernel)
+  } else if (grid) {
+    CUDA_TRY(launch_grid_levels(level, n, grid[0], grid[1], grid[2], stream));
+  } else {
   CUDA_TRY(cudaMemsetAsync(level, 0xFF, sizeof(int) * (size_t)n, stream));
   CUDA_TRY(reset_control(stream));
   RowsArgs a{};
@@ -94,6 +102,7 @@ int DevicePlan::run_levels() {
   CUDA_TRY(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));
   if (hs.code == SPTRSV_E_TIMEOUT) return fail(SPTRSV_E_TIMEOUT, "level analysis exceeded the timeout");
+  }
 
   // group components by level: stable sort (level, row) -> ascending rows per level
   int *iota = nullptr, *keys_out = nullptr, *cnt = nullptr, *tick = nullptr, *tb = nullptr;

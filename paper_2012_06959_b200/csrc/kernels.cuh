@@ -21,6 +21,7 @@ cudaError_t launch_gather_offdiag(const int* sorted_entry, const int* colE, cons
 cudaError_t launch_scale_rows(const int* rp, const double* cv, const double* dg, int n, double* wv, double* rdg,
                               cudaStream_t s);
 cudaError_t launch_iota(int* a, int n, cudaStream_t s);
+cudaError_t launch_grid_levels(int* level, long long n, int nx, int ny, int nz, cudaStream_t s);
 cudaError_t launch_widen(const int* a, long long* out, long long n, cudaStream_t s);
 cudaError_t launch_level_hist(const int* level, int n, int* cnt, cudaStream_t s);
 cudaError_t launch_tickets_per_level(const int* cnt, int nl, int* t, cudaStream_t s);

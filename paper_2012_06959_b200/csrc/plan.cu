@@ -4,6 +4,9 @@
 // reference's vocabulary (engine.py:445-490 + analysis.py:43-64).
 #include <string>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include "plan.hpp"
 #include "kernels.cuh"
 
@@ -23,6 +26,16 @@ static cudaError_t dal(T** p, size_t count) {
 }
 
 int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const double* values, int64_t* bad_col) {
+  // SPTRSV_SETUP_TRACE=1: phase times of plan creation on stderr (diagnostics)
+  static const bool trace = std::getenv("SPTRSV_SETUP_TRACE") != nullptr;
+  auto tr0 = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!trace) return;
+    cudaStreamSynchronize(stream);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %9.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tr0).count());
+    tr0 = now;
+  };
   P_TRY(cudaSetDevice(device));
   P_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
   P_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
@@ -54,6 +67,7 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   P_TRY(cudaMemcpyAsync(&h_sbad, sbad, sizeof(int), cudaMemcpyDeviceToHost, stream));
   P_TRY(cudaMemcpyAsync(&h_fv, fviol, sizeof(h_fv), cudaMemcpyDeviceToHost, stream));
   P_TRY(cudaStreamSynchronize(stream));
+  mark("upload + validate");
   cudaFree(d_cp);
   cudaFree(d_ri64);
   cudaFree(sbad);
@@ -108,6 +122,7 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   P_TRY(dal(&cv, noff));
   P_TRY(launch_gather_offdiag(entry_s, colE, d_val, noff, ci, cv, stream));
   P_TRY(cudaStreamSynchronize(stream));
+  mark("in-degree + CSR transpose");
   cudaFree(key);
   cudaFree(entry);
   cudaFree(key_s);
@@ -136,7 +151,48 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
   P_TRY(cudaStreamSynchronize(stream));
 
   // K6: levels (bit-exact) + level-ordered tickets for the component pool
-  int rc = run_levels();
+  mark("scratch");
+  // host copy of the CSR structure for structure detection and the schedulers
+  std::vector<int> h_rp, h_ci;
+  int grid_dims[3] = {0, 0, 0};
+  bool grid_known = false;
+  // (structure-only plans too: detection needs only the pattern, and a grid
+  // stencil's levels have a closed form)
+  if (!indeg_only && opt.executor != SPTRSV_EXECUTOR_ROWS && opt.executor != SPTRSV_EXECUTOR_PUSH) {
+    h_rp.resize(n + 1);
+    h_ci.resize(noff);
+    P_TRY(cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
+    if (noff) P_TRY(cudaMemcpy(h_ci.data(), ci, sizeof(int) * noff, cudaMemcpyDeviceToHost));
+    mark("CSR to host");
+    if (opt.executor == SPTRSV_EXECUTOR_AUTO || opt.executor == SPTRSV_EXECUTOR_STENCIL) {
+      if (const int nx = detect_stencil2d(n, h_rp, h_ci)) {
+        grid_dims[0] = nx, grid_dims[1] = (int)(n / nx), grid_dims[2] = 0;
+        grid_known = true;
+      } else if (detect_stencil3d(n, h_rp, h_ci, grid_dims)) {
+        grid_known = true;
+      }
+      mark("structure detection");
+    }
+  }
+  // a narrow band: levels from the band window kernel in (max, +1) mode
+  // (the pool would pay a memory round trip per level: 4.7 M levels)
+  bool levels_done = false;
+  if (!grid_known && !h_rp.empty() && !structure_only &&
+      (opt.executor == SPTRSV_EXECUTOR_AUTO || opt.executor == SPTRSV_EXECUTOR_BAND) && band_narrow(h_rp, h_ci)) {
+    int brc = build_band();
+    if (brc != SPTRSV_OK) return brc;
+    brc = band_levels(level);
+    if (brc != SPTRSV_OK) return brc;
+    levels_done = true;
+    mark("band structure + levels");
+  }
+  int rc = run_levels(grid_known ? grid_dims : nullptr, levels_done);
+  mark("levels + ticket order");
+  if (rc != SPTRSV_OK) return rc;
+  // keep the band (n x 64 doubles) only if the band executor will run on it
+  if (band.ready && !(opt.executor == SPTRSV_EXECUTOR_BAND ||
+                      (opt.executor == SPTRSV_EXECUTOR_AUTO && n_levels > n / 8)))
+    band.release();
   if (rc != SPTRSV_OK) return rc;
 
   executor_used = SPTRSV_EXECUTOR_ROWS;
@@ -147,13 +203,10 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
     return SPTRSV_OK;
   }
   if (!structure_only && opt.executor != SPTRSV_EXECUTOR_ROWS) {
-    // host copy of the CSR structure for the schedulers
-    std::vector<int> h_rp(n + 1), h_ci(noff);
-    P_TRY(cudaMemcpy(h_rp.data(), rp, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
-    if (noff) P_TRY(cudaMemcpy(h_ci.data(), ci, sizeof(int) * noff, cudaMemcpyDeviceToHost));
     if (opt.executor == SPTRSV_EXECUTOR_AUTO || opt.executor == SPTRSV_EXECUTOR_STENCIL) {
       rc = build_stencil(h_rp, h_ci);
       if (rc != SPTRSV_OK) return rc;
+      mark("stencil detect + pack");
       if (stencil.ready) {
         executor_used = SPTRSV_EXECUTOR_STENCIL;
         return SPTRSV_OK;
@@ -176,11 +229,19 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
           if (h_rp[i] < h_rp[i + 1] && i - h_ci[h_rp[i]] > 64) narrow = false;
         if (!narrow) return plan_fail(SPTRSV_E_UNSUPPORTED, "band executor needs every dependency within 64 rows");
       }
-      rc = build_band();
-      if (rc != SPTRSV_OK) return rc;
+      if (!band.ready) {
+        rc = build_band();
+        if (rc != SPTRSV_OK) return rc;
+      }
       executor_used = SPTRSV_EXECUTOR_BAND;
       return SPTRSV_OK;
     }
+    // AUTO prefers lane chains only when every row has at most 8 dependencies
+    // (chains_preferred); skip building a schedule that cannot win
+    int max_deps = 0;
+    if (opt.executor == SPTRSV_EXECUTOR_AUTO)
+      for (long long i = 0; i < n; ++i) max_deps = std::max(max_deps, h_rp[i + 1] - h_rp[i]);
+    if (opt.executor == SPTRSV_EXECUTOR_AUTO && max_deps > 8) return SPTRSV_OK;
     rc = build_chains(h_rp, h_ci);
     if (rc != SPTRSV_OK) return rc;
     if (chains.ready && (opt.executor == SPTRSV_EXECUTOR_CHAINS || chains_preferred()))

@@ -102,6 +102,8 @@ struct DevicePlan {
   bool band_candidate(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const;
   int build_band();
   int solve_band(const double* d_b, double* d_x, cudaStream_t s);
+  int band_levels(int* level_out);
+  bool band_narrow(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const;
   int solve_push(const double* d_b, double* d_x, cudaStream_t s);
 
   // PE partition (partition.cu): each PE owns components (PartitionPlan.owner_arr)
@@ -134,7 +136,10 @@ struct DevicePlan {
   bool pending = false;
 
   int build(const int64_t* col_ptr, const int64_t* row_idx, const double* values, int64_t* bad_col);
-  int run_levels();
+  // levels: the component pool in (max, +1) arithmetic, or the closed form
+  // x + y (+ z) when the CSR is a detected 2D / 3D lower stencil (grid = nx,
+  // ny, nz; nz = 0 for 2D)
+  int run_levels(const int* grid = nullptr, bool precomputed = false);
   int rows_grid(int mode) const;
   int solve_rows(const double* d_b, double* d_x, cudaStream_t s);
   int solve_chains(const double* d_b, double* d_x, cudaStream_t s);

@@ -9,6 +9,7 @@
 //   cv[noff]   L values             (exact mode)
 //   wv[noff]   -L_ij / L_ii         (fast mode, rows pre-scaled by 1/diag)
 //   dg[n], rdg[n]  diagonal and its correctly rounded reciprocal
+#include <algorithm>
 #include "common.cuh"
 #include "kernels.cuh"
 #include <cub/cub.cuh>
@@ -198,6 +199,19 @@ cudaError_t launch_iota(int* a, int n, cudaStream_t s) {
 
 cudaError_t launch_widen(const int* a, long long* out, long long n, cudaStream_t s) {
   k_widen<<<grid_for(n, 256), 256, 0, s>>>(a, out, n);
+  return cudaGetLastError();
+}
+
+// Closed-form levels of a 2D (nz == 0) or 3D lower stencil in natural order.
+__global__ void k_grid_levels(int* __restrict__ level, long long n, int nx, int ny, int nz) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long x = i % nx, y = (i / nx) % ny, z = nz ? i / ((long long)nx * ny) : 0;
+    level[i] = (int)(x + y + z);
+  }
+}
+
+cudaError_t launch_grid_levels(int* level, long long n, int nx, int ny, int nz, cudaStream_t s) {
+  k_grid_levels<<<grid_for((int)std::min<long long>(n, 1 << 30), 256), 256, 0, s>>>(level, n, nx, ny, nz);
   return cudaGetLastError();
 }
 

@@ -189,7 +189,38 @@ __device__ void band_compute(const BandArgs& a, unsigned char* smem, int* ctl, i
   }
 }
 
-template <bool EXACT>
+// Level mode (K6 for narrow bands): the same window in (max, +1) integer
+// arithmetic over the presence masks — level_j = max over stored entries
+// (j, i) of level_i + 1 — one shuffle per row, bit-exact by construction.
+__device__ void band_levels(const BandArgs& a, unsigned char* smem, int* ctl, int lane, unsigned long long deadline) {
+  int acc[2] = {0, 0};
+  int* level = reinterpret_cast<int*>(a.x);
+  for (int c = 0; c < a.nchunks; ++c) {
+    if (!b_wait(ctl, kBInReady, c + 1, deadline, 0)) return;
+    const int slot = c % kBSlots;
+    const unsigned long long* msk = reinterpret_cast<const unsigned long long*>(smem + BSmem::kMask) + slot * kBK;
+#pragma unroll 8
+    for (int k = 0; k < kBK; ++k) {
+      const long long j = (long long)c * kBK + k;
+      const int p = k, owner = p >> 1, os = p & 1;
+      int lv = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
+      if (lane == owner && j < a.n) level[j] = lv;
+      const unsigned long long mj = msk[k];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int d = ((2 * lane + s - p - 1) & (kBW - 1)) + 1;
+        int v = (lane == owner && s == os) ? 0 : acc[s];  // row j + 64 enters with level 0
+        if ((mj >> (d - 1)) & 1ull) v = max(v, lv + 1);
+        acc[s] = v;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kBInDone, c + 1);
+    if (ld_acquire_cta(ctl + kBAbort)) return;
+  }
+}
+
+template <int MODE>  // 0 fast, 1 exact, 2 levels
 __global__ void __launch_bounds__(kBThreads, 1) k_band(const __grid_constant__ BandArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   int* ctl = reinterpret_cast<int*>(smem + BSmem::kCtl);
@@ -202,8 +233,27 @@ __global__ void __launch_bounds__(kBThreads, 1) k_band(const __grid_constant__ B
   }
   __syncthreads();
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
-  if (warp == 0) band_compute<EXACT>(a, smem, ctl, lane, deadline);
+  if (warp == 0) {
+    if (MODE == 2) band_levels(a, smem, ctl, lane, deadline);
+    else band_compute<MODE == 1>(a, smem, ctl, lane, deadline);
+  }
   else band_loader(a, smem, ctl, lane, deadline);
+}
+
+template <int MODE>
+cudaError_t launch_band_v(const BandArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_band<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, BSmem::kTotal);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_band<MODE><<<1, kBThreads, BSmem::kTotal, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band(const BandArgs& a, int mode, cudaStream_t s) {
+  return mode == 2 ? launch_band_v<2>(a, s) : mode == 1 ? launch_band_v<1>(a, s) : launch_band_v<0>(a, s);
 }
 
 __global__ void k_band_scatter(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ val,
@@ -218,12 +268,17 @@ __global__ void k_band_scatter(const int* __restrict__ rp, const int* __restrict
 
 }  // namespace
 
-// Narrow band (every dependency within kBW rows) and low parallelism.
-bool DevicePlan::band_candidate(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const {
+// Every dependency within kBW rows.
+bool DevicePlan::band_narrow(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const {
   if (n < 2 * kBW) return false;
   for (long long i = 0; i < n; ++i)
     if (h_rp[i] < h_rp[i + 1] && i - h_ci[h_rp[i]] > kBW) return false;
-  return n_levels > n / 8;  // the pool wins when levels are wide
+  return true;
+}
+
+// Narrow band and low parallelism (the pool wins when levels are wide).
+bool DevicePlan::band_candidate(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const {
+  return n_levels > n / 8 && band_narrow(h_rp, h_ci);
 }
 
 int DevicePlan::build_band() {
@@ -263,18 +318,38 @@ int DevicePlan::solve_band(const double* d_b, double* d_x, cudaStream_t s) {
   a.n = n;
   a.nchunks = band.nchunks;
   a.exact = opt.precision != SPTRSV_PRECISION_FAST;
-  static bool attr[2] = {false, false};
-  auto kern = a.exact ? k_band<true> : k_band<false>;
-  if (!attr[a.exact]) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BSmem::kTotal)) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    attr[a.exact] = true;
-  }
+  const int mode = a.exact ? 1 : 0;
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  kern<<<1, kBThreads, BSmem::kTotal, s>>>(a);
-  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = launch_band(a, mode, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;
+  return SPTRSV_OK;
+}
+
+// K6 for a narrow band: levels into `level` (int32[n]) with the window kernel.
+int DevicePlan::band_levels(int* level_out) {
+  if (!band.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "band structure not built");
+  cudaError_t e;
+  if ((e = reset_control(stream)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  BandArgs a{};
+  a.coef = band.coef;
+  a.mask = band.mask;
+  a.b = dg;  // row data are streamed but unused in level mode
+  a.dg = dg;
+  a.rdg = rdg;
+  a.x = reinterpret_cast<double*>(level_out);
+  a.status = status;
+  a.abort_flag = abort_flag;
+  a.timeout_ns = (unsigned long long)(std::max(opt.timeout_s, 600.0) * 1e9);
+  a.n = n;
+  a.nchunks = band.nchunks;
+  a.exact = 1;  // loader: unshifted row data
+  if ((e = launch_band(a, 2, stream)) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  DeviceStatus hs{};
+  if ((e = cudaMemcpy(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if (hs.code == SPTRSV_E_TIMEOUT) return plan_fail(SPTRSV_E_TIMEOUT, "level analysis exceeded the timeout");
   return SPTRSV_OK;
 }
 

@@ -688,6 +688,46 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
 
 }  // namespace
 
+// Pack the coefficient stream [task][step][field][pair][lane] (see
+// stencil.hpp) from the CSR: one thread per (task, step, lane). Row i's
+// entries are (i, i - nx) when y > 0 then (i, i - 1) when x > 0 (the
+// detected structure). Padding elements get zero coefficients and, in exact
+// mode, d = 1/d = 1 so the Markstein guard stays on the fast path.
+__global__ void k_st_pack(const int* __restrict__ rp, const double* __restrict__ val, const double* __restrict__ dg,
+                          const double* __restrict__ rdg, int nx, int ny, int n_tasks, int steps, int exact,
+                          unsigned char* __restrict__ out) {
+  const long long items = (long long)n_tasks * steps * kStLanes;
+  const int nblk = nx / kStC, NF = exact ? 4 : 3, pairs = kStBlock / 2;
+  const size_t step_doubles = (size_t)NF * pairs * kStLanes * 2;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(it % kStLanes);
+    const long long ts = it / kStLanes;
+    const int sidx = (int)(ts % steps), t = (int)(ts / steps);
+    const int j = sidx - l;
+    double* stepbuf = reinterpret_cast<double*>(out) + (size_t)ts * step_doubles;
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) {
+      const long long y = (long long)t * kStBand + kStR * l + r;
+#pragma unroll
+      for (int c = 0; c < kStC; ++c) {
+        const int e_ = r * kStC + c, k = e_ / 2, half = e_ % 2;
+        double f[4] = {0.0, 0.0, exact ? 1.0 : 0.0, exact ? 1.0 : 0.0};
+        if (j >= 0 && j < nblk && y < ny) {
+          const long long i = y * nx + (long long)j * kStC + c;
+          int kk = rp[i];
+          const double fu = y > 0 ? val[kk++] : 0.0;
+          const double fl = (j * kStC + c) > 0 ? val[kk] : 0.0;
+          f[0] = fu, f[1] = fl;
+          if (exact) f[2] = dg[i], f[3] = rdg[i];
+          else f[2] = rdg[i];
+        }
+        for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
+      }
+    }
+  }
+}
+
 // Reset `count` mailbox words to kStNotReady (cuMemsetD32Async through the
 // runtime's driver entry point).
 static cudaError_t fill_not_ready(unsigned long long* p, long long count, cudaStream_t s) {
@@ -741,7 +781,7 @@ static int encode_b_map(CUtensorMap* map, const double* b, int nx, int ny) {
 }
 
 // Detect the 2D five-point lower structure on the host CSR; returns nx or 0.
-static int detect_stencil2d(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
+int detect_stencil2d(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
   if (n < 4) return 0;
   long long nx = 0;
   for (long long i = 1; i < n && !nx; ++i)
@@ -782,51 +822,7 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   const int NF = st_fields(exact);
   const size_t step_bytes = st_step_bytes(exact);
   const size_t bytes = step_bytes * stencil.steps_per_task * stencil.n_tasks;
-  // coefficients (host copies of the device CSR values)
-  std::vector<double> h_val(noff), h_dg(n), h_rdg(n);
   cudaError_t e;
-  if ((noff && (e = cudaMemcpy(h_val.data(), exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
-                   cudaSuccess) ||
-      (e = cudaMemcpy(h_dg.data(), dg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(h_rdg.data(), rdg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  std::vector<double> st(bytes / 8, 0.0);
-  const int nblk = nx / kStC;
-  const int pairs = kStBlock / 2;
-  for (int t = 0; t < stencil.n_tasks; ++t) {
-    for (int s = 0; s < stencil.steps_per_task; ++s) {
-      double* stepbuf = st.data() + ((size_t)t * stencil.steps_per_task + s) * (step_bytes / 8);
-      for (int l = 0; l < kStLanes; ++l) {
-        const int j = s - l;
-        for (int r = 0; r < kStR; ++r) {
-          const long long y = (long long)t * kStBand + kStR * l + r;
-          for (int c = 0; c < kStC; ++c) {
-            const int e_ = r * kStC + c;
-            const int k = e_ / 2, half = e_ % 2;
-            double f[4];
-            if (j < 0 || j >= nblk || y >= stencil.ny) {
-              // padding element: no coefficients; exact mode divides by 1 so
-              // the block's Markstein guard stays on the fast path
-              f[0] = f[1] = 0.0, f[2] = exact ? 1.0 : 0.0, f[3] = exact ? 1.0 : 0.0;
-              for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
-              continue;
-            }
-            const long long i = y * nx + (long long)j * kStC + c;
-            double fu = 0.0, fl = 0.0;
-            int kk = h_rp[i];
-            if (y > 0) fu = h_val[kk++];
-            if (j * kStC + c > 0) fl = h_val[kk];
-            if (exact) {
-              f[0] = fu, f[1] = fl, f[2] = h_dg[i], f[3] = h_rdg[i];
-            } else {
-              f[0] = fu, f[1] = fl, f[2] = h_rdg[i];
-            }
-            for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
-          }
-        }
-      }
-    }
-  }
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
   if ((e = al((void**)&stencil.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&stencil.mbox, 2 * sizeof(unsigned long long) * (size_t)stencil.n_tasks * nx)) != cudaSuccess ||
@@ -835,9 +831,18 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
       (e = al((void**)&stencil.bflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = al((void**)&stencil.xflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = cudaMemset(stencil.bflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
-      (e = cudaMemset(stencil.xflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
-      (e = cudaMemcpy(stencil.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess)
+      (e = cudaMemset(stencil.xflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // the coefficient stream is packed on the device from the CSR (one thread
+  // per lane-step, no host round trip of the values)
+  {
+    const long long items = (long long)stencil.n_tasks * stencil.steps_per_task * kStLanes;
+    const int grid = (int)std::min<long long>((items + 255) / 256, 148 * 64);
+    k_st_pack<<<grid, 256, 0, stream>>>(rp, exact ? cv : wv, dg, rdg, nx, stencil.ny, stencil.n_tasks,
+                                        stencil.steps_per_task, exact ? 1 : 0, stencil.stream);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
   stencil.n_my_tasks = stencil.n_tasks;
   stencil.stream_bytes = (long long)bytes;
   stencil.ready = true;

@@ -109,6 +109,10 @@ struct StencilPlan {
   }
 };
 
+// Structure detection on the host CSR (stencil.cu, stencil3d.cu).
+int detect_stencil2d(long long n, const std::vector<int>& rp, const std::vector<int>& ci);
+bool detect_stencil3d(long long n, const std::vector<int>& rp, const std::vector<int>& ci, int* dims);
+
 // 3D seven-point lower structure (stencil3d.cu): tiles of 32 y-rows x 4
 // z-planes, one CTA each, dispatched in ascending (Z, Y) order.
 struct Stencil3Plan {

@@ -536,8 +536,49 @@ static cudaError_t s3_fill_not_ready(unsigned long long* p, long long words, cud
 
 }  // namespace
 
+// Pack the 3D coefficient stream [task][step][field][pair][lane]: fields
+// wz wy wx [d] rd per element (row i's entries in ascending column order:
+// z, y, x neighbours); padding elements zero, exact d = 1/d = 1.
+__global__ void k_s3_pack(const int* __restrict__ rp, const double* __restrict__ val, const double* __restrict__ dg,
+                          const double* __restrict__ rdg, int nx, int ny, int nz, int nyt, int n_tasks, int steps,
+                          int exact, unsigned char* __restrict__ out) {
+  const long long items = (long long)n_tasks * steps * k3Lanes;
+  const int nblk = nx / k3C, NF = exact ? 5 : 4;
+  const size_t step_doubles = (size_t)NF * k3Pairs * k3Lanes * 2;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(it % k3Lanes);
+    const long long ts = it / k3Lanes;
+    const int s = (int)(ts % steps), t = (int)(ts / steps);
+    const int Y = t % nyt, Z = t / nyt, j = s - l;
+    const long long y = (long long)Y * k3Lanes + l;
+    double* sb = reinterpret_cast<double*>(out) + (size_t)ts * step_doubles;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      const long long z = (long long)Z * k3R + r;
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) {
+        const int e_ = r * k3C + q, pair = e_ / 2, half = e_ % 2;
+        double f[5] = {0.0, 0.0, 0.0, exact ? 1.0 : 0.0, exact ? 1.0 : 0.0};
+        if (j >= 0 && j < nblk && y < ny && z < nz) {
+          const long long x = (long long)j * k3C + q;
+          const long long i = (z * ny + y) * nx + x;
+          int kk = rp[i];
+          const double fz = z > 0 ? val[kk++] : 0.0;
+          const double fy = y > 0 ? val[kk++] : 0.0;
+          const double fx = x > 0 ? val[kk] : 0.0;
+          f[0] = fz, f[1] = fy, f[2] = fx;
+          if (exact) f[3] = dg[i], f[4] = rdg[i];
+          else f[3] = rdg[i];
+        }
+        for (int fld = 0; fld < NF; ++fld) sb[((fld * k3Pairs + pair) * k3Lanes + l) * 2 + half] = f[fld];
+      }
+    }
+  }
+}
+
 // 3D seven-point lower structure on the host CSR: returns true and (nx, ny, nz).
-static bool detect_stencil3d(long long n, const std::vector<int>& rp, const std::vector<int>& ci, int* dims) {
+bool detect_stencil3d(long long n, const std::vector<int>& rp, const std::vector<int>& ci, int* dims) {
   if (n < 8) return false;
   long long nx = 0, nxy = 0;
   for (long long i = 1; i < n && (!nx || !nxy); ++i)
@@ -587,55 +628,25 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
   const int NF = s3_fields(exact);
   const size_t step_doubles = s3_step_bytes(exact) / 8;
   const size_t bytes = s3_step_bytes(exact) * (size_t)P.steps * P.n_tasks;
-  std::vector<double> h_val(noff), h_dg(n), h_rdg(n);
   cudaError_t e;
-  if ((noff && (e = cudaMemcpy(h_val.data(), exact ? cv : wv, sizeof(double) * noff, cudaMemcpyDeviceToHost)) !=
-                   cudaSuccess) ||
-      (e = cudaMemcpy(h_dg.data(), dg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess ||
-      (e = cudaMemcpy(h_rdg.data(), rdg, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
-    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  std::vector<double> st(bytes / 8, 0.0);
-  for (int t = 0; t < P.n_tasks; ++t) {
-    const int Y = t % P.nyt, Z = t / P.nyt;
-    for (int s = 0; s < P.steps; ++s) {
-      double* sb = st.data() + ((size_t)t * P.steps + s) * step_doubles;
-      for (int l = 0; l < k3Lanes; ++l) {
-        const int j = s - l;
-        const long long y = (long long)Y * k3Lanes + l;
-        for (int r = 0; r < k3R; ++r) {
-          const long long z = (long long)Z * k3R + r;
-          for (int q = 0; q < k3C; ++q) {
-            const int e_ = r * k3C + q, pair = e_ / 2, half = e_ % 2;
-            double f[5] = {0.0, 0.0, 0.0, exact ? 1.0 : 0.0, exact ? 1.0 : 0.0};
-            if (!exact) f[3] = 0.0;  // fast: fields wz wy wx rd (rd of padding 0)
-            if (j >= 0 && j < nblk && y < P.ny && z < P.nz) {
-              const long long x = (long long)j * k3C + q;
-              const long long i = (z * P.ny + y) * P.nx + x;
-              int kk = h_rp[i];
-              const double fz = z > 0 ? h_val[kk++] : 0.0;
-              const double fy = y > 0 ? h_val[kk++] : 0.0;
-              const double fx = x > 0 ? h_val[kk] : 0.0;
-              if (exact) {
-                f[0] = fz, f[1] = fy, f[2] = fx, f[3] = h_dg[i], f[4] = h_rdg[i];
-              } else {
-                f[0] = fz, f[1] = fy, f[2] = fx, f[3] = h_rdg[i];
-              }
-            }
-            for (int fld = 0; fld < NF; ++fld) sb[((fld * k3Pairs + pair) * k3Lanes + l) * 2 + half] = f[fld];
-          }
-        }
-      }
-    }
-  }
+  (void)step_doubles;
+  (void)NF;
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
   const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
   if ((e = al((void**)&P.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
       (e = al((void**)&P.zmail, 2 * sizeof(unsigned long long) * zw)) != cudaSuccess ||
-      (e = cudaMemcpy(P.stream, st.data(), bytes, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = s3_fill_not_ready(P.ymail, 2 * yw, 0)) != cudaSuccess ||
       (e = s3_fill_not_ready(P.zmail, 2 * zw, 0)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  {  // pack the coefficient stream on the device (one thread per tile-step-lane)
+    const long long items = (long long)P.n_tasks * P.steps * k3Lanes;
+    const int grid = (int)std::min<long long>((items + 255) / 256, 148 * 64);
+    k_s3_pack<<<grid, 256, 0, stream>>>(rp, exact ? cv : wv, dg, rdg, P.nx, P.ny, P.nz, P.nyt, P.n_tasks, P.steps,
+                                        exact ? 1 : 0, P.stream);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
   P.stream_bytes = (long long)bytes;
   P.ready = true;
   P.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -427,3 +427,30 @@ def test_solve_many_columns():
     xs = sp.solve_many(l, bs, precision="exact")
     for k in range(5):
         assert xs[:, k].tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, bs[:, k].copy()).tobytes()
+
+
+@pytest.mark.parametrize("name", ["lap2d-64x50", "lap3d-9x7x5", "lap3d-16", "banded-5k-16", "banded-3k-64-dense",
+                                  "bidiagonal-3000", "random-band"])
+def test_levels_fast_paths_bit_exact(name):
+    """K6 takes the closed form x+y(+z) for verified grid stencils and the band
+    window kernel in (max,+1) mode for narrow bands: levels and in-degrees
+    must equal the oracle's bit for bit."""
+    l = {
+        "lap2d-64x50": lambda: synth.lap2d(64, 50),
+        "lap3d-9x7x5": lambda: synth.lap3d(10, 7, 5),
+        "lap3d-16": lambda: synth.lap3d(16),
+        "banded-5k-16": BAND_CASES["banded-5k-16"],
+        "banded-3k-64-dense": BAND_CASES["banded-3k-64-dense"],
+        "bidiagonal-3000": BAND_CASES["bidiagonal-3000"],
+        "random-band": lambda: synth.random_lower(4000, 0.01, 9, bandwidth=40, dominant=True),
+    }[name]()
+    lv, nl = oracle.levels(l.col_ptr, l.row_idx)
+    sched = sp.compute_level_schedule(l)
+    assert sched.n_levels == nl
+    np.testing.assert_array_equal(sched.level_of, lv)
+    np.testing.assert_array_equal(sp.compute_in_degrees(l), oracle.in_degrees(l.col_ptr, l.row_idx))
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor="auto")
+    level_of, order, level_ptr, n_levels = plan.levels()
+    assert n_levels == nl
+    np.testing.assert_array_equal(level_of, lv)
+    plan.close()
