@@ -275,7 +275,10 @@ def main():
             t1 = time.perf_counter()
             plan.solve(hb_np, out=hx_np)
             t_e2e.append(time.perf_counter() - t1)
-        assert hx_np.tobytes() == x_dev.tobytes()
+        # same solution through both paths (bitwise when the executor is
+        # deterministic; fast-mode split rows add partial sums atomically)
+        diff = np.abs(hx_np - x_dev) / np.maximum(np.abs(x_dev), 1.0)
+        assert (not diff.size) or float(np.nanmax(diff)) <= 1e-12, float(np.nanmax(diff))
         d2h = 8 * n
     else:
         rows = solver.rows
