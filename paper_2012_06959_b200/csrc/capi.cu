@@ -1,6 +1,7 @@
 // C ABI (include/sptrsv_b200.h): plan lifetime, preprocessing pipeline and the
 // solve entry points. Host-side runtime in C++; all compute is device kernels.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -369,16 +370,33 @@ int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st
   for (int t = 0; t < nt; ++t)
     if (g_write32(stream, (unsigned long long)(stencil.xflag + t), ep, 0) != 0)
       return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
-  for (int t = 0; t < nt; ++t) {
-    const long long off = t * band, cnt = std::min(band, n - off);
+  // Copy granularity (bands per copy): b goes in doubling chunks (1, 2, 4
+  // bands: the first band starts the kernel early, bigger copies keep the link
+  // efficient); x comes out 2 bands at a time. Tunable by SPTRSV_STREAM_IN /
+  // SPTRSV_STREAM_OUT (tools/e2e_sweep.sh: 4.3-4.8 ms over 1..32 bands per copy
+  // on lap2d-4096 — the PCIe link shared by both directions is the limit).
+  static const int in_max = [] {
+    const char* e = std::getenv("SPTRSV_STREAM_IN");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
+  }();
+  static const int out_n = [] {
+    const char* e = std::getenv("SPTRSV_STREAM_OUT");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 2;
+  }();
+  for (int t0b = 0, w = 1; t0b < nt; t0b += w, w = std::min(2 * w, in_max)) {
+    const int t1b = std::min(nt, t0b + w);
+    const long long off = t0b * band, cnt = std::min(band * (t1b - t0b), n - off);
     CUDA_TRY(cudaMemcpyAsync(bbuf + off, b + off, sizeof(double) * cnt, cudaMemcpyHostToDevice, cs_in));
-    if (g_write32(cs_in, (unsigned long long)(stencil.bflag + t), ep, 0) != 0)
-      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
+    for (int t = t0b; t < t1b; ++t)
+      if (g_write32(cs_in, (unsigned long long)(stencil.bflag + t), ep, 0) != 0)
+        return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
   }
-  for (int t = 0; t < nt; ++t) {
-    const long long off = t * band, cnt = std::min(band, n - off);
-    if (g_wait32(cs_out, (unsigned long long)(stencil.xflag + t), ep, kWaitGeq) != 0)
-      return fail(SPTRSV_E_CUDA, "cuStreamWaitValue32 failed");
+  for (int t0b = 0; t0b < nt; t0b += out_n) {
+    const int t1b = std::min(nt, t0b + out_n);
+    const long long off = t0b * band, cnt = std::min(band * (t1b - t0b), n - off);
+    for (int t = t0b; t < t1b; ++t)
+      if (g_wait32(cs_out, (unsigned long long)(stencil.xflag + t), ep, kWaitGeq) != 0)
+        return fail(SPTRSV_E_CUDA, "cuStreamWaitValue32 failed");
     CUDA_TRY(cudaMemcpyAsync(x + off, xbuf + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, cs_out));
   }
   CUDA_TRY(cudaStreamSynchronize(cs_in));
