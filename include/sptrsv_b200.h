@@ -183,6 +183,14 @@ int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr
 void* sptrsv_plan_segment(const sptrsv_plan* plan); /* this process's first segment (device pointer) */
 int sptrsv_ipc_handle_size(void);
 
+/* Matrix Market ingestion (reference mmio.py:132-144 `_coo_to_csc`): COO
+ * (0-based int64 rows/cols, float64 values, nnz entries) -> CSC sorted
+ * column-major, rows ascending, duplicate coordinates summed in input order
+ * (bit-identical to the reference). Outputs: col_ptr int64[n+1], row_idx and
+ * values sized nnz (upper bound); *nnz_out = unique entries. On the GPU. */
+int sptrsv_coo_to_csc(int64_t n, const int64_t* rows, const int64_t* cols, const double* vals, int64_t nnz,
+                      int32_t device, int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* nnz_out);
+
 /* Diagnostics: copy up to `count` probe timestamps (clock64) recorded by the
  * last solve when options.probe_flags asked for them. */
 int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count);

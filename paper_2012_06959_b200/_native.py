@@ -115,6 +115,9 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_plan_levels.restype = C.c_int
     lib.sptrsv_in_degrees.argtypes = [_P64, _P64, C.c_int64, C.c_int32, _P64]
     lib.sptrsv_in_degrees.restype = C.c_int
+    lib.sptrsv_coo_to_csc.argtypes = [C.c_int64, _P64, _P64, _PD, C.c_int64, C.c_int32, _P64, _P64, _PD,
+                                      C.POINTER(C.c_int64)]
+    lib.sptrsv_coo_to_csc.restype = C.c_int
     lib.sptrsv_solve.argtypes = [C.c_void_p, _PD, _PD, C.POINTER(Stats)]
     lib.sptrsv_solve.restype = C.c_int
     lib.sptrsv_solve_device_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -386,3 +389,23 @@ def partitioned_plan_for(l, partition, **kw) -> NativePlan:
 
 def env_device() -> int:
     return int(os.environ.get("SPTRSV_DEVICE", "0"))
+
+
+def coo_to_csc(n: int, rows, cols, vals, device: int | None = None):
+    """COO -> (col_ptr, row_idx, values) on the GPU: column-major, duplicates summed (mmio.py:132-144)."""
+    lib = require_gpu()
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    v = np.ascontiguousarray(vals, dtype=np.float64)
+    nnz = int(r.size)
+    col_ptr = np.empty(n + 1, dtype=np.int64)
+    row_idx = np.empty(max(nnz, 1), dtype=np.int64)
+    values = np.empty(max(nnz, 1), dtype=np.float64)
+    out_nnz = C.c_int64(0)
+    rc = lib.sptrsv_coo_to_csc(int(n), _ptr(r, C.c_int64), _ptr(c, C.c_int64), _ptr(v, C.c_double), nnz,
+                               env_device() if device is None else int(device), _ptr(col_ptr, C.c_int64),
+                               _ptr(row_idx, C.c_int64), _ptr(values, C.c_double), C.byref(out_nnz))
+    raise_for_status(rc, _err(lib))
+    k = int(out_nnz.value)
+    return col_ptr, row_idx[:k].copy(), values[:k].copy()
+
