@@ -1,0 +1,36 @@
+"""CPU: record emission in the reference's JSON-lines / CSV formats (row f2)."""
+
+from __future__ import annotations
+
+import csv
+import io
+import json
+
+from paper_2012_06959_b200 import records
+
+
+def _rec(**kw):
+    r = dict.fromkeys(records.FIELDS, 0)
+    r.update(name="m", engine="shared", max_rel_error=None, mean_wall_time=1.5e-3)
+    r.update(kw)
+    return r
+
+
+def test_fields_match_schema_order():
+    assert len(records.FIELDS) == 23 and records.FIELDS[:3] == ("name", "engine", "n")
+    assert records.FIELDS[-1] == "remote_updates"
+
+
+def test_emit_json_and_csv(tmp_path, capsys):
+    recs = [_rec(), _rec(name="k", engine="partitioned", max_rel_error=0.0)]
+    text = records.emit(recs, "json")
+    assert capsys.readouterr().out == text
+    lines = [json.loads(line) for line in text.splitlines()]
+    assert list(lines[0]) == list(records.FIELDS) and lines[0]["max_rel_error"] is None
+    out = tmp_path / "r.csv"
+    text = records.emit(recs, "csv", str(out))
+    assert out.read_text() == text
+    rows = list(csv.reader(io.StringIO(text)))
+    assert rows[0] == list(records.FIELDS)
+    assert rows[1][records.FIELDS.index("max_rel_error")] == ""  # null -> empty cell
+    assert rows[2][records.FIELDS.index("engine")] == "partitioned"
