@@ -466,6 +466,51 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   }
 }
 
+// Fast mode, 2 x 2 blocks (SPTRSV_ST_EXPAND=1, diagnostics): every element as an affine function of the four
+// inputs that arrive late (the two values above, by shuffle, and the two on
+// the left, from this lane's previous step), its coefficients products of
+// the block's own coefficients computed off the critical path. The bottom row
+// is then one (x10) and two (x11) FMAs behind the shuffle instead of two and
+// four. Same operations modulo re-association (fast mode's 1e-12 contract).
+#ifndef SPTRSV_ST_EXPAND
+#define SPTRSV_ST_EXPAND 0
+#endif
+// early shuffle (default): the next step's row above is shuffled as soon as
+// this step's bottom row exists and the look-ahead loads are issued at the top
+// of the step, which lets ptxas software-pipeline the loads under the FMA
+// chain (exact lap2d-4096: 1.46 -> 1.39 ms; fast unchanged). The expanded
+// block (SPTRSV_ST_EXPAND=1) halves the chain but adds 15 DP operations per
+// step and measured slower (fast 0.63 -> 0.70 ms): the step is bound by the
+// warp's instruction stream, not by the FMA chain.
+#ifndef SPTRSV_ST_EARLY_SHFL
+#define SPTRSV_ST_EARLY_SHFL 1
+#endif
+constexpr bool kStExpand = SPTRSV_ST_EXPAND && kStR == 2 && kStC == 2;
+constexpr bool kStEarlyShfl = SPTRSV_ST_EARLY_SHFL;
+
+template <bool EXACT>
+__device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double (&up)[kStC],
+                                             const double (&left)[kStR], double (&x)[kStR][kStC]) {
+  if constexpr (kStR == 2 && kStC == 2) {
+    const double *wu = b.wu, *wl = b.wl;
+    // right-hand sides of the block's own elimination (no late inputs)
+    const double k0 = __dmul_rn(b.bv[0], b.rd[0]);
+    const double k1 = __fma_rn(wl[1], k0, __dmul_rn(b.bv[1], b.rd[1]));
+    const double k2 = __fma_rn(wu[2], k0, __dmul_rn(b.bv[2], b.rd[2]));
+    const double k3 = __fma_rn(wu[3], k1, __fma_rn(wl[3], k2, __dmul_rn(b.bv[3], b.rd[3])));
+    // coefficients of (up0, up1, left0, left1)
+    const double a1 = __dmul_rn(wl[1], wu[0]), c1 = __dmul_rn(wl[1], wl[0]);
+    const double a2 = __dmul_rn(wu[2], wu[0]), c2 = __dmul_rn(wu[2], wl[0]);
+    const double a3 = __fma_rn(wu[3], a1, __dmul_rn(wl[3], a2)), b3 = __dmul_rn(wu[3], wu[1]);
+    const double c3 = __fma_rn(wu[3], c1, __dmul_rn(wl[3], c2)), d3 = __dmul_rn(wl[3], wl[2]);
+    // late inputs outermost: the shuffled values last
+    x[0][0] = __fma_rn(wu[0], up[0], __fma_rn(wl[0], left[0], k0));
+    x[0][1] = __fma_rn(a1, up[0], __fma_rn(wu[1], up[1], __fma_rn(c1, left[0], k1)));
+    x[1][0] = __fma_rn(a2, up[0], __fma_rn(c2, left[0], __fma_rn(wl[2], left[1], k2)));
+    x[1][1] = __fma_rn(a3, up[0], __fma_rn(b3, up[1], __fma_rn(c3, left[0], __fma_rn(d3, left[1], k3))));
+  }
+}
+
 // ---- warp 0: the lockstep wavefront -----------------------------------------
 // ABL: compile-time ablations for timing experiments only (0 in production):
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
@@ -485,15 +530,22 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   double xleft[kStR];
 #pragma unroll
   for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
-  double bottom[kStC];
+  double bottom[kStC], upv[kStC];
 #pragma unroll
-  for (int q = 0; q < kStC; ++q) bottom[q] = 0.0;
+  for (int q = 0; q < kStC; ++q) bottom[q] = upv[q] = 0.0;
 
   // step k of chunk c; `nxt` receives the next step's inputs
   // step k of chunk c computes from `cur` (loaded two steps earlier) and
   // loads step k + 2 into `nxt2`: a full step of slack hides the shared-memory
   // latency that a one-step lookahead leaves exposed
   auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt2) -> bool {
+    auto load_ahead = [&]() {
+      if (k + 2 < kStG) {
+        if (!(ABL & 2)) nxt2.load(smem, c % NB, k + 2, lane);
+      } else if (c + 1 < nchunks) {
+        nxt2.load(smem, (c + 1) % NB, k + 2 - kStG, lane);
+      }
+    };
     // the first step that loads from chunk c + 1: make sure it is ready
     if (k == kStG - 2 && c + 1 < nchunks && !solo) {
       if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
@@ -504,10 +556,11 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     const int s = c * kStG + k;
     const int j = s - lane;
     const bool active = j >= 0 && j < nblk;
+    if (kStEarlyShfl) load_ahead();
     double top[kStC];
 #pragma unroll
     for (int q = 0; q < kStC; ++q) {
-      const double up = (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
+      const double up = kStEarlyShfl ? upv[q] : (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
       top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
     }
     double xb[kStR][kStC];
@@ -551,7 +604,9 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       }
       return bad;
     };
-    if (solve_block(false) && EXACT) {
+    if (kStExpand && !EXACT) {
+      expand_block(cur, top, xleft, xb);
+    } else if (solve_block(false) && EXACT) {
       if (a.probe & 128) atomicAdd(&a.status->remote_reads, 1ull);  // diagnostics: count IEEE fallbacks
       solve_block(true);
     }
@@ -564,6 +619,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
 #pragma unroll
     for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
+    // early shuffle: the next step's row above enters the shared-memory
+    // pipe ahead of this step's stores and the look-ahead loads
+    if (kStEarlyShfl) {
+#pragma unroll
+      for (int q = 0; q < kStC; ++q) upv[q] = (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
+    }
     if (!(ABL & 8)) {
 #pragma unroll
       for (int q = 0; q < kStC; ++q)
@@ -580,11 +641,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
       for (int q = 0; q < kStC; q += 2)
         if (!(ABL & 1)) dst[st_b_piece(r, lane, k, q / 2)] = make_double2(xb[r][q], xb[r][q + 1]);
-    if (k + 2 < kStG) {
-      if (!(ABL & 2)) nxt2.load(smem, c % NB, k + 2, lane);
-    } else if (c + 1 < nchunks) {
-      nxt2.load(smem, (c + 1) % NB, k + 2 - kStG, lane);
-    }
+    if (!kStEarlyShfl) load_ahead();
     if (k == kStG - 1) {
       // chunk boundary: hand over the outputs and the input slot
       __syncwarp();

@@ -353,6 +353,14 @@ struct S3Blk {
   }
 };
 
+// early shuffle (as in stencil.cu): the next step's y-neighbours are
+// shuffled right after the block and the look-ahead loads issue at the top
+// of the step
+#ifndef SPTRSV_S3_EARLY_SHFL
+#define SPTRSV_S3_EARLY_SHFL 1
+#endif
+constexpr bool k3EarlyShfl = SPTRSV_S3_EARLY_SHFL;
+
 template <bool EXACT>
 __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane,
                            unsigned long long deadline) {
@@ -377,12 +385,13 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
     const int s = c * k3G + k;
     const int j = s - lane;
     const bool active = j >= 0 && j < nblk;
+    if (k3EarlyShfl && k + 1 < k3G) nxt.load(smem, c % NB, k + 1, lane);
     double yn[k3R][k3C];
 #pragma unroll
     for (int r = 0; r < k3R; ++r)
 #pragma unroll
       for (int q = 0; q < k3C; ++q) {
-        const double up = __shfl_up_sync(0xffffffffu, prev[r][q], 1);
+        const double up = k3EarlyShfl ? prev[r][q] : __shfl_up_sync(0xffffffffu, prev[r][q], 1);
         yn[r][q] = lane == 0 ? cur.yin[r][q] : up;
       }
     double xb[k3R][k3C];
@@ -422,7 +431,8 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
     for (int r = 0; r < k3R; ++r) {
       xleft[r] = xb[r][k3C - 1];
 #pragma unroll
-      for (int q = 0; q < k3C; ++q) prev[r][q] = xb[r][q];
+      for (int q = 0; q < k3C; ++q)
+        prev[r][q] = k3EarlyShfl ? __shfl_up_sync(0xffffffffu, xb[r][q], 1) : xb[r][q];
     }
 #pragma unroll
     for (int r = 0; r < k3R; ++r)
@@ -438,7 +448,7 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
     for (int r = 0; r < k3R; ++r) dst[r * k3Lanes] = make_double2(xb[r][0], xb[r][1]);
     if (a.dbg && lane == 0 && c == 0 && k == k3G - 1 && t < 192) a.dbg[2 * t + 1] = (long long)globaltimer_ns();
     if (k + 1 < k3G) {
-      nxt.load(smem, c % NB, k + 1, lane);
+      if (!k3EarlyShfl) nxt.load(smem, c % NB, k + 1, lane);
     } else {
       __syncwarp();
       if (lane == 0) {
