@@ -57,6 +57,13 @@ namespace {
 // p ^ (l & 7): the compute warp's 16-byte loads are conflict-free.
 constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
 
+// Speculative exact division (SPTRSV_ST_SPEC, default on): see compute().
+// Off, every step branches on its guard (exact lap2d-4096 1.38 ms; with
+// the guard ablated 0.81 ms).
+#ifndef SPTRSV_ST_SPEC
+#define SPTRSV_ST_SPEC 1
+#endif
+
 // Mailbox sentinel: a signalling NaN. FP64 arithmetic propagates NaN
 // payloads but always quiets them (tools/microbench/nan_bits.cu), so no
 // solved value can alias it and values are published without conversion.
@@ -527,12 +534,130 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks && !below_remote;
   const bool publish_sys = lane == kStLanes - 1 && below_remote;
   const bool solo = (a.probe & 32) != 0;  // diagnostics: run without the helper warps
+  constexpr bool kStSpec = EXACT && SPTRSV_ST_SPEC && kStC % 2 == 0;
   double xleft[kStR];
 #pragma unroll
   for (int r = 0; r < kStR; ++r) xleft[r] = 0.0;
   double bottom[kStC], upv[kStC];
 #pragma unroll
   for (int q = 0; q < kStC; ++q) bottom[q] = upv[q] = 0.0;
+
+  // One 2 x C block. exact: Markstein division with its operand-range guards
+  // folded into the returned flag (ieee: IEEE division); fast: pre-scaled FMAs.
+  auto block = [&](const StBlk<EXACT>& blk, const double (&top)[kStC], double (&xb)[kStR][kStC],
+                   bool ieee) -> bool {
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) {
+#pragma unroll
+      for (int q = 0; q < kStC; ++q) {
+        const int e = r * kStC + q;
+        const double up = r == 0 ? top[q] : xb[r - 1][q];
+        const double left = q == 0 ? xleft[r] : xb[r][q - 1];
+        if (EXACT) {
+          double acc = __dadd_rn(0.0, __dmul_rn(blk.wu[e], up));
+          acc = __dadd_rn(acc, __dmul_rn(blk.wl[e], left));
+          const double num = __dsub_rn(blk.bv[e], acc);
+          if (ieee) {
+            xb[r][q] = __ddiv_rn(num, blk.dd[e]);
+          } else {
+            const double qv = __dmul_rn(num, blk.rd[e]);
+            // a zero numerator is exact too (x = +-0 with the IEEE sign):
+            // the zero-filled steps before a lane's first block stay fast
+            // (bitwise, not short-circuit: no branch per element)
+            const int ok = (int)markstein_ok(blk.dd[e]) &
+                           ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+            bad |= !ok;
+            xb[r][q] = __fma_rn(__fma_rn(-qv, blk.dd[e], num), blk.rd[e], qv);
+          }
+        } else if (q == 0) {
+          // left comes from the previous step (early): the late operand
+          // (up, possibly straight off the shuffle) goes in the outer FMA
+          xb[r][q] = __fma_rn(blk.wu[e], up, __fma_rn(blk.wl[e], left, __dmul_rn(blk.bv[e], blk.rd[e])));
+        } else {
+          xb[r][q] = __fma_rn(blk.wl[e], left, __fma_rn(blk.wu[e], up, __dmul_rn(blk.bv[e], blk.rd[e])));
+        }
+      }
+    }
+    return bad;
+  };
+  // A solved block: carry its right column and bottom row, stage it for the
+  // storer. No select on `active`: steps before a lane's first block see zero
+  // coefficients, zero b (the loader zero-fills it) and zero neighbours, so
+  // they compute exact zeros -- the boundary values the first block needs;
+  // steps past the last block compute garbage that only ever reaches other
+  // past-the-end steps (never published, never stored).
+  auto retire = [&](int c, int k, const double (&xb)[kStR][kStC]) {
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
+#pragma unroll
+    for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
+    // early shuffle: the next step's row above enters the shared-memory
+    // pipe ahead of this step's stores and the look-ahead loads
+    if (kStEarlyShfl) {
+#pragma unroll
+      for (int q = 0; q < kStC; ++q) upv[q] = (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
+    }
+    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
+#pragma unroll
+    for (int r = 0; r < kStR; ++r)
+#pragma unroll
+      for (int q = 0; q < kStC; q += 2)
+        if (!(ABL & 1)) dst[st_b_piece(r, lane, k, q / 2)] = make_double2(xb[r][q], xb[r][q + 1]);
+  };
+  // Speculative exact mode (kStSpec): steps run Markstein unguarded and only
+  // accumulate the guard; a chunk in which any lane's guard failed is rolled
+  // back to its starting state and recomputed with IEEE division before its
+  // outputs and its band-below mailbox row leave the warp. Values are
+  // therefore published per chunk (one warp store from the staged outputs),
+  // which is also the poller's granularity.
+  bool spec_bad = false;
+  double sv_xleft[kStR], sv_bottom[kStC], sv_upv[kStC];
+  auto save_chunk_state = [&]() {
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) sv_xleft[r] = xleft[r];
+#pragma unroll
+    for (int q = 0; q < kStC; ++q) sv_bottom[q] = bottom[q], sv_upv[q] = upv[q];
+  };
+  auto redo_chunk = [&](int c) {
+    if ((a.probe & 128) && lane == 0) atomicAdd(&a.status->remote_reads, 1ull);  // diagnostics: count redos
+#pragma unroll
+    for (int r = 0; r < kStR; ++r) xleft[r] = sv_xleft[r];
+#pragma unroll
+    for (int q = 0; q < kStC; ++q) bottom[q] = sv_bottom[q], upv[q] = sv_upv[q];
+#pragma unroll 1
+    for (int k = 0; k < kStG; ++k) {
+      StBlk<EXACT> blk;
+      blk.load(smem, c % NB, k, lane);
+      double top[kStC], xb[kStR][kStC];
+#pragma unroll
+      for (int q = 0; q < kStC; ++q) {
+        const double up = kStEarlyShfl ? upv[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
+        top[q] = lane == 0 ? (has_above ? blk.inbox[q] : 0.0) : up;
+      }
+      block(blk, top, xb, true);
+      retire(c, k, xb);
+    }
+  };
+  // lane 31's bottom rows of chunk c, staged in the out ring, to the band below
+  auto publish_chunk = [&](int c) {
+    constexpr int kHalves = kStC / 2;
+    if (t + 1 >= a.n_tasks || lane >= kStG * kHalves) return;
+    const int k = lane / kHalves, h = lane % kHalves;
+    const int jj = c * kStG + k - (kStLanes - 1);
+    if (jj < 0 || jj >= nblk) return;
+    const double2 v = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) *
+                                                                            S::kOutChunk)[st_b_piece(
+        kStR - 1, kStLanes - 1, k, h)];
+    unsigned long long* w = below + (size_t)jj * kStC + 2 * h;
+    if (PART && below_remote) {
+      st_relaxed_sys_u64_if(w, as_u64(v.x), true);
+      st_relaxed_sys_u64_if(w + 1, as_u64(v.y), true);
+    } else {
+      st_relaxed_u64_if(w, as_u64(v.x), true);
+      st_relaxed_u64_if(w + 1, as_u64(v.y), true);
+    }
+  };
 
   // step k of chunk c; `nxt` receives the next step's inputs
   // step k of chunk c computes from `cur` (loaded two steps earlier) and
@@ -564,68 +689,17 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
     }
     double xb[kStR][kStC];
-    // exact: Markstein division for the whole block, with its operand-range
-    // guards folded into one flag; the rare lane whose guard fails (and the
-    // inactive edge steps, whose d is 0) redoes the block with IEEE division,
-    // so the block costs one branch instead of one per element
-    auto solve_block = [&](bool ieee) -> bool {
-      bool bad = false;
-#pragma unroll
-      for (int r = 0; r < kStR; ++r) {
-#pragma unroll
-        for (int q = 0; q < kStC; ++q) {
-          const int e = r * kStC + q;
-          const double up = r == 0 ? top[q] : xb[r - 1][q];
-          const double left = q == 0 ? xleft[r] : xb[r][q - 1];
-          if (EXACT) {
-            double acc = __dadd_rn(0.0, __dmul_rn(cur.wu[e], up));
-            acc = __dadd_rn(acc, __dmul_rn(cur.wl[e], left));
-            const double num = __dsub_rn(cur.bv[e], acc);
-            if (ieee) {
-              xb[r][q] = __ddiv_rn(num, cur.dd[e]);
-            } else {
-              const double qv = __dmul_rn(num, cur.rd[e]);
-              // a zero numerator is exact too (x = +-0 with the IEEE sign):
-              // the zero-filled steps before a lane's first block stay fast
-              // (bitwise, not short-circuit: no branch per element)
-              const int ok = (int)markstein_ok(cur.dd[e]) &
-                             ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
-              bad |= !ok;
-              xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
-            }
-          } else if (q == 0) {
-            // left comes from the previous step (early): the late operand
-            // (up, possibly straight off the shuffle) goes in the outer FMA
-            xb[r][q] = __fma_rn(cur.wu[e], up, __fma_rn(cur.wl[e], left, __dmul_rn(cur.bv[e], cur.rd[e])));
-          } else {
-            xb[r][q] = __fma_rn(cur.wl[e], left, __fma_rn(cur.wu[e], up, __dmul_rn(cur.bv[e], cur.rd[e])));
-          }
-        }
-      }
-      return bad;
-    };
     if (kStExpand && !EXACT) {
       expand_block(cur, top, xleft, xb);
-    } else if (solve_block(false) && EXACT) {
+    } else if (kStSpec) {
+      if (k == 0) save_chunk_state();
+      spec_bad |= block(cur, top, xb, false);
+    } else if (block(cur, top, xb, false) && EXACT) {
       if (a.probe & 128) atomicAdd(&a.status->remote_reads, 1ull);  // diagnostics: count IEEE fallbacks
-      solve_block(true);
+      block(cur, top, xb, true);
     }
-    // No select on `active`: steps before a lane's first block see zero
-    // coefficients, zero b (the loader zero-fills it) and zero neighbours, so
-    // they compute exact zeros -- the boundary values the first block needs;
-    // steps past the last block compute garbage that only ever reaches
-    // other past-the-end steps (never published, never stored).
-#pragma unroll
-    for (int r = 0; r < kStR; ++r) xleft[r] = xb[r][kStC - 1];
-#pragma unroll
-    for (int q = 0; q < kStC; ++q) bottom[q] = xb[kStR - 1][q];
-    // early shuffle: the next step's row above enters the shared-memory
-    // pipe ahead of this step's stores and the look-ahead loads
-    if (kStEarlyShfl) {
-#pragma unroll
-      for (int q = 0; q < kStC; ++q) upv[q] = (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
-    }
-    if (!(ABL & 8)) {
+    retire(c, k, xb);
+    if (!(ABL & 8) && !kStSpec) {
 #pragma unroll
       for (int q = 0; q < kStC; ++q)
         st_relaxed_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish && active);
@@ -635,14 +709,16 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
           st_relaxed_sys_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish_sys && active);
       }
     }
-    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % kStOutSlots) * S::kOutChunk);
-#pragma unroll
-    for (int r = 0; r < kStR; ++r)
-#pragma unroll
-      for (int q = 0; q < kStC; q += 2)
-        if (!(ABL & 1)) dst[st_b_piece(r, lane, k, q / 2)] = make_double2(xb[r][q], xb[r][q + 1]);
     if (!kStEarlyShfl) load_ahead();
     if (k == kStG - 1) {
+      if (kStSpec) {
+        // a guard failed somewhere in this chunk: recompute it with IEEE
+        // division (rare: operands outside Markstein's exponent window)
+        if (__any_sync(0xffffffffu, spec_bad)) redo_chunk(c);
+        spec_bad = false;
+        __syncwarp();
+        publish_chunk(c);
+      }
       // chunk boundary: hand over the outputs and the input slot
       __syncwarp();
       if (lane == 0) {

@@ -230,6 +230,37 @@ def test_stencil_executor_matches_oracle(shape, precision):
     plan.close()
 
 
+@pytest.mark.parametrize("shape", [(64, 64), (256, 130)])
+def test_stencil_exact_guard_redo(shape):
+    """Operands outside Markstein's exponent window (tiny / huge b, tiny
+    diagonals) fail the division guard inside some chunks: the speculative
+    exact stencil must roll those chunks back and recompute them with IEEE
+    division, bit-identical to the serial oracle (and count the redos)."""
+    nx, ny = shape
+    l = _random_coefficients(synth.lap2d(nx, ny), 7 * nx + ny)
+    rng = np.random.default_rng(nx + ny)
+    b = rng.uniform(-1.0, 1.0, l.n)
+    hot = rng.choice(l.n, size=max(4, l.n // 500), replace=False)
+    b[hot[0::3]] *= 1e-310  # subnormal numerators
+    b[hot[1::3]] *= 1e300   # huge numerators
+    vals = l.values.copy()
+    diag = l.row_idx == l.entry_columns()
+    dpos = np.flatnonzero(diag)[hot[2::3]]
+    vals[dpos] *= 1e-300    # tiny diagonals: huge quotients
+    l = sp.CscMatrix(n=l.n, col_ptr=l.col_ptr, row_idx=l.row_idx, values=vals)
+    with np.errstate(all="ignore"):
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor="stencil",
+                              probe_flags=128)
+    for _ in range(2):
+        x, st = plan.solve(b)
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(x), nan)
+        assert x[~nan].tobytes() == ref[~nan].tobytes()
+    assert st["remote_reads"] > 0  # probe 128: chunks recomputed with IEEE division
+    plan.close()
+
+
 def test_stencil_not_chosen_for_other_structures():
     l = synth.lap2d(31, 10)  # nx not a multiple of the column block: general executors
     plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="auto")
