@@ -75,6 +75,7 @@ struct S3Args {
   int nx, ny, nz, nyt, nzt, n_tasks, steps;
   int b_aligned, x_aligned;  // 16-byte vector paths (else 8-byte halves)
   long long* dbg;            // diagnostics (probe_flags & 16): per-task globaltimer [start, ready, end]
+  int probe;                 // diagnostics flags (probe_flags; 128: count exact-mode chunk redos)
   unsigned long long* ymail_next;  // the other mailbox halves: the storer resets each tile's part
   unsigned long long* zmail_next;  // for the next solve
 };
@@ -360,6 +361,9 @@ struct S3Blk {
 #define SPTRSV_S3_EARLY_SHFL 1
 #endif
 constexpr bool k3EarlyShfl = SPTRSV_S3_EARLY_SHFL;
+#ifndef SPTRSV_S3_SPEC
+#define SPTRSV_S3_SPEC 1
+#endif
 
 template <bool EXACT>
 __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t, int lane,
@@ -374,6 +378,7 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
   unsigned long long* zpub = a.zmail + ((size_t)t * k3Lanes + lane) * a.nx;
   const bool pub_y = lane == k3Lanes - 1 && Y + 1 < a.nyt;
   const bool pub_z = Z + 1 < a.nzt;
+  constexpr bool k3Spec = EXACT && SPTRSV_S3_SPEC && k3C == 2;
   double xleft[k3R], prev[k3R][k3C];
 #pragma unroll
   for (int r = 0; r < k3R; ++r) {
@@ -381,6 +386,115 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
 #pragma unroll
     for (int q = 0; q < k3C; ++q) prev[r][q] = 0.0;
   }
+  // one 4 x 2 block (exact: Markstein with its guard folded into the
+  // returned flag, or IEEE division; fast: pre-scaled FMAs)
+  auto block = [&](const S3Blk<EXACT>& blk, const double (&yn)[k3R][k3C], double (&xb)[k3R][k3C],
+                   bool ieee) -> bool {
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) {
+        const int e = r * k3C + q;
+        const double zn = r == 0 ? blk.zin[q] : xb[r - 1][q];
+        const double left = q == 0 ? xleft[r] : xb[r][q - 1];
+        if (EXACT) {
+          double acc = __dadd_rn(0.0, __dmul_rn(blk.wz[e], zn));
+          acc = __dadd_rn(acc, __dmul_rn(blk.wy[e], yn[r][q]));
+          acc = __dadd_rn(acc, __dmul_rn(blk.wx[e], left));
+          const double num = __dsub_rn(blk.bv[e], acc);
+          if (ieee) {
+            xb[r][q] = __ddiv_rn(num, blk.dd[e]);
+          } else {
+            const double qv = __dmul_rn(num, blk.rd[e]);
+            const int ok = (int)markstein_ok(blk.dd[e]) &
+                           ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+            bad |= !ok;
+            xb[r][q] = __fma_rn(__fma_rn(-qv, blk.dd[e], num), blk.rd[e], qv);
+          }
+        } else {
+          const double inner = __fma_rn(blk.wz[e], zn, __fma_rn(blk.wx[e], left, __dmul_rn(blk.bv[e], blk.rd[e])));
+          xb[r][q] = __fma_rn(blk.wy[e], yn[r][q], inner);
+        }
+      }
+    }
+    return bad;
+  };
+  // a solved block: carry its right column and (shuffled) rows, stage it
+  auto retire = [&](int c, int k, const double (&xb)[k3R][k3C]) {
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      xleft[r] = xb[r][k3C - 1];
+#pragma unroll
+      for (int q = 0; q < k3C; ++q)
+        prev[r][q] = k3EarlyShfl ? __shfl_up_sync(0xffffffffu, xb[r][q], 1) : xb[r][q];
+    }
+    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk) + k * k3Pairs * k3Lanes +
+                   lane;
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) dst[r * k3Lanes] = make_double2(xb[r][0], xb[r][1]);
+  };
+  // Speculative exact mode (as in stencil.cu): guards accumulate per chunk; a
+  // chunk with a failed guard is rolled back and recomputed with IEEE
+  // division before its outputs and mailbox words leave the warp, so both
+  // mailboxes are published per chunk from the staged outputs.
+  bool spec_bad = false;
+  double sv_xleft[k3R], sv_prev[k3R][k3C];
+  auto save_chunk_state = [&]() {
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      sv_xleft[r] = xleft[r];
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) sv_prev[r][q] = prev[r][q];
+    }
+  };
+  auto redo_chunk = [&](int c) {
+    if ((a.probe & 128) && lane == 0) atomicAdd(&a.status->remote_reads, 1ull);  // diagnostics: count redos
+#pragma unroll
+    for (int r = 0; r < k3R; ++r) {
+      xleft[r] = sv_xleft[r];
+#pragma unroll
+      for (int q = 0; q < k3C; ++q) prev[r][q] = sv_prev[r][q];
+    }
+#pragma unroll 1
+    for (int k = 0; k < k3G; ++k) {
+      S3Blk<EXACT> blk;
+      blk.load(smem, c % NB, k, lane);
+      double yn[k3R][k3C], xb[k3R][k3C];
+#pragma unroll
+      for (int r = 0; r < k3R; ++r)
+#pragma unroll
+        for (int q = 0; q < k3C; ++q) {
+          const double up = k3EarlyShfl ? prev[r][q] : __shfl_up_sync(0xffffffffu, prev[r][q], 1);
+          yn[r][q] = lane == 0 ? blk.yin[r][q] : up;
+        }
+      block(blk, yn, xb, true);
+      retire(c, k, xb);
+    }
+  };
+  auto publish_chunk = [&](int c) {
+    const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk);
+    // y: lane 31's rows, one (step, row) per lane
+    if (Y + 1 < a.nyt && lane < k3G * k3R) {
+      const int k = lane / k3R, r = lane % k3R, jj = c * k3G + k - (k3Lanes - 1);
+      if (jj >= 0 && jj < nblk) {
+        const double2 v = src[(k * k3Pairs + r) * k3Lanes + k3Lanes - 1];
+        unsigned long long* w = ypub + (size_t)r * a.nx + (size_t)jj * k3C;
+        st_relaxed_u64_if(w, as_u64(v.x), true);
+        st_relaxed_u64_if(w + 1, as_u64(v.y), true);
+      }
+    }
+    // z: every lane's last plane
+    if (pub_z) {
+#pragma unroll
+      for (int k = 0; k < k3G; ++k) {
+        const int jj = c * k3G + k - lane;
+        const double2 v = src[(k * k3Pairs + k3R - 1) * k3Lanes + lane];
+        st_relaxed_u64_if(zpub + (size_t)jj * k3C, as_u64(v.x), jj >= 0 && jj < nblk);
+        st_relaxed_u64_if(zpub + (size_t)jj * k3C + 1, as_u64(v.y), jj >= 0 && jj < nblk);
+      }
+    }
+  };
   auto step = [&](int c, int k, const S3Blk<EXACT>& cur, S3Blk<EXACT>& nxt) -> bool {
     const int s = c * k3G + k;
     const int j = s - lane;
@@ -395,61 +509,34 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
         yn[r][q] = lane == 0 ? cur.yin[r][q] : up;
       }
     double xb[k3R][k3C];
-    auto solve_block = [&](bool ieee) -> bool {
-      bool bad = false;
-#pragma unroll
-      for (int r = 0; r < k3R; ++r) {
-#pragma unroll
-        for (int q = 0; q < k3C; ++q) {
-          const int e = r * k3C + q;
-          const double zn = r == 0 ? cur.zin[q] : xb[r - 1][q];
-          const double left = q == 0 ? xleft[r] : xb[r][q - 1];
-          if (EXACT) {
-            double acc = __dadd_rn(0.0, __dmul_rn(cur.wz[e], zn));
-            acc = __dadd_rn(acc, __dmul_rn(cur.wy[e], yn[r][q]));
-            acc = __dadd_rn(acc, __dmul_rn(cur.wx[e], left));
-            const double num = __dsub_rn(cur.bv[e], acc);
-            if (ieee) {
-              xb[r][q] = __ddiv_rn(num, cur.dd[e]);
-            } else {
-              const double qv = __dmul_rn(num, cur.rd[e]);
-              const int ok = (int)markstein_ok(cur.dd[e]) &
-                             ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
-              bad |= !ok;
-              xb[r][q] = __fma_rn(__fma_rn(-qv, cur.dd[e], num), cur.rd[e], qv);
-            }
-          } else {
-            const double inner = __fma_rn(cur.wz[e], zn, __fma_rn(cur.wx[e], left, __dmul_rn(cur.bv[e], cur.rd[e])));
-            xb[r][q] = __fma_rn(cur.wy[e], yn[r][q], inner);
-          }
-        }
-      }
-      return bad;
-    };
-    if (solve_block(false) && EXACT) solve_block(true);
-#pragma unroll
-    for (int r = 0; r < k3R; ++r) {
-      xleft[r] = xb[r][k3C - 1];
-#pragma unroll
-      for (int q = 0; q < k3C; ++q)
-        prev[r][q] = k3EarlyShfl ? __shfl_up_sync(0xffffffffu, xb[r][q], 1) : xb[r][q];
+    if (k3Spec) {
+      if (k == 0) save_chunk_state();
+      spec_bad |= block(cur, yn, xb, false);
+    } else if (block(cur, yn, xb, false) && EXACT) {
+      block(cur, yn, xb, true);
     }
+    retire(c, k, xb);
+    if (!k3Spec) {
 #pragma unroll
-    for (int r = 0; r < k3R; ++r)
+      for (int r = 0; r < k3R; ++r)
+#pragma unroll
+        for (int q = 0; q < k3C; ++q)
+          st_relaxed_u64_if(ypub + (size_t)r * a.nx + (size_t)j * k3C + q, as_u64(xb[r][q]), pub_y && active);
 #pragma unroll
       for (int q = 0; q < k3C; ++q)
-        st_relaxed_u64_if(ypub + (size_t)r * a.nx + (size_t)j * k3C + q, as_u64(xb[r][q]), pub_y && active);
-#pragma unroll
-    for (int q = 0; q < k3C; ++q)
-      st_relaxed_u64_if(zpub + (size_t)j * k3C + q, as_u64(xb[k3R - 1][q]), pub_z && active);
-    double2* dst = reinterpret_cast<double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk) + k * k3Pairs * k3Lanes +
-                   lane;
-#pragma unroll
-    for (int r = 0; r < k3R; ++r) dst[r * k3Lanes] = make_double2(xb[r][0], xb[r][1]);
+        st_relaxed_u64_if(zpub + (size_t)j * k3C + q, as_u64(xb[k3R - 1][q]), pub_z && active);
+    }
     if (a.dbg && lane == 0 && c == 0 && k == k3G - 1 && t < 192) a.dbg[2 * t + 1] = (long long)globaltimer_ns();
     if (k + 1 < k3G) {
       if (!k3EarlyShfl) nxt.load(smem, c % NB, k + 1, lane);
     } else {
+      if (k3Spec) {
+        // a guard failed somewhere in this chunk: recompute it with IEEE division
+        if (__any_sync(0xffffffffu, spec_bad)) redo_chunk(c);
+        spec_bad = false;
+        __syncwarp();
+        publish_chunk(c);
+      }
       __syncwarp();
       if (lane == 0) {
         st_release_cta(ctl + kC3OutReady, c + 1);
@@ -684,6 +771,7 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s) 
   a.status = status;
   a.abort_flag = abort_flag;
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  a.probe = opt.probe_flags;
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.nx = P.nx, a.ny = P.ny, a.nz = P.nz, a.nyt = P.nyt, a.nzt = P.nzt;

@@ -230,14 +230,15 @@ def test_stencil_executor_matches_oracle(shape, precision):
     plan.close()
 
 
-@pytest.mark.parametrize("shape", [(64, 64), (256, 130)])
+@pytest.mark.parametrize("shape", [(64, 64), (256, 130), (16, 40, 9)])
 def test_stencil_exact_guard_redo(shape):
     """Operands outside Markstein's exponent window (tiny / huge b, tiny
     diagonals) fail the division guard inside some chunks: the speculative
     exact stencil must roll those chunks back and recompute them with IEEE
     division, bit-identical to the serial oracle (and count the redos)."""
-    nx, ny = shape
-    l = _random_coefficients(synth.lap2d(nx, ny), 7 * nx + ny)
+    nx, ny = shape[:2]
+    grid = synth.lap2d(nx, ny) if len(shape) == 2 else synth.lap3d(*shape)
+    l = _random_coefficients(grid, 7 * nx + ny)
     rng = np.random.default_rng(nx + ny)
     b = rng.uniform(-1.0, 1.0, l.n)
     hot = rng.choice(l.n, size=max(4, l.n // 500), replace=False)
