@@ -562,11 +562,14 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
             xb[r][q] = __ddiv_rn(num, blk.dd[e]);
           } else {
             const double qv = __dmul_rn(num, blk.rd[e]);
-            // a zero numerator is exact too (x = +-0 with the IEEE sign):
-            // the zero-filled steps before a lane's first block stay fast
+            // a +0 numerator is exact too (x = qv + 0 = +-0 with the IEEE
+            // sign), so the zero-filled steps before a lane's first block
+            // stay fast; -0 is not (qv = -0 for d > 0, but r = +0 and
+            // x = +0 + -0 = +0): it takes the IEEE path
             // (bitwise, not short-circuit: no branch per element)
             const int ok = (int)markstein_ok(blk.dd[e]) &
-                           ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+                           (((int)(num == 0.0) & (int)(__double2hiint(num) == 0)) |
+                            ((int)markstein_ok(qv) & (int)markstein_ok(num)));
             bad |= !ok;
             xb[r][q] = __fma_rn(__fma_rn(-qv, blk.dd[e], num), blk.rd[e], qv);
           }

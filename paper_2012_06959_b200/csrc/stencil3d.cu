@@ -408,7 +408,8 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
           } else {
             const double qv = __dmul_rn(num, blk.rd[e]);
             const int ok = (int)markstein_ok(blk.dd[e]) &
-                           ((int)(num == 0.0) | ((int)markstein_ok(qv) & (int)markstein_ok(num)));
+                           (((int)(num == 0.0) & (int)(__double2hiint(num) == 0)) |
+                            ((int)markstein_ok(qv) & (int)markstein_ok(num)));  // +0 only: see stencil.cu
             bad |= !ok;
             xb[r][q] = __fma_rn(__fma_rn(-qv, blk.dd[e], num), blk.rd[e], qv);
           }

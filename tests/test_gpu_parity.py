@@ -262,6 +262,22 @@ def test_stencil_exact_guard_redo(shape):
     plan.close()
 
 
+@pytest.mark.parametrize("dims", [(64, 70), (16, 40, 9)])
+def test_stencil_exact_signed_zeros(dims):
+    """b of +0 / -0 only: every x is a signed zero, and the sign depends on
+    the oracle's s = 0 + ... accumulation order (IEEE -0 + -0 = -0 but
+    (0 + -0) + -0 = +0) — bitwise parity on the 2D and 3D stencils."""
+    grid = synth.lap2d(*dims) if len(dims) == 2 else synth.lap3d(*dims)
+    rng = np.random.default_rng(len(dims))
+    b = np.where(rng.random(grid.n) < 0.5, -0.0, 0.0)
+    ref = oracle.solve_serial(grid.col_ptr, grid.row_idx, grid.values, b)
+    assert np.signbit(ref).any() and (~np.signbit(ref)).any()
+    plan = _native.NativePlan(grid.col_ptr, grid.row_idx, grid.values, grid.n, precision="exact", executor="stencil")
+    x, _ = plan.solve(b)
+    assert x.tobytes() == ref.tobytes()
+    plan.close()
+
+
 def test_stencil_not_chosen_for_other_structures():
     l = synth.lap2d(31, 10)  # nx not a multiple of the column block: general executors
     plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="auto")
