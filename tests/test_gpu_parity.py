@@ -278,6 +278,21 @@ def test_stencil_exact_signed_zeros(dims):
     plan.close()
 
 
+@pytest.mark.parametrize("executor", ["rows", "chains", "band"])
+def test_signed_zero_rhs_general_executors(executor):
+    """The same signed-zero bar for the general executors (their division is
+    div_exact, whose window check sends zero numerators to IEEE division)."""
+    l = synth.banded(3000, 64, 0.5, seed=3) if executor == "band" else synth.lap2d(31, 40)
+    rng = np.random.default_rng(5)
+    b = np.where(rng.random(l.n) < 0.5, -0.0, 0.0)
+    b[rng.choice(l.n, 20, replace=False)] = 1.0  # a few nonzero sources
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="exact", executor=executor)
+    x, _ = plan.solve(b)
+    assert x.tobytes() == ref.tobytes()
+    plan.close()
+
+
 def test_stencil_not_chosen_for_other_structures():
     l = synth.lap2d(31, 10)  # nx not a multiple of the column block: general executors
     plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor="auto")
