@@ -244,6 +244,8 @@ def test_stencil_exact_guard_redo(shape):
     hot = rng.choice(l.n, size=max(4, l.n // 500), replace=False)
     b[hot[0::3]] *= 1e-310  # subnormal numerators
     b[hot[1::3]] *= 1e300   # huge numerators
+    b[hot[1]] = np.inf      # non-finite numerators propagate like IEEE
+    b[hot[4]] = np.nan
     vals = l.values.copy()
     diag = l.row_idx == l.entry_columns()
     dpos = np.flatnonzero(diag)[hot[2::3]]
