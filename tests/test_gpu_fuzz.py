@@ -55,3 +55,39 @@ def test_random_sweep(seed):
         x, _ = plan.solve(b)
         plan.close()
         assert sp.compare_solutions(x, ref, TOL).within_tol, (seed, executor, precision)
+
+
+def _random_coefficients(l, seed):
+    """Random off-diagonals, diagonally dominant diagonal of random sign."""
+    rng = np.random.default_rng(seed)
+    vals = l.values.copy()
+    off = l.row_idx != l.entry_columns()
+    vals[off] = rng.uniform(-1.0, 1.0, off.sum())
+    dom = 1.0 + np.bincount(l.row_idx[off], weights=np.abs(vals[off]), minlength=l.n)
+    vals[~off] = np.where(rng.random(l.n) < 0.5, -1.0, 1.0) * dom
+    return sp.CscMatrix(n=l.n, col_ptr=l.col_ptr, row_idx=l.row_idx, values=vals)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_stencil_grids(seed):
+    """Random 2D / 3D grid sizes (the stencil executors when the shape allows)."""
+    rng = np.random.default_rng(2000 + seed)
+    if seed % 2 == 0:
+        grid = synth.lap2d(2 * int(rng.integers(1, 160)), int(rng.integers(1, 300)))
+    else:
+        grid = synth.lap3d(2 * int(rng.integers(1, 24)), int(rng.integers(1, 70)), int(rng.integers(1, 12)))
+    l = _random_coefficients(grid, seed)
+    b = rng.uniform(-1.0, 1.0, l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    used = set()
+    for precision in ("exact", "fast"):
+        plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil")
+        used.add(plan.info()["executor"])
+        for _ in range(2):
+            x, _ = plan.solve(b)
+            if precision == "exact":
+                assert x.tobytes() == ref.tobytes(), (seed, plan.info()["executor"])
+            else:
+                assert sp.compare_solutions(x, ref, TOL).within_tol, (seed, plan.info()["executor"])
+        plan.close()
+    assert used == {"stencil"}
