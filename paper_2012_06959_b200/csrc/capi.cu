@@ -362,19 +362,14 @@ int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st
   const unsigned ep = ++stencil.epoch;
   const long long band = (long long)kStBand * stencil.nx;
   const int nt = stencil.n_tasks;
-  CUDA_TRY(cudaEventRecord(ev0, stream));
-  int rc = solve_stencil(bbuf, xbuf, stream, true, true);
-  if (rc != SPTRSV_OK) return rc;
-  CUDA_TRY(cudaEventRecord(ev1, stream));
-  pending = true;
-  for (int t = 0; t < nt; ++t)
-    if (g_write32(stream, (unsigned long long)(stencil.xflag + t), ep, 0) != 0)
-      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
   // Copy granularity (bands per copy): b goes in doubling chunks (1, 2, 4
   // bands: the first band starts the kernel early, bigger copies keep the link
   // efficient); x comes out 2 bands at a time. Tunable by SPTRSV_STREAM_IN /
   // SPTRSV_STREAM_OUT (tools/e2e_sweep.sh: 4.3-4.8 ms over 1..32 bands per copy
   // on lap2d-4096 — the PCIe link shared by both directions is the limit).
+  // One stream memory operation per copy, not per band: each one costs the
+  // copy stream a gap (64 flag writes + 64 waits + 64 post-kernel writes were
+  // ~1 ms of a 4.3 ms solve).
   static const int in_max = [] {
     const char* e = std::getenv("SPTRSV_STREAM_IN");
     return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
@@ -383,18 +378,25 @@ int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st
     const char* e = std::getenv("SPTRSV_STREAM_OUT");
     return e && std::atoi(e) > 0 ? std::atoi(e) : 2;
   }();
+  stencil.b_chunk_max = in_max;
+  CUDA_TRY(cudaEventRecord(ev0, stream));
+  int rc = solve_stencil(bbuf, xbuf, stream, true, true);
+  if (rc != SPTRSV_OK) return rc;
+  CUDA_TRY(cudaEventRecord(ev1, stream));
+  pending = true;
+  // never leave the x copies waiting if the kernel stopped early
+  CUDA_TRY(stencil_release_flags(stencil.xflag, nt, ep, stream));
   for (int t0b = 0, w = 1; t0b < nt; t0b += w, w = std::min(2 * w, in_max)) {
     const int t1b = std::min(nt, t0b + w);
     const long long off = t0b * band, cnt = std::min(band * (t1b - t0b), n - off);
     CUDA_TRY(cudaMemcpyAsync(bbuf + off, b + off, sizeof(double) * cnt, cudaMemcpyHostToDevice, cs_in));
-    for (int t = t0b; t < t1b; ++t)
-      if (g_write32(cs_in, (unsigned long long)(stencil.bflag + t), ep, 0) != 0)
-        return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
+    if (g_write32(cs_in, (unsigned long long)(stencil.bflag + t1b - 1), ep, 0) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
   }
   for (int t0b = 0; t0b < nt; t0b += out_n) {
     const int t1b = std::min(nt, t0b + out_n);
     const long long off = t0b * band, cnt = std::min(band * (t1b - t0b), n - off);
-    for (int t = t0b; t < t1b; ++t)
+    for (int t = SPTRSV_ST_XFLAG_ORDER ? t1b - 1 : t0b; t < t1b; ++t)
       if (g_wait32(cs_out, (unsigned long long)(stencil.xflag + t), ep, kWaitGeq) != 0)
         return fail(SPTRSV_E_CUDA, "cuStreamWaitValue32 failed");
     CUDA_TRY(cudaMemcpyAsync(x + off, xbuf + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, cs_out));

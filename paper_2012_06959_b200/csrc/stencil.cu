@@ -63,6 +63,12 @@ constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
 #ifndef SPTRSV_ST_SPEC
 #define SPTRSV_ST_SPEC 1
 #endif
+// x leaves interior chunks by one TMA tensor store (SPTRSV_ST_X_TMA=1) or by
+// the storer's 16-byte stores (default): measured the same on lap2d-4096
+#ifndef SPTRSV_ST_X_TMA
+#define SPTRSV_ST_X_TMA 0
+#endif
+
 
 // Mailbox sentinel: a signalling NaN. FP64 arithmetic propagates NaN
 // payloads but always quiets them (tools/microbench/nan_bits.cu), so no
@@ -95,6 +101,7 @@ struct alignas(64) StArgs {
   const unsigned* bflag;
   unsigned* xflag;
   unsigned epoch;
+  int b_chunk_max;  // bflag is written for the last band of each doubling chunk only (0: every band)
   // PE partition (stencil.hpp): tickets index my_tasks (null: ticket = band);
   // mbox is this PE's mailbox half of this solve, peers' halves are
   // pe_mbox[owner] + mbox_half
@@ -324,7 +331,16 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // overlapped host solve: this band's b may still be on its way over PCIe
   if (a.bflag) {
     int polls = 0;
-    while ((int)(ld_acquire_sys_u32(a.bflag + t) - a.epoch) < 0) {
+    // the copy stream flags the last band of each chunk (1, 2, 4, ... bands)
+    int flag_band = t;
+    if (a.b_chunk_max > 0) {
+      for (int t0b = 0, w = 1;; t0b += w, w = min(2 * w, a.b_chunk_max))
+        if (t < t0b + w) {
+          flag_band = min(a.n_tasks, t0b + w) - 1;
+          break;
+        }
+    }
+    while ((int)(ld_acquire_sys_u32(a.bflag + flag_band) - a.epoch) < 0) {
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
       if (!__all_sync(0xffffffffu, ok)) {
         abort_task(a, ctl, lane);
@@ -466,9 +482,17 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
   }
   if (x_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
-  // overlapped host solve: band t's x may now be copied to the host
+  // overlapped host solve: band t's x may now be copied to the host. Flags
+  // are raised in band order (after band t - 1's), so the copy stream waits
+  // on the last band of each copy only
   if (a.xflag && lane == 0) {
     __threadfence_system();
+    int polls = 0;
+    while (SPTRSV_ST_XFLAG_ORDER && t > 0 && (int)(ld_acquire_sys_u32(a.xflag + t - 1) - a.epoch) < 0) {
+      if (ld_relaxed_s32(a.abort_flag)) break;  // the flags are released after the kernel anyway
+      if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) break;
+      __nanosleep(64);
+    }
     st_release_sys_u32(a.xflag + t, a.epoch);
   }
 }
@@ -969,6 +993,11 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
       (e = cudaMemset(stencil.bflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
       (e = cudaMemset(stencil.xflag, 0, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // load the flag-release kernel now: under lazy module loading its first
+  // launch would otherwise wait for the device while the solve kernel spins
+  // on b flags that only later copies write (a deadlock until the watchdog)
+  if ((e = stencil_release_flags(stencil.xflag, stencil.n_tasks, 0u, stream)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   // the coefficient stream is packed on the device from the CSR (one thread
   // per lane-step, no host round trip of the values)
   {
@@ -984,6 +1013,17 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
   stencil.ready = true;
   stencil.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return SPTRSV_OK;
+}
+
+// Streamed host solves: after the kernel, every band's x flag is set to the
+// epoch (one launch), so a copy stream waiting on them never hangs when the
+// kernel stopped early (timeout / abort); normally the storers already did.
+__global__ void k_set_flags(unsigned* f, int n, unsigned v) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) st_release_sys_u32(f + i, v);
+}
+cudaError_t stencil_release_flags(unsigned* f, int n, unsigned v, cudaStream_t s) {
+  k_set_flags<<<1, 128, 0, s>>>(f, n, v);
+  return cudaGetLastError();
 }
 
 int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags) {
@@ -1029,11 +1069,12 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
   a.b_tma_bands = (kStBTma && a.b_aligned) ? encode_b_map(&a.bmap, d_b, stencil.nx, stencil.ny) : 0;
-  a.x_tma_bands = (kStBTma && a.x_aligned) ? encode_b_map(&a.xmap, d_x, stencil.nx, stencil.ny) : 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
+  a.x_tma_bands = (SPTRSV_ST_X_TMA && kStBTma && a.x_aligned) ? encode_b_map(&a.xmap, d_x, stencil.nx, stencil.ny) : 0;
   if (b_flags) a.bflag = stencil.bflag;
   if (x_flags) a.xflag = stencil.xflag;
   a.epoch = stencil.epoch;
+  a.b_chunk_max = b_flags ? stencil.b_chunk_max : 0;
   a.nap = (opt.probe_flags & 4) ? (opt.probe_flags >> 8) & 1023 : 64;  // probe bit 4: override the nap
   if (opt.probe_flags & 16) {
     if (!probe_buf && cudaMalloc((void**)&probe_buf, sizeof(long long) * kProbeWords) != cudaSuccess)

@@ -62,6 +62,9 @@ struct StencilPlan {
   unsigned* bflag = nullptr;  // [n_tasks]
   unsigned* xflag = nullptr;  // [n_tasks]
   unsigned epoch = 0;
+  // b arrives in chunks of bands (1, 2, 4, ... up to b_chunk_max): only the
+  // last band of a chunk gets a flag write, the loader derives it (0: per band)
+  int b_chunk_max = 0;
   // Mailboxes are double-buffered by solve parity ([2][n_tasks][nx]): solve k
   // reads and writes half k % 2 and resets the other half for solve k + 1, so
   // a PE never resets a half a peer may still be reading (consecutive solves
@@ -132,5 +135,14 @@ struct Stencil3Plan {
     *this = Stencil3Plan();
   }
 };
+
+// x flags raised in band order (the storer of band t waits for band t - 1's
+// flag first), so the host copy stream waits once per copy, on its last band
+#ifndef SPTRSV_ST_XFLAG_ORDER
+#define SPTRSV_ST_XFLAG_ORDER 1
+#endif
+
+// sets f[0..n) = v with system-scope release stores (one launch)
+cudaError_t stencil_release_flags(unsigned* f, int n, unsigned v, cudaStream_t s);
 
 }  // namespace sptrsv
