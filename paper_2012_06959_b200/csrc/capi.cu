@@ -362,17 +362,19 @@ int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st
   const unsigned ep = ++stencil.epoch;
   const long long band = (long long)kStBand * stencil.nx;
   const int nt = stencil.n_tasks;
-  // Copy granularity (bands per copy): b goes in doubling chunks (1, 2, 4
+  // Copy granularity (bands per copy): b goes in doubling chunks (1, 2, 4, 8
   // bands: the first band starts the kernel early, bigger copies keep the link
   // efficient); x comes out 2 bands at a time. Tunable by SPTRSV_STREAM_IN /
-  // SPTRSV_STREAM_OUT (tools/e2e_sweep.sh: 4.3-4.8 ms over 1..32 bands per copy
-  // on lap2d-4096 — the PCIe link shared by both directions is the limit).
+  // SPTRSV_STREAM_OUT (lap2d-4096: 3.8-4.4 ms over 1..16 bands per copy, also
+  // with big x copies until the tail; the PCIe link shared by both directions
+  // is the limit: 3.3 ms for the same copy pattern without the solve,
+  // tools/pcie_pattern.py).
   // One stream memory operation per copy, not per band: each one costs the
   // copy stream a gap (64 flag writes + 64 waits + 64 post-kernel writes were
   // ~1 ms of a 4.3 ms solve).
   static const int in_max = [] {
     const char* e = std::getenv("SPTRSV_STREAM_IN");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : 4;
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
   }();
   static const int out_n = [] {
     const char* e = std::getenv("SPTRSV_STREAM_OUT");
