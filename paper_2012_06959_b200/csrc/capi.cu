@@ -330,7 +330,7 @@ constexpr unsigned kWaitGeq = 0;  // CU_STREAM_WAIT_VALUE_GEQ
 bool DevicePlan::streamed_io_ok() const {
   return executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !stencil.part &&
          !(opt.flags & SPTRSV_PLAN_NO_STREAMED_IO) &&
-         stencil.bflag && stream_memops();
+         (stencil3.ready ? stencil3.bflag != nullptr : stencil.bflag != nullptr) && stream_memops();
 }
 
 // Pinned host memory (cudaHostAlloc / cudaHostRegister under UVA): the whole
@@ -355,9 +355,61 @@ static bool device_mapped_host(const void* p, size_t bytes) {
 // kernel's xflag[t] >= epoch and copies that slice of x out. After the kernel
 // the solve stream writes every xflag itself, so an aborted kernel (watchdog)
 // can never leave the output stream waiting.
+// The 3D executor's version: b in z-slabs (k3R planes, one row of tiles),
+// doubling copies up to 8 slabs, flagged on their last slab; x per 2 slabs,
+// each copy waiting on the flag of its last tile (flags rise in tile order).
+int DevicePlan::solve_host_streamed3d(const double* b, double* x, sptrsv_stats* st) {
+  auto t0 = std::chrono::steady_clock::now();
+  Stencil3Plan& P = stencil3;
+  const unsigned ep = ++P.epoch;
+  const long long slab = 4LL * P.ny * P.nx;  // k3R planes
+  static const int in_max = [] {
+    const char* e = std::getenv("SPTRSV_STREAM3_IN");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
+  }();
+  static const int out_n = [] {
+    const char* e = std::getenv("SPTRSV_STREAM3_OUT");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 2;
+  }();
+  const int ns = P.nzt;
+  P.b_chunk_max = in_max;
+  CUDA_TRY(cudaEventRecord(ev0, stream));
+  int rc = solve_stencil3d(bbuf, xbuf, stream, true);
+  if (rc != SPTRSV_OK) return rc;
+  CUDA_TRY(cudaEventRecord(ev1, stream));
+  pending = true;
+  CUDA_TRY(stencil_release_flags(P.xflag, P.n_tasks, ep, stream));
+  for (int s0 = 0, w = 1; s0 < ns; s0 += w, w = std::min(2 * w, in_max)) {
+    const int s1 = std::min(ns, s0 + w);
+    const long long off = s0 * slab, cnt = std::min(slab * (s1 - s0), n - off);
+    CUDA_TRY(cudaMemcpyAsync(bbuf + off, b + off, sizeof(double) * cnt, cudaMemcpyHostToDevice, cs_in));
+    if (g_write32(cs_in, (unsigned long long)(P.bflag + s1 - 1), ep, 0) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWriteValue32 failed");
+  }
+  for (int s0 = 0; s0 < ns; s0 += out_n) {
+    const int s1 = std::min(ns, s0 + out_n);
+    const long long off = s0 * slab, cnt = std::min(slab * (s1 - s0), n - off);
+    if (g_wait32(cs_out, (unsigned long long)(P.xflag + (long long)s1 * P.nyt - 1), ep, kWaitGeq) != 0)
+      return fail(SPTRSV_E_CUDA, "cuStreamWaitValue32 failed");
+    CUDA_TRY(cudaMemcpyAsync(x + off, xbuf + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, cs_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(cs_in));
+  CUDA_TRY(cudaStreamSynchronize(cs_out));
+  rc = finish(st);
+  if (rc != SPTRSV_OK) return rc;
+  if (st) {
+    st->h2d_ms = 0.0;
+    st->d2h_ms = 0.0;
+    st->e2e_ms = ms_since(t0);
+    st->streamed_io = 1;
+  }
+  return SPTRSV_OK;
+}
+
 int DevicePlan::solve_host_streamed(const double* b, double* x, sptrsv_stats* st) {
   if (!cs_in) CUDA_TRY(cudaStreamCreateWithFlags(&cs_in, cudaStreamNonBlocking));
   if (!cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&cs_out, cudaStreamNonBlocking));
+  if (stencil3.ready) return solve_host_streamed3d(b, x, st);
   auto t0 = std::chrono::steady_clock::now();
   const unsigned ep = ++stencil.epoch;
   const long long band = (long long)kStBand * stencil.nx;

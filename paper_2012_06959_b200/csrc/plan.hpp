@@ -69,7 +69,8 @@ struct DevicePlan {
   StencilPlan stencil;
   Stencil3Plan stencil3;
   int build_stencil3d(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
-  int solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s);
+  int solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, bool flags = false);
+  int solve_host_streamed3d(const double* b, double* x, sptrsv_stats* st);
   // push executor (solve_push.cu): CSC of the off-diagonals + shared counters
   struct PushPlan {
     bool ready = false;

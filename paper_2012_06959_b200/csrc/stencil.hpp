@@ -128,8 +128,15 @@ struct Stencil3Plan {
   unsigned char* stream = nullptr;
   unsigned long long* ymail = nullptr;  // [2][tasks][4][nx]
   unsigned long long* zmail = nullptr;  // [2][tasks][32][nx]
+  // streamed host solves: b arrives by z-slabs (k3R planes = one row of
+  // tiles), flagged on the last slab of each copy; x flags per tile, raised
+  // in tile order
+  unsigned* bflag = nullptr;  // [nzt]
+  unsigned* xflag = nullptr;  // [n_tasks]
+  unsigned epoch = 0;
+  int b_chunk_max = 0;
   void release() {
-    void* ptrs[] = {stream, ymail, zmail};
+    void* ptrs[] = {stream, ymail, zmail, bflag, xflag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     *this = Stencil3Plan();

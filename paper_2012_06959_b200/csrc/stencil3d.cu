@@ -78,6 +78,12 @@ struct S3Args {
   int probe;                 // diagnostics flags (probe_flags; 128: count exact-mode chunk redos)
   unsigned long long* ymail_next;  // the other mailbox halves: the storer resets each tile's part
   unsigned long long* zmail_next;  // for the next solve
+  // streamed host solves (null otherwise): slab Z's b is resident once the
+  // flag of the last slab of its copy reaches epoch; x flags per tile
+  const unsigned* bflag;
+  unsigned* xflag;
+  unsigned epoch;
+  int b_chunk_max;
 };
 
 template <bool EXACT>
@@ -163,6 +169,24 @@ __device__ void s3_loader(const S3Args& a, unsigned char* smem, int* ctl, int t,
   };
   int issued = 0;
   bool ok = true;
+  if (a.bflag) {
+    // this tile's slab arrives with the copy of slabs [s0, s0 + w) (doubling w)
+    int flag_slab = Z;
+    for (int s0 = 0, w = 1;; s0 += w, w = min(2 * w, a.b_chunk_max))
+      if (Z < s0 + w) {
+        flag_slab = min(a.nzt, s0 + w) - 1;
+        break;
+      }
+    int polls = 0;
+    while ((int)(ld_acquire_sys_u32(a.bflag + flag_slab) - a.epoch) < 0) {
+      if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
+      if (!__all_sync(0xffffffffu, ok)) {
+        s3_abort(a, ctl, lane);
+        return;
+      }
+      __nanosleep(256);
+    }
+  }
   for (int c = 0; c < nchunks; ++c) {
     const int done = ld_acquire_cta(ctl + kC3InDone);
     while (issued < nchunks && issued < done + NB) issue(issued++);
@@ -309,6 +333,18 @@ __device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t,
     }
     __syncwarp();
     if (lane == 0) st_release_cta(ctl + kC3OutDone, c + 1);
+  }
+  // streamed host solve: tile t's x may be copied once its flag is up; flags
+  // go up in tile order so a copy of whole slabs waits on its last tile only
+  if (a.xflag && lane == 0) {
+    __threadfence_system();
+    int polls = 0;
+    while (t > 0 && (int)(ld_acquire_sys_u32(a.xflag + t - 1) - a.epoch) < 0) {
+      if (ld_relaxed_s32(a.abort_flag)) break;  // released after the kernel anyway
+      if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) break;
+      __nanosleep(64);
+    }
+    st_release_sys_u32(a.xflag + t, a.epoch);
   }
 }
 
@@ -735,7 +771,14 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
       (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
       (e = al((void**)&P.zmail, 2 * sizeof(unsigned long long) * zw)) != cudaSuccess ||
       (e = s3_fill_not_ready(P.ymail, 2 * yw, 0)) != cudaSuccess ||
-      (e = s3_fill_not_ready(P.zmail, 2 * zw, 0)) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess)
+      (e = s3_fill_not_ready(P.zmail, 2 * zw, 0)) != cudaSuccess ||
+      (e = al((void**)&P.bflag, sizeof(unsigned) * P.nzt)) != cudaSuccess ||
+      (e = al((void**)&P.xflag, sizeof(unsigned) * P.n_tasks)) != cudaSuccess ||
+      (e = cudaMemset(P.bflag, 0, sizeof(unsigned) * P.nzt)) != cudaSuccess ||
+      (e = cudaMemset(P.xflag, 0, sizeof(unsigned) * P.n_tasks)) != cudaSuccess ||
+      (e = cudaDeviceSynchronize()) != cudaSuccess ||
+      // loaded now, not lazily while a streamed solve spins (see stencil.cu)
+      (e = stencil_release_flags(P.xflag, P.n_tasks, 0u, stream)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   {  // pack the coefficient stream on the device (one thread per tile-step-lane)
     const long long items = (long long)P.n_tasks * P.steps * k3Lanes;
@@ -751,7 +794,7 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
   return SPTRSV_OK;
 }
 
-int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s) {
+int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, bool flags) {
   Stencil3Plan& P = stencil3;
   if (!P.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 3D seven-point lower structured");
   const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
@@ -773,6 +816,12 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s) 
   a.abort_flag = abort_flag;
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   a.probe = opt.probe_flags;
+  if (flags) {
+    a.bflag = stencil3.bflag;
+    a.xflag = stencil3.xflag;
+    a.epoch = stencil3.epoch;
+    a.b_chunk_max = stencil3.b_chunk_max;
+  }
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.nx = P.nx, a.ny = P.ny, a.nz = P.nz, a.nyt = P.nyt, a.nzt = P.nzt;

@@ -348,13 +348,13 @@ def test_stencil3d_unaligned_and_device_resident():
 
 
 @pytest.mark.parametrize("precision", ["exact", "fast"])
-@pytest.mark.parametrize("shape", [(64, 64), (128, 200), (512, 1000)])
+@pytest.mark.parametrize("shape", [(64, 64), (128, 200), (512, 1000), (16, 40, 9), (64, 70, 33)])
 def test_stencil_streamed_host_solve(shape, precision):
     """sptrsv_solve on host buffers: pinned (band-granular copies overlapping
     the kernel) and pageable give the same x as the unstreamed plan and
     (exact) the oracle; repeated solves (epoch flags never reset)."""
     torch = pytest.importorskip("torch")
-    l = _random_coefficients(synth.lap2d(*shape), 11)
+    l = _random_coefficients(synth.lap2d(*shape) if len(shape) == 2 else synth.lap3d(*shape), 11)
     rng = np.random.default_rng(12)
     plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil")
     flat = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision, executor="stencil",
