@@ -16,7 +16,12 @@ configured matrix with b = ones (the reference CLI default, cli.py:139-140).
   (``sptrsv_solve``: pinned b -> device, solve, device -> pinned x), wall clock.
 * ``roofline``: the solve kernel's algorithmic bytes (SURVEY.md §8d:
   12·nnz + 4·(n+1) + 16·n) over its CUDA-event duration, against the measured
-  HBM copy bandwidth in MEASURED_PEAKS.json.
+  HBM copy bandwidth in MEASURED_PEAKS.json (N > 1: the slowest rank's kernel
+  against N HBMs).
+* ``timing``: >= 100 repeats with mean / min / max per solve,
+  kernel-only times, setup and the combined setup + solve figure
+  (cli.py:199-202). Inputs under 5x the L2 size are timed with a 256 MB
+  scratch write between solves (the L2-cold figure; ``l2_warm_ms`` beside it).
 * ``cpu_baseline``: the C port of the reference ``solve_serial`` (oracle/) on
   one host core, full matrix (rank 0, N = 1 only).
 
@@ -154,7 +159,7 @@ def reference_arm(args, l, b, n, nnz):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="lap2d-4096")
@@ -162,6 +167,9 @@ def main():
     ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil", "push", "band"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l2", choices=["auto", "flush", "warm"], default="auto",
+                    help="auto: flush a 256 MB scratch buffer between timed solves when the solve's inputs are "
+                         "< 5x the L2 size, else back-to-back solves")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -226,6 +234,26 @@ def main():
             torch.distributed.all_reduce(order_word)
         plan.solve_device_async(db.data_ptr(), dx.data_ptr(), sh)
 
+    alg = algorithmic_bytes(n, nnz)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = args.l2 == "flush" or (args.l2 == "auto" and alg < 5 * l2_bytes)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}") if flush else None
+
+    def timed_loop(k: int, do_flush: bool) -> tuple[list[float], list[float]]:
+        """k solves; per-solve device times (events on the solve stream) and kernel times."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k)]
+        kms = []
+        for i in range(k):
+            if do_flush:
+                scratch.fill_(i & 0xFF)  # 256 MB > 126 MB L2, outside the timed events
+            ev[2 * i].record(stream)
+            one_solve()
+            ev[2 * i + 1].record(stream)
+            if do_flush or i >= k - 10:
+                kms.append(plan.synchronize()["kernel_ms"])
+        torch.cuda.synchronize(dev)
+        return [ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(k)], kms
+
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             one_solve()
@@ -233,29 +261,40 @@ def main():
         torch.cuda.synchronize(dev)
         if ws > 1:
             torch.distributed.barrier()
-        kernel_ms = []
         with ClockSampler(dev) as clocks:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(dev)
-            e0.record(stream)
+            if flush:
+                per_solve, kernel_ms = timed_loop(args.steps, True)
+                total_ms = sum(per_solve)
+            else:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(args.steps):
+                    one_solve()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                total_ms = e0.elapsed_time(e1)
+                # per-solve spread and per-launch kernel durations (same stream)
+                per_solve, kernel_ms = timed_loop(min(args.steps, 30), False)
+        warm = None
+        if flush:  # the back-to-back (L2-warm) figure beside the flushed one
+            w0 = torch.cuda.Event(enable_timing=True)
+            w1 = torch.cuda.Event(enable_timing=True)
+            w0.record(stream)
             for _ in range(args.steps):
                 one_solve()
-            e1.record(stream)
+            w1.record(stream)
             torch.cuda.synchronize(dev)
-            total_ms = e0.elapsed_time(e1)
-            # per-launch kernel durations (events around the kernel, same stream)
-            for _ in range(min(args.steps, 10)):
-                one_solve()
-                st = plan.synchronize()
-                kernel_ms.append(st["kernel_ms"])
+            warm = w0.elapsed_time(w1) / args.steps
         if ws > 1:
             torch.distributed.barrier()
         ms = total_ms / args.steps
+        kern = statistics.mean(kernel_ms) if kernel_ms else ms
         if ws > 1:
-            t = torch.tensor([ms], device=f"cuda:{dev}")
+            t = torch.tensor([ms, kern], device=f"cuda:{dev}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
+            ms, kern = float(t[0].item()), float(t[1].item())
             # x: each rank holds its owned rows; the sum over ranks assembles it
             xfull = dx * owned
             torch.distributed.all_reduce(xfull)
@@ -288,14 +327,15 @@ def main():
             sl = slice(int(rows[0]), int(rows[-1]) + 1)
         else:
             sl = slice(0, n)
-        for _ in range(args.e2e_steps + 1):
-            torch.distributed.barrier()
-            t1 = time.perf_counter()
-            db[sl].copy_(hb[sl], non_blocking=True)
-            one_solve()
-            plan.synchronize()
-            hx[sl].copy_(dx[sl], non_blocking=False)
-            t_e2e.append(time.perf_counter() - t1)
+        with torch.cuda.stream(stream):  # copy -> all-reduce -> solve -> copy, ordered on one stream
+            for _ in range(args.e2e_steps + 1):
+                torch.distributed.barrier()
+                t1 = time.perf_counter()
+                db[sl].copy_(hb[sl], non_blocking=True)
+                one_solve()
+                plan.synchronize()
+                hx[sl].copy_(dx[sl], non_blocking=False)
+                t_e2e.append(time.perf_counter() - t1)
         t_e2e = t_e2e[1:]
         h2d_rank = 8 * (sl.stop - sl.start)
         d2h = 8 * (sl.stop - sl.start)
@@ -324,9 +364,9 @@ def main():
     res_inf = residual_norm(l, x_dev, b)[1]
     res_2 = residual_norm_2(l, x_dev, b)
 
-    kern = statistics.mean(kernel_ms) if kernel_ms else ms
     peak, peak_kind = measured_peaks()
-    alg = algorithmic_bytes(n, nnz)
+    # N > 1: the whole job's bytes over the slowest rank's kernel, against N HBMs
+    peak = peak * ws
     achieved = alg / (kern * 1e-3) / 1e9
     traffic = None
     tr = ROOT / "profiles" / "traffic.json"
@@ -358,8 +398,23 @@ def main():
             "precision": args.precision,
             "executor": info["executor"],
             "parallelism": f"column-block x{ws} (block_partition), IPC peer segments" if ws > 1 else "single GPU",
-            "l2": f"no flush: solve inputs {alg / 1e6:.0f} MB vs 126 MB L2" if alg > 256e6
-            else "inputs fit L2 (warm-L2 figure)",
+            "l2": (f"flushed: 256 MB scratch write between timed solves (solve inputs {alg / 1e6:.0f} MB vs "
+                   f"{l2_bytes / 1e6:.0f} MB L2)") if flush else
+                  f"back-to-back: solve inputs {alg / 1e6:.0f} MB vs {l2_bytes / 1e6:.0f} MB L2",
+        },
+        "timing": {
+            "repeats": args.steps,
+            "mean_ms": ms,
+            "min_ms": min(per_solve),
+            "max_ms": max(per_solve),
+            "per_solve_sample": len(per_solve),
+            "kernel_mean_ms": kern,
+            "kernel_min_ms": min(kernel_ms) if kernel_ms else None,
+            "l2_warm_ms": warm,
+            "setup_ms": setup_s * 1e3,
+            # the paper's protocol sums analysis and solve (
+            # the reference's mean_combined_time, cli.py:199-202)
+            "combined_ms": setup_s * 1e3 + ms,
         },
         "roofline": {
             "bound": "hbm",

@@ -10,12 +10,27 @@
 // in_degree/left_sum counter pair (reference engine.py:495-550).
 #pragma once
 #include <cstdint>
+#include <atomic>
 #include <cuda_runtime.h>
 
 namespace sptrsv {
 
 constexpr unsigned long long kNotReady = 0xFFFFFFFFFFFFFFFFull;
 constexpr int kWarp = 32;
+
+// cudaFuncSetAttribute applies to the current device's context only: track,
+// per kernel instantiation, the devices it was set on (one bit per ordinal).
+template <typename F>
+inline cudaError_t set_max_dyn_smem(F* fn, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+  if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_relaxed);
+  return e;
+}
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
   unsigned long long v;

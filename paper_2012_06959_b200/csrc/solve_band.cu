@@ -242,12 +242,8 @@ __global__ void __launch_bounds__(kBThreads, 1) k_band(const __grid_constant__ B
 
 template <int MODE>
 cudaError_t launch_band_v(const BandArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_band<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, BSmem::kTotal);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = set_max_dyn_smem(k_band<MODE>, BSmem::kTotal, attr); e != cudaSuccess) return e;
   k_band<MODE><<<1, kBThreads, BSmem::kTotal, s>>>(a);
   return cudaGetLastError();
 }

@@ -333,13 +333,8 @@ __global__ void __launch_bounds__(32, 1) k_chains(ChainArgs a) {
 
 template <bool EXACT, int W, bool PROBE>
 cudaError_t launch_variant(const ChainArgs& a, int blocks, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_chains<EXACT, W, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTotal);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = set_max_dyn_smem(k_chains<EXACT, W, PROBE>, kSmemTotal, attr); e != cudaSuccess) return e;
   k_chains<EXACT, W, PROBE><<<blocks, 32, kSmemTotal, s>>>(a);
   return cudaGetLastError();
 }

@@ -639,13 +639,8 @@ __global__ void __launch_bounds__(k3Threads, 1) k_stencil3d(const __grid_constan
 
 template <bool EXACT>
 cudaError_t launch_s3(const S3Args& a, int blocks, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_stencil3d<EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         S3Smem<EXACT>::kTotal);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = set_max_dyn_smem(k_stencil3d<EXACT>, S3Smem<EXACT>::kTotal, attr); e != cudaSuccess) return e;
   k_stencil3d<EXACT><<<blocks, k3Threads, S3Smem<EXACT>::kTotal, s>>>(a);
   return cudaGetLastError();
 }

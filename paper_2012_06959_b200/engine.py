@@ -29,6 +29,7 @@ only into its own segment).
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -85,6 +86,10 @@ class SolverConfig:
             raise ValueError(f"precision must be one of {sorted(_native.PRECISION)}, got {self.precision!r}")
         if self.executor not in _native.EXECUTOR:
             raise ValueError(f"executor must be one of {sorted(_native.EXECUTOR)}, got {self.executor!r}")
+        if self.executor == "push" and self.precision == "exact":
+            # Alg. 2 accumulates with atomics in arrival order: within 1e-12 of
+            # the oracle, never bit-identical, so it cannot honour "exact"
+            raise ValueError('executor="push" (atomic left sums) is not bit-exact: use precision="fast"')
 
 
 @dataclass
@@ -173,10 +178,13 @@ _struct_cache: dict = {}
 
 
 def _entry_owner_split(l: CscMatrix, plan: PartitionPlan):
-    """Per off-diagonal entry: (row, col, owner(row), owner(col)); cached per (L, plan)."""
+    """Per off-diagonal entry: (row, col, owner(row), owner(col)); cached per (L, plan).
+
+    The cache holds L weakly: an entry is dropped when its matrix is collected.
+    """
     key = (id(l), id(plan))
     hit = _struct_cache.get(key)
-    if hit is not None and hit[0] is l and hit[1] is plan:
+    if hit is not None and hit[0]() is l and hit[1] is plan:
         return hit[2]
     cols = l.entry_columns()
     off = l.row_idx != cols
@@ -185,7 +193,8 @@ def _entry_owner_split(l: CscMatrix, plan: PartitionPlan):
     val = (rows, cols, own[rows], own[cols], l.values[off])
     if len(_struct_cache) > 8:
         _struct_cache.clear()
-    _struct_cache[key] = (l, plan, val)
+    _struct_cache[key] = (weakref.ref(l), plan, val)
+    weakref.finalize(l, _struct_cache.pop, key, None)
     return val
 
 

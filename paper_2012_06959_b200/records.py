@@ -20,6 +20,7 @@ import json
 import sys
 from dataclasses import dataclass, replace
 from pathlib import Path
+from typing import Callable, Optional
 
 import numpy as np
 
@@ -38,6 +39,36 @@ FIELDS = (
     "mean_setup_time", "mean_combined_time", "max_rel_error", "lock_wait_spins", "remote_reads_issued",
     "remote_reads_skipped", "local_updates", "remote_updates",
 )
+
+
+_INT = {"type": "integer", "minimum": 0}
+_INT1 = {"type": "integer", "minimum": 1}
+_SEC = {"type": "number", "minimum": 0}
+# The record contract of the reference (docs/record_schema.json, draft 2020-12),
+# restated: field types, bounds, the engine enum, no extra fields.
+RECORD_SCHEMA = {
+    "$schema": "https://json-schema.org/draft/2020-12/schema",
+    "type": "object",
+    "properties": {
+        "name": {"type": "string"}, "engine": {"enum": ["shared", "partitioned"]},
+        "n": _INT1, "nnz": _INT1, "n_levels": _INT1, "parallelism": _INT1,
+        "dependency": {"type": "number", "exclusiveMinimum": 0},
+        "n_pes": _INT1, "tasks_per_pe": _INT1, "workers_per_pe": _INT1, "repeats": _INT1, "engine_runs": _INT1,
+        "mean_wall_time": _SEC, "min_wall_time": _SEC, "max_wall_time": _SEC, "mean_setup_time": _SEC,
+        "mean_combined_time": _SEC, "max_rel_error": {"type": ["number", "null"], "minimum": 0},
+        "lock_wait_spins": _INT, "remote_reads_issued": _INT, "remote_reads_skipped": _INT,
+        "local_updates": _INT, "remote_updates": _INT,
+    },
+    "required": list(FIELDS),
+    "additionalProperties": False,
+}
+
+
+def validate_record(record: dict) -> None:
+    """Raise ``jsonschema.ValidationError`` unless ``record`` satisfies RECORD_SCHEMA."""
+    import jsonschema
+
+    jsonschema.validate(record, RECORD_SCHEMA, cls=jsonschema.Draft202012Validator)
 
 
 class VerificationFailed(SptrsvError):
@@ -61,6 +92,10 @@ class RunSpec:
     verify: bool = True
     precision: str = "exact"
     executor: str = "auto"
+    # verify against this serial solve (the reference checks against its own
+    # Python loop, cli.py:166-167); None: this package's solve_serial, which
+    # runs on the GPU, so max_rel_error is then GPU self-consistency only
+    reference: Optional[Callable[[CscMatrix, np.ndarray], np.ndarray]] = None
 
     def config(self) -> SolverConfig:
         return SolverConfig(engine=self.engine, n_pes=self.n_pes, workers_per_pe=self.workers_per_pe,
@@ -75,7 +110,7 @@ def run_benchmark(spec: RunSpec) -> dict:
     stats = analysis.compute_stats(spec.matrix)
     plan = task_round_robin_partition(spec.matrix.n, spec.n_pes, spec.tasks_per_pe)
     cfg = spec.config()
-    x_ref = solve_serial(spec.matrix, spec.rhs) if spec.verify else None
+    x_ref = (spec.reference or solve_serial)(spec.matrix, spec.rhs) if spec.verify else None
     solve_times, setup_times, combined = [], [], []
     max_rel_error = None
     report = None

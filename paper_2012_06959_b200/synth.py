@@ -152,18 +152,35 @@ def rmat(scale: int, edge_factor: int = 8, seed: int = 0, a=0.57, b=0.19, c=0.19
     ab, abc = a + b, a + b + c
     for bit in range(scale):
         r = rng.random(m)
-        right = ((r >= a) & (r < ab)) | (r >= abc)  # quadrants b, d set the column bit
-        down = r >= ab  # quadrants c, d set the row bit
-        u |= down.astype(np.int64) << bit
-        v |= right.astype(np.int64) << bit
+        q = (r >= a).view(np.int8) + (r >= ab).view(np.int8) + (r >= abc).view(np.int8)  # quadrant a,b,c,d = 0..3
+        u |= (q >= 2).astype(np.int64) << bit  # quadrants c, d set the row bit
+        v |= (q & 1).astype(np.int64) << bit  # quadrants b, d set the column bit
     lo = np.minimum(u, v)
     hi = np.maximum(u, v)
+    del u, v
     keep = lo != hi
-    key = np.unique(hi[keep] * n + lo[keep])
+    key = np.sort(hi[keep] * n + lo[keep])
+    del lo, hi, keep
+    key = key[np.concatenate(([True], key[1:] != key[:-1]))] if key.size else key  # unique, row-major
     rows = key // n
-    cols = key % n
+    cols = key - rows * n
     vals = rng.uniform(-1.0, 1.0, size=rows.size)
-    return _from_coo_lower(n, rows, cols, vals, _dominant_diag(n, rows, vals, rng))
+    diag = _dominant_diag(n, rows, vals, rng)
+    # CSC: entries by (column, row), the diagonal first in each column
+    order = np.argsort(cols * n + rows)
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    counts = 1 + np.bincount(cols, minlength=n)
+    col_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=col_ptr[1:])
+    nnz = int(col_ptr[-1])
+    row_idx = np.empty(nnz, dtype=np.int64)
+    values = np.empty(nnz)
+    pos = np.arange(rows.size, dtype=np.int64) + cols + 1
+    row_idx[pos] = rows
+    values[pos] = vals
+    row_idx[col_ptr[:-1]] = np.arange(n, dtype=np.int64)
+    values[col_ptr[:-1]] = diag
+    return CscMatrix(n=n, col_ptr=col_ptr, row_idx=row_idx, values=values)
 
 
 def diagonal(n: int) -> CscMatrix:

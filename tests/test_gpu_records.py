@@ -10,6 +10,7 @@ import json
 import numpy as np
 import pytest
 
+import oracle
 import paper_2012_06959_b200 as sp
 from paper_2012_06959_b200 import records, synth
 from paper_2012_06959_b200.errors import IndivisibleTaskTotal, InvalidSpec
@@ -23,17 +24,25 @@ REQUIRED = ["name", "engine", "n", "nnz", "n_levels", "parallelism", "dependency
             "remote_reads_skipped", "local_updates", "remote_updates"]
 
 
+def _oracle_serial(l, b):
+    # the independent CPU check (the reference verifies against its own serial loop)
+    return oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+
+
 def _spec(**kw):
     l = synth.lap2d(48, 40)
-    return records.RunSpec(name="lap2d-48x40", matrix=l, rhs=np.ones(l.n), repeats=3, **kw)
+    kw.setdefault("reference", _oracle_serial)
+    return records.RunSpec(name="lap2d-48x40", matrix=l, rhs=np.random.default_rng(3).uniform(-1, 1, l.n),
+                           repeats=3, **kw)
 
 
 def test_record_fields_and_values():
     r = records.run_benchmark(_spec())
     assert list(r) == REQUIRED
+    records.validate_record(r)
     assert r["engine"] in ("shared", "partitioned")
     assert r["n"] == 1920 and r["n_levels"] == 48 + 40 - 1 and r["engine_runs"] == 3
-    assert r["max_rel_error"] == 0.0  # exact mode: bit-identical to solve_serial
+    assert r["max_rel_error"] == 0.0  # exact mode: bit-identical to the C oracle
     assert 0 <= r["min_wall_time"] <= r["mean_wall_time"] <= r["max_wall_time"]
     assert r["local_updates"] + r["remote_updates"] == r["nnz"] - r["n"]
 
@@ -47,6 +56,9 @@ def test_sweeps_and_emit(tmp_path):
     with pytest.raises(IndivisibleTaskTotal):
         records.sweep_pes(base, [3], fixed_total_tasks=32)
     recs += records.sweep_tasks(base, [1, 4])
+    for r in recs:
+        records.validate_record(r)
+        assert 0.0 <= r["max_rel_error"] <= 1e-12  # fast mode vs the C oracle
     text = records.emit(recs, "json", str(tmp_path / "r.jsonl"))
     assert [json.loads(line)["tasks_per_pe"] for line in text.splitlines()] == [32, 16, 8, 1, 4]
     text = records.emit(recs, "csv", str(tmp_path / "r.csv"))

@@ -100,6 +100,9 @@ def test_solver_config_validation():
         sp.SolverConfig(engine=sp.Engine.SHARED_ATOMICS, timeout=0.0)
     with pytest.raises(ValueError):
         sp.SolverConfig(engine=sp.Engine.SHARED_ATOMICS, precision="half")
+    with pytest.raises(ValueError, match="push"):
+        sp.SolverConfig(engine=sp.Engine.SHARED_ATOMICS, executor="push", precision="exact")
+    sp.SolverConfig(engine=sp.Engine.SHARED_ATOMICS, executor="push", precision="fast")
 
 
 def test_engine_argument_checks_need_no_gpu(worked_3x3):

@@ -37,10 +37,21 @@ def _text(name):
     ("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n", MalformedEntry),
     ("%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1\n", MalformedEntry),
     ("%%MatrixMarket matrix coordinate real general\n% only comments\n", MalformedHeader),
+    # tokens the pandas tokenizer would read as NaN, and trailing comment text:
+    # the reference's line parser rejects all of them
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 NA\n2 2 1\n", MalformedEntry),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 null\n2 2 1\n", MalformedEntry),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 3.0 % note\n2 2 1\n", MalformedEntry),
+    ("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 N/A\n2 2 1\n", MalformedEntry),
 ])
 def test_parser_errors_match_reference_classes(text, exc):
     with pytest.raises(exc):
         mmio.parse_coo(text.encode())
+
+
+def test_comment_lines_inside_the_block_are_skipped():
+    n, r, c, v = mmio.parse_coo(b"%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.5\n% mid\n2 2 2.5\n")
+    assert n == 2 and r.tolist() == [0, 1] and c.tolist() == [0, 1] and v.tolist() == [1.5, 2.5]
 
 
 @pytest.mark.parametrize("name", NAMES)
@@ -50,8 +61,9 @@ def test_fast_and_slow_entry_parsers_agree(name):
     lines = text.splitlines()
     field, symmetry, n, n_decl, first = mmio._header(lines)
     slow = mmio._entries_slow(lines, first, n, n_decl, field == "pattern")
-    fast = mmio._entries_fast("\n".join(lines[first:]), n, n_decl, field == "pattern")
-    if n_decl == 0:
+    body = "\n".join(lines[first:])
+    fast = mmio._entries_fast(body, n, n_decl, field == "pattern")
+    if n_decl == 0 or "%" in body:  # comment lines: the line parser handles the block
         assert fast is None
         return
     assert fast is not None
