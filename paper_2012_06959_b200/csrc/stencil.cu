@@ -63,16 +63,6 @@ constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
 #ifndef SPTRSV_ST_SPEC
 #define SPTRSV_ST_SPEC 1
 #endif
-// Compute-warp chunk waits on mbarriers (SPTRSV_ST_MBWAIT=1): the input slot's
-// TMA barrier, a per-slot inbox barrier the poller's lanes arrive on and a
-// per-slot out-ring barrier the storer's lanes arrive on, probed with
-// mbarrier.test_wait, instead of three ld.acquire polls of the chunk
-// counters (the loader's zero-fill of the first chunks still goes through
-// the InReady counter).
-#ifndef SPTRSV_ST_MBWAIT
-#define SPTRSV_ST_MBWAIT 0
-#endif
-constexpr bool kStMbWait = SPTRSV_ST_MBWAIT;
 // x leaves interior chunks by one TMA tensor store (SPTRSV_ST_X_TMA=1) or by
 // the storer's 16-byte stores (default): measured the same on lap2d-4096
 #ifndef SPTRSV_ST_X_TMA
@@ -190,10 +180,8 @@ struct StSmem {
   // whole chunk leaves with one TMA tensor store through the skewed view of x
   static constexpr int kOut = (kInbox + kSlots * kStG * kStC * 8 + 1023) / 1024 * 1024;
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
-  static constexpr int kBars = kOut + kStOutSlots * kOutChunk;  // [kSlots] input, [kSlots] inbox, [out slots] out
-  static constexpr int kInBars = kBars + 8 * kSlots;
-  static constexpr int kOutBars = kInBars + 8 * kSlots;
-  static constexpr int kCtl = kOutBars + 8 * kStOutSlots;
+  static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
+  static constexpr int kCtl = kBars + 8 * kSlots;
   static constexpr int kTotal = kCtl + 64 + 1024;  // + alignment slack of the ring base
   static_assert(kB % 1024 == 0 && kBChunk % 1024 == 0, "b slots on 1024-byte boundaries (TMA swizzle)");
 };
@@ -430,7 +418,6 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
-    if (kStMbWait) mbar_arrive(reinterpret_cast<unsigned long long*>(smem + S::kInBars) + c % NB);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
   }
 #pragma unroll
@@ -492,7 +479,6 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       }
     }
     __syncwarp();
-    if (kStMbWait) mbar_arrive(reinterpret_cast<unsigned long long*>(smem + S::kOutBars) + c % kStOutSlots);
     if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
   }
   if (x_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
@@ -561,44 +547,11 @@ __device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
 // active/publish branch
 template <bool EXACT, int ABL, bool PART>
-__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
-                        unsigned (&ph)[3]) {
+__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const bool has_above = t > 0;
-  unsigned long long* in_bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
-  unsigned long long* ib_bars = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
-  unsigned long long* ob_bars = reinterpret_cast<unsigned long long*>(smem + S::kOutBars);
-  // Chunk cn's inputs (slot cn % NB), its band-above inbox and a free output
-  // slot (the storer done with chunk cn - kStOutSlots). ph[] are this warp's
-  // phase bits of the input / inbox / output barriers, kept across tasks: every
-  // phase is consumed exactly once, in order.
-  auto wait_next = [&](int cn) -> bool {
-    const int sl = cn % NB, so = cn % kStOutSlots;
-    const bool need_out = cn >= kStOutSlots;
-    if (!kStMbWait || cn * kStG < kStLanes) {
-      // the loader zero-fills the first chunks after their TMA landed: counters
-      if (!wait_chunk(ctl, cn + 1, has_above ? cn + 1 : 0, need_out ? cn + 1 - kStOutSlots : 0, deadline))
-        return false;
-    } else {
-      int polls = 0;
-      while (true) {
-        bool ok = mbar_test_wait(in_bars + sl, (ph[0] >> sl) & 1u);
-        if (has_above) ok &= mbar_test_wait(ib_bars + sl, (ph[1] >> sl) & 1u);
-        if (need_out) ok &= mbar_test_wait(ob_bars + so, (ph[2] >> so) & 1u);
-        if (ok) break;
-        if (*reinterpret_cast<volatile int*>(ctl + kCtlAbort)) return false;
-        if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
-      }
-    }
-    if (kStMbWait) {
-      ph[0] ^= 1u << sl;
-      if (has_above) ph[1] ^= 1u << sl;
-      if (need_out) ph[2] ^= 1u << so;
-    }
-    return true;
-  };
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   // the band below on another PE reads these over NVLink: system-scope stores
   const bool below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
@@ -748,7 +701,8 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     // the first step that loads from chunk c + 1: make sure it is ready
     if (k == kStG - 2 && c + 1 < nchunks && !solo) {
       if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-      if (!wait_next(c + 1)) return false;
+      if (!wait_chunk(ctl, c + 2, has_above ? c + 2 : 0, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0, deadline))
+        return false;
       if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
     }
     const int s = c * kStG + k;
@@ -806,7 +760,8 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   long long* tstamp = (a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
-  if (!solo && !wait_next(0)) return abort_task(a, ctl, lane);
+  if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
+  if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, 1, deadline)) return abort_task(a, ctl, lane);
   if (tstamp) tstamp[1] = (long long)globaltimer_ns();
   static_assert(kStG >= 3, "the two-step lookahead stays within one chunk boundary");
   buf[0].load(smem, 0, 0, lane);
@@ -823,18 +778,6 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     }
   }
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
-  if (kStMbWait && !solo) {
-    // consume the storer's last output phases so the bits stay in step for the next task
-    for (int m = nchunks > kStOutSlots ? nchunks - kStOutSlots : 0; m < nchunks; ++m) {
-      const int so = m % kStOutSlots;
-      int polls = 0;
-      while (!mbar_test_wait(ob_bars + so, (ph[2] >> so) & 1u)) {
-        if (*reinterpret_cast<volatile int*>(ctl + kCtlAbort)) return;
-        if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return abort_task(a, ctl, lane);
-      }
-      ph[2] ^= 1u << so;
-    }
-  }
 }
 
 template <bool EXACT, int ABL, bool PART>
@@ -848,14 +791,9 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
   if (threadIdx.x == 0) {
     unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
     for (int k = 0; k < S::kSlots; ++k) mbar_init(&bars[k], 1 + kStLanes);
-    unsigned long long* ib = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
-    unsigned long long* ob = reinterpret_cast<unsigned long long*>(smem + S::kOutBars);
-    for (int k = 0; k < S::kSlots; ++k) mbar_init(&ib[k], kStLanes);
-    for (int k = 0; k < kStOutSlots; ++k) mbar_init(&ob[k], kStLanes);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned phase_bits = 0;
-  unsigned cph[3] = {0u, 0u, 0u};  // compute warp's barrier phase bits
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
   while (true) {
     if (threadIdx.x == 0) {
@@ -867,7 +805,7 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
     __syncthreads();
     const int t = ctl[kCtlTask];
     if (t >= a.n_tasks) break;
-    if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline, cph);
+    if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline);
     else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
     } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
     else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
