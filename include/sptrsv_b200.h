@@ -181,6 +181,14 @@ int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* ipc_handle_out);
 int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* ipc_handle);
 int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr);
 void* sptrsv_plan_segment(const sptrsv_plan* plan); /* this process's first segment (device pointer) */
+/* One synchronous solve over all PEs of a partition held by ONE process
+ * (replaces the reference's thread-per-PE engine run, engine.py:438-582):
+ * plans[p] is PE p (set_partition(owner, n_plans, p)), peers wired with
+ * sptrsv_plan_set_peer_segment (which enables P2P access when the peer lives
+ * on another device). Plans may share a device or sit one per GPU; every PE's
+ * kernel runs concurrently on its own stream; b and x are host arrays. */
+int sptrsv_solve_group(sptrsv_plan* const* plans, int32_t n_plans, const double* b, double* x,
+                       sptrsv_stats* stats);
 int sptrsv_ipc_handle_size(void);
 
 /* Matrix Market ingestion (reference mmio.py:132-144 `_coo_to_csc`): COO

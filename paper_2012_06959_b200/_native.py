@@ -148,6 +148,8 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_plan_segment.restype = C.c_void_p
     lib.sptrsv_ipc_handle_size.argtypes = []
     lib.sptrsv_ipc_handle_size.restype = C.c_int
+    lib.sptrsv_solve_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32, _PD, _PD, C.POINTER(Stats)]
+    lib.sptrsv_solve_group.restype = C.c_int
 
 
 def load_library() -> C.CDLL:
@@ -385,6 +387,154 @@ def partitioned_plan_for(l, partition, **kw) -> NativePlan:
     with _cache_lock:
         per[key] = (partition, plan)
     return plan
+
+
+class PeGroup:
+    """All PEs of a partition in this process: one plan per PE (``plans[p]`` is PE p).
+
+    The PEs' plans sit on one device or one per GPU (P2P peer pointers); one
+    ``sptrsv_solve_group`` call launches every PE's kernel concurrently and
+    assembles x from each PE's own rows.
+    """
+
+    def __init__(self, plans: list[NativePlan], devices: list[int], mode: str):
+        self.plans = plans
+        self.devices = devices
+        self.mode = mode
+        self.n = plans[0].n
+        self._lib = plans[0]._lib
+
+    def info(self) -> dict:
+        d = self.plans[0].info()
+        d["pe_mode"] = self.mode
+        return d
+
+    def solve(self, b: np.ndarray, out: np.ndarray | None = None) -> tuple[np.ndarray, dict]:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = out if out is not None else np.empty(self.n, dtype=np.float64)
+        handles = (C.c_void_p * len(self.plans))(*[p.handle.value for p in self.plans])
+        st = Stats()
+        rc = self._lib.sptrsv_solve_group(handles, len(self.plans), _ptr(b, C.c_double), _ptr(x, C.c_double),
+                                          C.byref(st))
+        raise_for_status(rc, _err(self._lib))
+        d = st.as_dict()
+        d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
+        d["pe_mode"] = self.mode
+        d["devices"] = list(self.devices)
+        return x, d
+
+    def close(self) -> None:
+        for p in self.plans:
+            p.close()
+
+
+class SharedSegment:
+    """Virtual PEs sharing one published segment: the structured executors
+    (band window, 3D wavefront, lane chains, or a 2D wavefront whose owner map
+    splits bands) have no per-PE mode, so on one device the whole matrix runs
+    on the single fast plan; the PE split only shapes the report."""
+
+    def __init__(self, plan: NativePlan):
+        self.plan = plan
+
+    def info(self) -> dict:
+        d = self.plan.info()
+        d["pe_mode"] = "shared-segment"
+        return d
+
+    def solve(self, b, out=None):
+        x, d = self.plan.solve(b, out=out)
+        d["pe_mode"] = "shared-segment"
+        d["devices"] = [self.plan.device]
+        return x, d
+
+
+def pe_devices(n_pes: int, base: int = 0) -> list[int]:
+    """Device of each PE: ``SPTRSV_PE_DEVICES`` (comma list, dealt round-robin),
+    else one PE per visible GPU round-robin from ``base`` (SURVEY.md §8a N2:
+    n_pes = number of GPUs), else every PE on ``base``."""
+    env = os.environ.get("SPTRSV_PE_DEVICES")
+    if env:
+        devs = [int(v) for v in env.split(",") if v.strip()]
+    else:
+        count = require_gpu().sptrsv_device_count()
+        devs = [(base + k) % count for k in range(count)] if count > 1 else [base]
+    return [devs[p % len(devs)] for p in range(n_pes)]
+
+
+def _wire(plans: list[NativePlan]) -> None:
+    for p, pl in enumerate(plans):
+        for q, peer in enumerate(plans):
+            if q != p:
+                pl.set_peer_segment(q, peer.segment_ptr())
+
+
+def pe_solver_for(l, partition, executor: str = "auto", **kw):
+    """The solver behind ``solve_partitioned`` with ``n_pes > 1`` (engine.py:438-582).
+
+    * several GPUs: one plan per PE on its own device (``pe_devices``), each
+      publishing its rows into its own HBM, peers read over NVLink (P2P);
+    * one GPU, 2D five-point L with whole 64-row bands per PE: one stencil
+      plan per PE, peers' mailboxes in the same HBM (``mode="stencil-pes"``);
+    * one GPU, unstructured L: the component pool with one segment per PE
+      (``mode="pool-segments"``);
+    * one GPU, any other structured L: the single fast plan
+      (``SharedSegment``).
+    Cached per (matrix, partition object, knobs) like ``partitioned_plan_for``.
+    """
+    key = ("pes", id(partition), executor) + tuple(sorted(kw.items()))
+    ident = id(l)
+    with _cache_lock:
+        per = _cache.get(ident)
+        if per is None:
+            per = {}
+            _cache[ident] = per
+            weakref.finalize(l, _evict, ident)
+        hit = per.get(key)
+    if hit is not None and hit[0] is partition:
+        return hit[1]
+    P = partition.n_pes
+    device = kw.pop("device", 0)
+    devs = pe_devices(P, device)
+    owner = partition.owner_arr
+
+    def build(dev: int, ex: str = executor) -> NativePlan:
+        return NativePlan(l.col_ptr, l.row_idx, l.values, l.n, executor=ex, device=dev, **kw)
+
+    if len(set(devs)) > 1:
+        plans = []
+        for p in range(P):
+            pl = build(devs[p])
+            pl.set_partition(owner, P, p)
+            plans.append(pl)
+        _wire(plans)
+        solver = PeGroup(plans, devs, "pe-per-gpu")
+    else:
+        single = plan_for(l, executor=executor, device=device, **kw)
+        ex = single.info()["executor"]
+        solver = None
+        if ex == "stencil":
+            first = build(device, "stencil")
+            first.set_partition(owner, P, 0)
+            if first.info()["executor"] == "stencil":  # whole bands per PE (2D): partitioned wavefront
+                plans = [first]
+                for p in range(1, P):
+                    pl = build(device, "stencil")
+                    pl.set_partition(owner, P, p)
+                    plans.append(pl)
+                _wire(plans)
+                solver = PeGroup(plans, devs, "stencil-pes")
+            else:
+                first.close()
+        if solver is None and ex in ("rows", "push"):
+            pool = build(device, "rows")
+            pool.set_partition(owner, P, -1)
+            solver = pool
+        if solver is None:
+            solver = SharedSegment(single)
+    with _cache_lock:
+        per[key] = (partition, solver)
+    return solver
 
 
 def env_device() -> int:

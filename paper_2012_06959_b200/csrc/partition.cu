@@ -14,6 +14,7 @@
 // Inside the solve there is no collective and no remote write; scattering b
 // and gathering x around it is the caller's (NCCL in bench.py).
 #include <vector>
+#include <chrono>
 #include <algorithm>
 #include <cstring>
 #include "plan.hpp"
@@ -52,6 +53,7 @@ void DevicePlan::release_partition() {
   pe_order_off = nullptr;
   pe_tickets = nullptr;
   host_seg_table.clear();
+  host_owner.clear();
   n_pes = 1;
   n_pe_local = 1;
   pe_base = 0;
@@ -68,6 +70,7 @@ int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
   }
   cudaSetDevice(device);
   release_partition();
+  host_owner = own;
   if (executor_used == SPTRSV_EXECUTOR_STENCIL && stencil.ready && my_pe >= 0) {
     // band-aligned block (or band round-robin) ownership: the stencil
     // executor runs partitioned; anything else falls back to the pool
@@ -173,7 +176,8 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   a.coop_long = 0;
   a.long_deps = 1 << 30;
   int per_sm = rows_blocks_per_sm(mode);
-  int blocks = std::max(1, num_sms * std::max(per_sm, 1));
+  // grid_cap: this PE's share of the SMs when several PEs' kernels share the device
+  int blocks = std::max(1, (grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms) * std::max(per_sm, 1));
   blocks = std::max(n_pe_local, blocks - blocks % n_pe_local);
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = launch_rows(mode, a, blocks, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
@@ -187,11 +191,127 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   return SPTRSV_OK;
 }
 
+// A peer pointer on another device of this process: enable P2P access from
+// this plan's device to it (NVLink/NVSwitch between B200s), once.
+int DevicePlan::enable_peer(const void* peer_ptr) {
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, peer_ptr);
+  if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if (at.type != cudaMemoryTypeDevice || at.device == device) return SPTRSV_OK;
+  int ok = 0;
+  if ((e = cudaDeviceCanAccessPeer(&ok, device, at.device)) != cudaSuccess || !ok)
+    return plan_fail(SPTRSV_E_CUDA, "no peer access between the plans' devices");
+  cudaSetDevice(device);
+  e = cudaDeviceEnablePeerAccess(at.device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  return e == cudaSuccess ? SPTRSV_OK : plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+}
+
 }  // namespace sptrsv
 
 using namespace sptrsv;
 
 extern "C" {
+
+// One solve over the PEs of a partition held by this process: plans[p] is PE
+// p (sptrsv_plan_set_partition(plan, owner, n_plans, p)), peers wired with
+// sptrsv_plan_set_peer_segment. b is copied once per device, every PE's kernel
+// is launched on its own stream (they depend on each other's published x, so
+// they must run concurrently; persistent grids are capped so that the PEs of
+// one device are co-resident), and x is assembled from each PE's rows.
+int sptrsv_solve_group(sptrsv_plan* const* plans, int32_t n_plans, const double* b, double* x,
+                       sptrsv_stats* stats) {
+  if (!plans || n_plans < 1 || !b || !x) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  std::vector<DevicePlan*> ps(n_plans);
+  for (int p = 0; p < n_plans; ++p) {
+    ps[p] = reinterpret_cast<DevicePlan*>(plans[p]);
+    if (!ps[p]) return plan_fail(SPTRSV_E_ARGUMENT, "null plan");
+    if (ps[p]->n != ps[0]->n) return plan_fail(SPTRSV_E_ARGUMENT, "plans of different matrices");
+    if ((long long)ps[p]->host_owner.size() != ps[p]->n)
+      return plan_fail(SPTRSV_E_INVALID_PE, "plan has no PE partition");
+  }
+  const long long n = ps[0]->n;
+  if (n == 0) return SPTRSV_OK;
+  // one b / x buffer per device: the first plan on the device lends its own
+  std::vector<int> devs;
+  std::vector<DevicePlan*> lead;
+  std::vector<int> dev_of(n_plans), count;
+  for (int p = 0; p < n_plans; ++p) {
+    int k = 0;
+    while (k < (int)devs.size() && devs[k] != ps[p]->device) ++k;
+    if (k == (int)devs.size()) {
+      devs.push_back(ps[p]->device);
+      lead.push_back(ps[p]);
+      count.push_back(0);
+    }
+    dev_of[p] = k;
+    ++count[k];
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  cudaError_t e;
+  for (size_t k = 0; k < devs.size(); ++k) {
+    cudaSetDevice(devs[k]);
+    if ((e = cudaMemcpyAsync(lead[k]->bbuf, b, sizeof(double) * n, cudaMemcpyHostToDevice, lead[k]->stream)) !=
+            cudaSuccess ||
+        (e = cudaStreamSynchronize(lead[k]->stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  for (int p = 0; p < n_plans; ++p) {
+    DevicePlan* d = ps[p];
+    const int k = dev_of[p];
+    d->grid_cap = count[k] > 1 ? std::max(1, d->num_sms / count[k]) : 0;
+    cudaSetDevice(d->device);
+    const int rc = d->solve_device(lead[k]->bbuf, lead[k]->xbuf, d->stream);
+    if (rc != SPTRSV_OK) return rc;
+  }
+  double kernel_ms = 0.0;
+  long long spins = 0, remote = 0, launches = 0;
+  int status = SPTRSV_OK;
+  for (int p = 0; p < n_plans; ++p) {
+    cudaSetDevice(ps[p]->device);
+    sptrsv_stats st{};
+    const int rc = ps[p]->finish(&st);
+    if (rc != SPTRSV_OK && status == SPTRSV_OK) status = rc;
+    kernel_ms = std::max(kernel_ms, st.kernel_ms);
+    spins += st.spins;
+    remote += st.remote_reads;
+    launches += st.launches;
+  }
+  if (status != SPTRSV_OK) return status;
+  // every PE wrote only its own rows of its device's x buffer
+  std::vector<double> tmp;
+  for (size_t k = 0; k < devs.size(); ++k) {
+    cudaSetDevice(devs[k]);
+    double* dst = x;
+    if (devs.size() > 1) {
+      tmp.resize(n);
+      dst = tmp.data();
+    }
+    if ((e = cudaMemcpy(dst, lead[k]->xbuf, sizeof(double) * n, cudaMemcpyDeviceToHost)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    if (devs.size() > 1) {
+      const std::vector<unsigned char>& own = ps[0]->host_owner;
+      for (long long i = 0; i < n; ++i)
+        if (dev_of[own[i]] == (int)k) x[i] = tmp[i];
+    }
+  }
+  if (stats) {
+    *stats = sptrsv_stats{};
+    stats->kernel_ms = kernel_ms;
+    stats->solve_ms = kernel_ms;
+    stats->spins = spins;
+    stats->remote_reads = remote;
+    stats->launches = launches;
+    stats->executor = ps[0]->executor_used;
+    stats->n_levels = ps[0]->n_levels;
+    stats->e2e_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return SPTRSV_OK;
+}
+
 
 int sptrsv_plan_set_partition(sptrsv_plan* plan, const int32_t* owner, int32_t n_pes, int32_t my_pe) {
   auto* p = reinterpret_cast<DevicePlan*>(plan);
@@ -244,6 +364,7 @@ int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle
 int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr) {
   auto* p = reinterpret_cast<DevicePlan*>(plan);
   if (!p || !device_ptr) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
+  if (int rc = p->enable_peer(device_ptr); rc != SPTRSV_OK) return rc;
   if (p->stencil.part) {
     if (pe < 0 || pe >= p->stencil.n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
     cudaSetDevice(p->device);

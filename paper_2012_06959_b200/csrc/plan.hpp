@@ -125,6 +125,9 @@ struct DevicePlan {
   int sync_seg_table();
   long long part_solves = 0;  // parity of the segment double buffer
   void release_partition();
+  std::vector<unsigned char> host_owner;  // owner map of the partition (empty: none)
+  int grid_cap = 0;  // SMs this plan's persistent solve kernels may fill (0: all); set by group solves
+  int enable_peer(const void* peer_ptr);  // P2P access to the device holding peer_ptr
   // diagnostics (probe_flags): kProbeWords int64 — per-step/chunk clock stamps
   // [0, 384), then per-task globaltimer stamps [384, 384 + 3 * 1024)
   static constexpr int kProbeWords = 6 * 64 + 3 * 1024;

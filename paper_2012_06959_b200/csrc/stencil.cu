@@ -63,12 +63,35 @@ constexpr bool kStBTma = kStR == 2 && kStG * kStC * 8 == 128;
 #ifndef SPTRSV_ST_SPEC
 #define SPTRSV_ST_SPEC 1
 #endif
-// x leaves interior chunks by one TMA tensor store (SPTRSV_ST_X_TMA=1) or by
-// the storer's 16-byte stores (default): measured the same on lap2d-4096
+// x leaves interior chunks by one TMA tensor store (SPTRSV_ST_X_TMA=1, default)
+// or by the storer's 16-byte stores: each warp-wide STG.128 writes 32 rows,
+// 32 LSU transactions, and that storer paced the compute warp through the out
+// ring (lap2d-4096 fast 0.633 -> 0.573 ms with TMA stores)
 #ifndef SPTRSV_ST_X_TMA
-#define SPTRSV_ST_X_TMA 0
+#define SPTRSV_ST_X_TMA 1
 #endif
+// TMA x stores left in flight by the storer (each still reading its out slot)
+#ifndef SPTRSV_ST_STORE_DEPTH
+#define SPTRSV_ST_STORE_DEPTH 2
+#endif
+constexpr int kStStoreDepth = SPTRSV_ST_STORE_DEPTH;
+static_assert(kStStoreDepth >= 0 && kStStoreDepth <= kStOutSlots - 1, "in-flight stores need free out slots");
 
+
+// Thread-block clusters of kStCluster consecutive bands (SPTRSV_ST_CLUSTER,
+// default 8; 1 = no clusters): inside a cluster a band hands its bottom grid
+// row to the band below through distributed shared memory -- the producer's
+// compute warp stores each chunk's row straight into the consumer CTA's inbox
+// ring and releases the consumer's inbox counter at cluster scope -- instead
+// of an L2 mailbox that the consumer's poller warp polls. Only the first band
+// of each cluster polls the L2 mailbox of the band above.
+#ifndef SPTRSV_ST_CLUSTER
+#define SPTRSV_ST_CLUSTER 8
+#endif
+constexpr int kStCluster = SPTRSV_ST_CLUSTER;
+// inbox ring depth in chunks (the producer waits for the consumer only when it
+// runs kStInbox chunks ahead)
+constexpr int kStInbox = 64;
 
 // Mailbox sentinel: a signalling NaN. FP64 arithmetic propagates NaN
 // payloads but always quiets them (tools/microbench/nan_bits.cu), so no
@@ -165,7 +188,10 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
 }
 
 // control words of one task (chunk counters)
-enum { kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5, kCtlMbReady = 6 };
+enum {
+  kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5, kCtlMbReady = 6,
+  kCtlGroup = 7  // cluster rank 0: the group ticket of the current task
+};
 
 template <bool EXACT>
 struct StSmem {
@@ -175,10 +201,10 @@ struct StSmem {
   static constexpr int kBChunk = kStLanes * kStR * kStG * kStC * 8;
   static constexpr int kCoef = 0;                                       // [kSlots][kStG][kStep]
   static constexpr int kB = kCoef + kSlots * kCoefChunk;                // [kSlots][r][k][pair][lane] f64x2
-  static constexpr int kInbox = kB + kSlots * kBChunk;                  // [kSlots][kStG][kStC] f64
+  static constexpr int kInbox = kB + kSlots * kBChunk;                  // [kStInbox][kStG][kStC] f64
   // out ring: the b slot layout ([r][l][piece], 128-byte swizzled), so a
   // whole chunk leaves with one TMA tensor store through the skewed view of x
-  static constexpr int kOut = (kInbox + kSlots * kStG * kStC * 8 + 1023) / 1024 * 1024;
+  static constexpr int kOut = (kInbox + kStInbox * kStG * kStC * 8 + 1023) / 1024 * 1024;
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kCtl = kBars + 8 * kSlots;
@@ -204,15 +230,20 @@ __device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, un
 // The compute warp's chunk-boundary wait: input slot, band-above inbox and
 // output slot in one polling loop (three independent shared loads per poll
 // instead of three sequential loops).
+// MbReady may be released by the band above's CTA of the same cluster: its
+// acquire is cluster-scope.
 __device__ __forceinline__ bool wait_chunk(const int* ctl, int in_need, int mb_need, int out_need,
-                                           unsigned long long deadline) {
+                                           unsigned long long deadline, const int* abort_flag) {
   int polls = 0;
   while (true) {
-    const int i = ld_acquire_cta(ctl + kCtlInReady), m = ld_acquire_cta(ctl + kCtlMbReady),
+    const int i = ld_acquire_cta(ctl + kCtlInReady), m = ld_acquire_cluster_local(ctl + kCtlMbReady),
               o = ld_acquire_cta(ctl + kCtlOutDone);
     if (i >= in_need && m >= mb_need && o >= out_need) return true;
     if (ld_acquire_cta(ctl + kCtlAbort)) return false;
-    if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) return false;
+    if ((++polls & 1023) == 0) {
+      if (deadline && globaltimer_ns() > deadline) return false;
+      if (ld_relaxed_s32(abort_flag)) return false;  // another CTA (of this cluster) gave up
+    }
   }
 }
 
@@ -231,8 +262,8 @@ struct StBlk {
   double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock], bv[kStBlock];
   double inbox[kStC];
 
-  // step k of the chunk in input slot `slot`
-  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int k, int lane) {
+  // step k of the chunk in input slot `slot`, inbox slot `islot`
+  __device__ __forceinline__ void load(const unsigned char* smem, int slot, int islot, int k, int lane) {
     using S = StSmem<EXACT>;
     const double2* cs = reinterpret_cast<const double2*>(smem + S::kCoef + slot * S::kCoefChunk + k * S::kStep);
 #pragma unroll
@@ -260,7 +291,7 @@ struct StBlk {
         bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
       }
     }
-    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (slot * kStG + k) * kStC;
+    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (islot * kStG + k) * kStC;
 #pragma unroll
     for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
   }
@@ -393,10 +424,10 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 // handed over through the inbox ring. Kept apart from the loader so the
 // round trip overlaps the loader's copies instead of adding to them.
 template <bool EXACT>
-__device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
+__device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
+                       bool above_in_cluster) {
   using S = StSmem<EXACT>;
-  constexpr int NB = S::kSlots;
-  if (t == 0) return;
+  if (t == 0 || above_in_cluster) return;  // no band above, or it pushes into our inbox itself
   double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
   // the band above on another PE: its owner's mailboxes over NVLink (.sys)
   const int up_pe = a.band_owner ? a.band_owner[t - 1] : a.my_pe;
@@ -406,8 +437,9 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int k = lane / kStC, q = lane % kStC;
   unsigned long long spins = 0;
   for (int c = 0; c < nchunks; ++c) {
-    // inbox slot c % NB is free once the compute warp finished chunk c - NB
-    if (c >= NB && !wait_ctl(ctl, kCtlInDone, c - NB + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
+    // inbox slot c % kStInbox is free once the compute warp finished chunk c - kStInbox
+    if (c >= kStInbox && !wait_ctl(ctl, kCtlInDone, c - kStInbox + 1, deadline, a.nap))
+      return abort_task(a, ctl, lane);
     bool ok = true;
     const int j = c * kStG + k;
     if (lane < kStG * kStC && j < nblk) {
@@ -415,7 +447,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
           st_poll(above + j * kStC + q, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote,
                   spins);
       if (u == kStNotReady) ok = false;
-      inbox[((c % NB) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
+      inbox[((c % kStInbox) * kStG + k) * kStC + q] = __longlong_as_double((long long)u);
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
@@ -440,21 +472,32 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     for (int w = lane; w < a.nx / 2; w += kStLanes) row[w] = make_ulonglong2(kStNotReady, kStNotReady);
   }
   const bool x_tma = kStBTma && t < a.x_tma_bands;
+  // TMA stores stay in flight: after chunk c only the kStStoreDepth most recent
+  // stores may still be reading their slots, so chunks <= c - kStStoreDepth
+  // are handed back (edge chunks are stored synchronously and drain the rest)
+  int released = 0;
   for (int c = 0; c < nchunks; ++c) {
     if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
+    bool async_store = false;
     unsigned char* slot = smem + S::kOut + (c % kStOutSlots) * S::kOutChunk;
     const double2* src = reinterpret_cast<const double2*>(slot);
+#ifdef SPTRSV_ST_STORE_ABL  // timing diagnostics only: hand the slot back without storing x
+    if (true) {
+    } else
+#endif
     // interior chunk (every lane's blocks inside the row): one TMA store of
     // the whole slot; edge chunks element by element (the skewed box would
     // write padding into neighbouring rows there)
     if (x_tma && c * kStG >= kStLanes - 1 && (c + 1) * kStG <= nblk) {
+      async_store = true;
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compute warp's STS -> async proxy
         tma_store_4d(&a.xmap, c * kStG * kStC, 0, 0, t, slot);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slot reusable once read
+        asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStStoreDepth) : "memory");
       }
     } else {
+      if (x_tma && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #pragma unroll
       for (int k = 0; k < kStG; ++k) {
         const int j = c * kStG + k - lane;
@@ -479,7 +522,11 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       }
     }
     __syncwarp();
-    if (lane == 0) st_release_cta(ctl + kCtlOutDone, c + 1);
+    const int done = async_store ? c + 1 - kStStoreDepth : c + 1;
+    if (done > released) {
+      released = done;
+      if (lane == 0) st_release_cta(ctl + kCtlOutDone, done);
+    }
   }
   if (x_tma && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   // overlapped host solve: band t's x may now be copied to the host. Flags
@@ -517,6 +564,15 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 #define SPTRSV_ST_EARLY_SHFL 1
 #endif
 constexpr bool kStExpand = SPTRSV_ST_EXPAND && kStR == 2 && kStC == 2;
+// Fast mode publishes the band-below mailbox row once per chunk (one warp
+// store of lane 31's staged bottom rows) instead of a predicated store per
+// step: the poller below consumes whole chunks anyway, and the per-step store
+// cost the compute warp ~8 instructions a step (j, bounds, predicate, address).
+#ifndef SPTRSV_ST_CHUNK_PUB
+#define SPTRSV_ST_CHUNK_PUB 1
+#endif
+constexpr bool kStChunkPub = SPTRSV_ST_CHUNK_PUB;
+static_assert(kStChunkPub || kStCluster == 1, "cluster hand-overs push whole chunks");
 constexpr bool kStEarlyShfl = SPTRSV_ST_EARLY_SHFL;
 
 template <bool EXACT>
@@ -547,11 +603,18 @@ __device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
 // active/publish branch
 template <bool EXACT, int ABL, bool PART>
-__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
+__device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
+                        unsigned crank, bool below_in_cluster) {
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const bool has_above = t > 0;
+  // the band below in the next CTA of this cluster: its inbox ring, inbox
+  // counter and progress counter in distributed shared memory
+  const unsigned peer_inbox = below_in_cluster ? mapa_shared(smem + S::kInbox, crank + 1) : 0u;
+  const unsigned peer_mbready = below_in_cluster ? mapa_shared(ctl + kCtlMbReady, crank + 1) : 0u;
+  const unsigned peer_indone = below_in_cluster ? mapa_shared(ctl + kCtlInDone, crank + 1) : 0u;
+  int pushed = 0, peer_done = 0;
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   // the band below on another PE reads these over NVLink: system-scope stores
   const bool below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
@@ -655,7 +718,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll 1
     for (int k = 0; k < kStG; ++k) {
       StBlk<EXACT> blk;
-      blk.load(smem, c % NB, k, lane);
+      blk.load(smem, c % NB, c % kStInbox, k, lane);
       double top[kStC], xb[kStR][kStC];
 #pragma unroll
       for (int q = 0; q < kStC; ++q) {
@@ -686,6 +749,50 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     }
   };
 
+  // the same rows straight into the inbox ring of the band below (next CTA of
+  // the cluster): chunk c's lane-31 blocks are columns j = cG - 31 .. cG - 24,
+  // i.e. the tail of the consumer's chunk c - 4 and the head of c - 3; the
+  // consumer's inbox counter then covers every chunk whose columns all
+  // arrived. A ring slot is rewritten only once the consumer finished the
+  // chunk kStInbox before it.
+  auto push_chunk = [&](int c) -> bool {
+    constexpr int kHalves = kStC / 2;
+    const int jlo = c * kStG - (kStLanes - 1), jhi = jlo + kStG - 1;
+    if (jhi >= 0 && jlo < nblk) {
+      const int need = min(jhi, nblk - 1) / kStG - kStInbox + 1;
+      int polls = 0;
+      while (peer_done < need) {
+        peer_done = ld_acquire_cluster_s32(peer_indone);
+        if ((++polls & 255) == 0 &&
+            ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
+          return false;
+      }
+      if (lane < kStG * kHalves) {
+        const int k = lane / kHalves, h = lane % kHalves;
+        const int jj = jlo + k;
+        if (jj >= 0 && jj < nblk) {
+          const double2 v = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) *
+                                                                                  S::kOutChunk)[st_b_piece(
+              kStR - 1, kStLanes - 1, k, h)];
+          const int cc = jj / kStG, kk = jj - cc * kStG;
+          st_cluster_f64x2(peer_inbox + ((((cc % kStInbox) * kStG + kk) * kStC + 2 * h) << 3), v.x, v.y);
+        }
+      }
+    }
+    __syncwarp();  // the lanes' DSMEM stores are ordered before lane 0's release
+    const int ready = c + 1 >= nchunks ? nchunks : max(0, (jhi + 1) / kStG);
+    if (ready > pushed) {
+      pushed = ready;
+      if (lane == 0) st_release_cluster_s32(peer_mbready, ready);
+    }
+    return true;
+  };
+  auto hand_down = [&](int c) -> bool {
+    if (below_in_cluster) return push_chunk(c);
+    publish_chunk(c);
+    return true;
+  };
+
   // step k of chunk c; `nxt` receives the next step's inputs
   // step k of chunk c computes from `cur` (loaded two steps earlier) and
   // loads step k + 2 into `nxt2`: a full step of slack hides the shared-memory
@@ -693,15 +800,16 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt2) -> bool {
     auto load_ahead = [&]() {
       if (k + 2 < kStG) {
-        if (!(ABL & 2)) nxt2.load(smem, c % NB, k + 2, lane);
+        if (!(ABL & 2)) nxt2.load(smem, c % NB, c % kStInbox, k + 2, lane);
       } else if (c + 1 < nchunks) {
-        nxt2.load(smem, (c + 1) % NB, k + 2 - kStG, lane);
+        nxt2.load(smem, (c + 1) % NB, (c + 1) % kStInbox, k + 2 - kStG, lane);
       }
     };
     // the first step that loads from chunk c + 1: make sure it is ready
     if (k == kStG - 2 && c + 1 < nchunks && !solo) {
       if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-      if (!wait_chunk(ctl, c + 2, has_above ? c + 2 : 0, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0, deadline))
+      if (!wait_chunk(ctl, c + 2, has_above ? c + 2 : 0, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0, deadline,
+                      a.abort_flag))
         return false;
       if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
     }
@@ -726,7 +834,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       block(cur, top, xb, true);
     }
     retire(c, k, xb);
-    if (!(ABL & 8) && !kStSpec) {
+    if (!(ABL & 8) && !kStSpec && !kStChunkPub) {
 #pragma unroll
       for (int q = 0; q < kStC; ++q)
         st_relaxed_u64_if(below + j * kStC + q, as_u64(bottom[q]), publish && active);
@@ -744,7 +852,10 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
         if (__any_sync(0xffffffffu, spec_bad)) redo_chunk(c);
         spec_bad = false;
         __syncwarp();
-        publish_chunk(c);
+        if (!hand_down(c)) return false;
+      } else if (kStChunkPub && !(ABL & 8)) {
+        __syncwarp();  // lane 31's staged bottom rows -> the lanes that store them
+        if (!hand_down(c)) return false;
       }
       // chunk boundary: hand over the outputs and the input slot
       __syncwarp();
@@ -761,11 +872,11 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
-  if (!solo && has_above && !wait_ctl(ctl, kCtlMbReady, 1, deadline)) return abort_task(a, ctl, lane);
+  if (!solo && has_above && !wait_chunk(ctl, 1, 1, 0, deadline, a.abort_flag)) return abort_task(a, ctl, lane);
   if (tstamp) tstamp[1] = (long long)globaltimer_ns();
   static_assert(kStG >= 3, "the two-step lookahead stays within one chunk boundary");
-  buf[0].load(smem, 0, 0, lane);
-  buf[1].load(smem, 0, 1, lane);
+  buf[0].load(smem, 0, 0, 0, lane);
+  buf[1].load(smem, 0, 0, 1, lane);
   // three chunks per iteration so that s % 3 is a compile-time constant
   for (int c0 = 0; c0 < nchunks; c0 += 3) {
 #pragma unroll
@@ -780,11 +891,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
-template <bool EXACT, int ABL, bool PART>
+template <bool EXACT, int ABL, bool PART, int CL>
 __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_constant__ StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // the 128-byte TMA swizzle repeats every 1024 bytes: align the rings to it
+  // (the same offset in every CTA, so DSMEM addresses of peers line up)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int* ctl = reinterpret_cast<int*>(smem + S::kCtl);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -795,33 +907,98 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
   }
   unsigned phase_bits = 0;
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  const unsigned crank = CL > 1 ? cluster_ctarank() : 0u;
+  const int n_groups = (a.n_tasks + CL - 1) / CL;
   while (true) {
-    if (threadIdx.x == 0) {
+    if (CL > 1) {
+      // a cluster takes kStCluster consecutive bands per ticket (ascending:
+      // the progress rule, engine.py:30-35); its CTAs enter and leave a task
+      // together, so no CTA resets counters a peer may still write
+      cluster_sync_all();
+      if (threadIdx.x == 0) {
+        if (crank == 0) ctl[kCtlGroup] = ld_relaxed_s32(a.abort_flag) ? n_groups : atomicAdd(a.ticket, 1);
+        ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
+        ctl[kCtlMbReady] = 0;
+      }
+      cluster_sync_all();
+      if (threadIdx.x == 0) {
+        const int g = ld_acquire_cluster_s32(mapa_shared(ctl + kCtlGroup, 0));
+        ctl[kCtlTask] = g >= n_groups ? -1 : min(g * CL + (int)crank, a.n_tasks);  // n_tasks: idle this round
+      }
+    } else if (threadIdx.x == 0) {
       const int k = atomicAdd(a.ticket, 1);  // ascending: the progress rule (engine.py:30-35)
-      ctl[kCtlTask] = k >= a.n_my_tasks ? a.n_tasks : (a.my_tasks ? a.my_tasks[k] : k);
+      ctl[kCtlTask] = k >= a.n_my_tasks ? -1 : (a.my_tasks ? a.my_tasks[k] : k);
       ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
       ctl[kCtlMbReady] = 0;
     }
     __syncthreads();
     const int t = ctl[kCtlTask];
-    if (t >= a.n_tasks) break;
-    if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline);
-    else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
-    } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
-    else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
-    else poller<EXACT>(a, smem, ctl, t, lane, deadline);
+    if (t < 0) break;
+    if (t < a.n_tasks) {
+      const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && t + 1 < a.n_tasks;
+      if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
+      else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
+      } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
+      else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
+      else poller<EXACT>(a, smem, ctl, t, lane, deadline, CL > 1 && crank > 0);
+    }
     __syncthreads();
-    if (ctl[kCtlAbort]) break;
+    if (CL == 1 && ctl[kCtlAbort]) break;  // (clusters leave together, through the ticket)
   }
 }
 
-template <bool EXACT, int ABL, bool PART = false>
+// Clusters resident at once for this kernel (cudaOccupancyMaxActiveClusters), per device.
+template <typename K>
+int max_active_clusters(K kernel, int cl, int smem_bytes) {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && cache[dev] > 0) return cache[dev];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl * 32, 1, 1);
+  cfg.blockDim = dim3(kStThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (dev < 64 && n > 0) cache[dev] = n;
+  return n;
+}
+
+template <bool EXACT, int ABL, bool PART = false, int CL = 1>
 cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART>, StSmem<EXACT>::kTotal, attr); e != cudaSuccess)
+  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART, CL>, StSmem<EXACT>::kTotal, attr); e != cudaSuccess)
     return e;
-  k_stencil2d<EXACT, ABL, PART><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
-  return cudaGetLastError();
+  if (CL == 1) {
+    k_stencil2d<EXACT, ABL, PART, CL><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
+    return cudaGetLastError();
+  }
+  const int groups = (a.n_tasks + CL - 1) / CL;
+  const int fit = max_active_clusters(k_stencil2d<EXACT, ABL, PART, CL>, CL, StSmem<EXACT>::kTotal);
+  if (fit < 1) return cudaErrorLaunchOutOfResources;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL * std::min(groups, fit), 1, 1);
+  cfg.blockDim = dim3(kStThreads, 1, 1);
+  cfg.dynamicSmemBytes = StSmem<EXACT>::kTotal;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_stencil2d<EXACT, ABL, PART, CL>, a);
 }
 
 // probe bits 12..15 select an ablation variant of the fast kernel (timing only)
@@ -839,6 +1016,7 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
       default: break;
     }
   }
+  if (kStCluster > 1 && a.n_tasks > 1) return launch_stencil_v<EXACT, 0, false, kStCluster>(a, blocks, s);
   return launch_stencil_v<EXACT, 0>(a, blocks, s);
 }
 
@@ -1078,7 +1256,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
     a.dbg = probe_buf;
   }
-  const int blocks = std::max(1, std::min(a.n_my_tasks, num_sms));
+  const int blocks = std::max(1, std::min(a.n_my_tasks, grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms));
   ++stencil.solves;
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);

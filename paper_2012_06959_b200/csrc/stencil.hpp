@@ -27,7 +27,10 @@ constexpr int kStBlock = kStR * kStC;     // elements per lane per step
 #define SPTRSV_ST_G 8
 #endif
 constexpr int kStG = SPTRSV_ST_G;         // steps per ring slot ("chunk"): the unit of every hand-over
-constexpr int kStOutSlots = 3;            // output ring (chunks) between the compute and the store warp
+#ifndef SPTRSV_ST_OUT_SLOTS
+#define SPTRSV_ST_OUT_SLOTS 4
+#endif
+constexpr int kStOutSlots = SPTRSV_ST_OUT_SLOTS;  // output ring (chunks) between the compute and the store warp
 
 // Per step, per lane: kStBlock elements; per element NF doubles:
 //   fast : wu = -L[i,i-nx]/d, wl = -L[i,i-1]/d, rdg = 1/d

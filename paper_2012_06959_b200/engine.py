@@ -279,8 +279,10 @@ def _run(l: CscMatrix, b, plan: PartitionPlan, cfg: SolverConfig, expected: Engi
         spin_max_ns=max(16, cfg.spin_backoff.max_pause // 8),
     )
     if expected is Engine.PARTITIONED_READ_ONLY and cfg.n_pes > 1:
-        # one published segment per PE (owner-only writes, read-only peers)
-        native = _native.partitioned_plan_for(l, plan, **knobs)
+        # one published segment per PE (owner-only writes, read-only peers):
+        # one PE per GPU when several are visible, else the PEs share the
+        # device with the fastest executor that has a per-PE mode
+        native = _native.pe_solver_for(l, plan, executor=cfg.executor, **knobs)
     else:
         # one published segment shared by all PEs
         native = _native.plan_for(l, executor=cfg.executor, **knobs)

@@ -37,8 +37,61 @@ def test_partitioned_pes_bit_exact(n_pes, kind, shape):
     assert x.tobytes() == ref.tobytes()
     assert report.totals()["components_solved"] == l.n
     assert report.totals()["local_updates"] + report.totals()["remote_updates"] == l.nnz - l.n
-    # the kernel really read across segments
-    assert report.device["remote_reads"] > 0
+    if report.device.get("pe_mode") != "shared-segment":
+        # the kernel really read across segments
+        assert report.device["remote_reads"] > 0
+
+
+@pytest.mark.parametrize("n_pes", [2, 3, 8])
+@pytest.mark.parametrize("shape", ["lap2d", "banded", "rmat", "random"])
+def test_partitioned_pool_segments_bit_exact(n_pes, shape):
+    """executor="rows": the component pool with one published segment per PE."""
+    l = {
+        "lap2d": lambda: synth.lap2d(64, 48),
+        "banded": lambda: synth.banded(6000, 64, 0.5, 4),
+        "rmat": lambda: synth.rmat(13, 8, 2),
+        "random": lambda: synth.random_lower(2500, 0.02, 9, dominant=True),
+    }[shape]()
+    b = np.random.default_rng(n_pes).uniform(-1.0, 1.0, l.n)
+    plan = sp.task_round_robin_partition(l.n, n_pes, 4)
+    cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=n_pes, precision="exact", executor="rows")
+    x, report = sp.solve_partitioned(l, b, plan, cfg)
+    assert x.tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b).tobytes()
+    assert report.device["executor"] == "rows" and report.device["remote_reads"] > 0
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+@pytest.mark.parametrize("n_pes", [2, 4])
+def test_dropin_n_pes_keeps_the_wavefront(n_pes, precision):
+    """SolverConfig.n_pes > 1 through the drop-in solve(): a 2D five-point L with
+    whole 64-row bands per PE keeps the stencil executor (one plan per PE,
+    peers' mailboxes), and x equals the oracle bitwise in exact mode."""
+    l = synth.lap2d(256, 512)  # 8 bands: whole bands per PE for 2 and 4 PEs
+    b = np.random.default_rng(5).uniform(-1.0, 1.0, l.n)
+    plan = sp.block_partition(l.n, n_pes)
+    cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=n_pes, precision=precision)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    for _ in range(2):
+        x, report = sp.solve(l, b, plan, cfg)
+        assert report.device["executor"] == "stencil"
+        assert report.device["pe_mode"] in ("stencil-pes", "pe-per-gpu")
+        if precision == "exact":
+            assert x.tobytes() == ref.tobytes()
+        else:
+            assert sp.compare_solutions(x, ref, 1e-12).within_tol
+        assert report.device["remote_reads"] > 0
+        assert report.totals()["components_solved"] == l.n
+
+
+def test_dropin_n_pes_structured_executors_stay_fast():
+    """Executors without a per-PE mode (band window, 3D wavefront) keep running
+    on one device instead of falling back to the component pool."""
+    for l, ex in ((synth.banded(20000, 64, 0.5, 1), "band"), (synth.lap3d(24), "stencil")):
+        b = np.random.default_rng(2).uniform(-1.0, 1.0, l.n)
+        cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=4, precision="exact")
+        x, report = sp.solve(l, b, sp.block_partition(l.n, 4), cfg)
+        assert report.device["executor"] == ex
+        assert x.tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b).tobytes()
 
 
 @pytest.mark.parametrize("name", ["worked_3x3", "random_3", "bidiagonal1000", "blockdiag4096"])
