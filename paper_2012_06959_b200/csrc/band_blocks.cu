@@ -1,0 +1,346 @@
+// Fast-mode band executor by row blocks (banded-8M: bandwidth 64, ~4.7 M
+// levels for 8.4 M rows).
+//
+// The window kernel (solve_band.cu) is one warp walking every column in order:
+// a shuffle and an FMA per row on one SM, ~67 ns a row, 0.32 s for 8.4 M rows.
+// Fast mode (pre-scaled rows, FMA; the 1e-12 contract) may re-associate, so
+// the recurrence is cut into row blocks of S rows (k = 0 .. nblk-1, rows
+// [kS, kS + S)). With bandwidth W = 64 a block depends on the blocks before
+// it only through x of the W rows just above it (the previous block's tail):
+//
+//   x_k = c_k + N_k t_{k-1},   c_k = (I - W_kk)^{-1} (rd * b)_k,
+//                              t_{k-1} = x of rows [kS - W, kS)
+//
+// where N_k (S x W) is how x_k responds to the W coupling values (built once
+// per plan, only its W x W tail is kept). One solve is then three kernels:
+//   K1  every block in parallel, one warp each: the band window sweep of the
+//       block with zero coupling; keeps c of the block's tail rows;
+//   K2  one CTA, nblk - 1 sequential steps: t_k = c_k^tail + N_k^tail t_{k-1}
+//       (a 64 x 64 matvec per step from a TMA-fed ring) -- the only
+//       sequential part, nblk steps instead of n rows;
+//   K3  every block in parallel again: the same sweep, its first W rows
+//       seeded with the coupling terms of t_{k-1}; writes x.
+// K1 and K3 each stream the dense band once (HBM-bound); K2 is latency-bound
+// at ~250 cycles per step. Exact mode keeps the column-ordered window kernel
+// (the serial oracle's summation order).
+#include <algorithm>
+#include <vector>
+#include "plan.hpp"
+#include "kernels.cuh"
+#include "ptx.cuh"
+
+namespace sptrsv {
+
+int plan_fail(int code, const char* msg);
+
+namespace {
+
+constexpr int kW = 64;           // bandwidth = window
+constexpr int kBBWarps = 4;      // sweep warps per CTA (one block each)
+constexpr int kPf = 16;          // coefficient prefetch distance (columns)
+constexpr int kTSlots = 4;       // K2 ring depth (steps)
+constexpr int kTailBytes = kW * kW * 8;
+
+// ---- setup: N_k tail ------------------------------------------------------
+// One CTA of two warps per block; lane m (of warp h) follows coupling column
+// m = 32h + lane: its response N[i][m] for the block's rows i, in a window of
+// 64 register accumulators (row i at slot i mod 64), pushed column by column
+// exactly like the solve: N[j][m] is final when column j is reached, then
+// acc[i] += w_ij N[j][m] for i = j+1 .. j+64. The band columns are staged in
+// shared memory (broadcast reads). Output layout (K2's): [h][i][r] of double2
+// (m = 32h + 2i + e), r = tail row.
+constexpr int kNtSmem = 2 * kW * kW * 8;  // two 64-column chunks of the band
+
+__global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef, long long n, int S, int nblk,
+                                                 double* __restrict__ nt) {
+  extern __shared__ __align__(16) double cs_raw[];
+  double (*cs)[kW][kW] = reinterpret_cast<double (*)[kW][kW]>(cs_raw);
+  // blocks 1 .. nblk - 2: block 0 has no coupling and the last block's tail
+  // feeds no further block (it is also the only block that may be partial)
+  const int k = blockIdx.x + 1;
+  if (k >= nblk - 1) return;
+  const long long s0 = (long long)k * S;
+  const int tid = threadIdx.x, h = tid >> 5, lane = tid & 31, m = 32 * h + lane;
+  double acc[kW];
+#pragma unroll
+  for (int u = 0; u < kW; ++u) acc[u] = 0.0;
+  const int nchunk = S / kW + 1;  // the coupling columns [s0 - 64, s0), then the block's
+  auto stage = [&](int c, int buf) {
+    const double2* src = reinterpret_cast<const double2*>(coef + (size_t)(s0 - kW + (long long)c * kW) * kW);
+    double2* dst = reinterpret_cast<double2*>(&cs[buf][0][0]);
+    for (int w = tid; w < kW * kW / 2; w += 64) dst[w] = src[w];
+  };
+  stage(0, 0);
+  __syncthreads();
+  for (int c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) stage(c + 1, (c + 1) & 1);
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const long long j = s0 - kW + (long long)c * kW + u;
+      // coupling column s0 - 64 + m has response 1 in lane m, 0 elsewhere
+      const double nj = c == 0 ? (u == m ? 1.0 : 0.0) : acc[u];
+      if (c > 0 && j >= s0 + S - kW && j < n) {
+        const int r = (int)(j - (s0 + S - kW)), i = (m & 31) >> 1, e = m & 1;
+        nt[(size_t)(k - 1) * (kTailBytes / 8) + ((h * 16 + i) * kW + r) * 2 + e] = nj;
+      }
+      acc[u] = 0.0;  // row j leaves the window; row j + 64 enters in its slot
+      const double* cj = &cs[c & 1][u][0];
+#pragma unroll
+      for (int d = 1; d <= kW; ++d) acc[(u + d) & (kW - 1)] = __fma_rn(cj[d - 1], nj, acc[(u + d) & (kW - 1)]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K1 / K3: one warp per block, the band window sweep --------------------
+struct SweepArgs {
+  const double* coef;  // [n_pad][64]: w(j + d, j) at [j][d - 1] (pre-scaled, fast mode)
+  const double* b;
+  const double* rdg;
+  const double* tt;    // K3: t_k = x of block k's tail rows, [nblk][64] (null in K1)
+  double* out;         // K1: c tails [nblk][64]; K3: x
+  long long n;
+  int S, nblk;
+};
+
+template <bool COUPLED>
+__global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constant__ SweepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kBBWarps + (threadIdx.x >> 5);
+  if (k >= a.nblk) return;
+  const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
+  // lane owns window rows 2 lane + s (s = 0, 1) of each 64-row window
+  double acc[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const long long i = s0 + 2 * lane + s;
+    acc[s] = i < s1 ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
+    if (COUPLED && k > 0 && i < s1) {
+      // coupling terms of the previous block's tail: sum_{j in [s0-64, s0)} w_ij t_j,
+      // in ascending column order
+      const double* tp = a.tt + (size_t)(k - 1) * kW;
+      for (int q = 0; q < kW; ++q) {
+        const long long j = s0 - kW + q;
+        const long long d = i - j;
+        if (d >= 1 && d <= kW) acc[s] = __fma_rn(a.coef[(size_t)j * kW + d - 1], tp[q], acc[s]);
+      }
+    }
+  }
+  // next window's b * rd of the lane's rows (one iteration ahead)
+  double nb[2];
+  const int ncol = (int)(s1 - s0);
+  // coefficient register ring: column j's two entries of this lane, kPf columns ahead
+  double cf[kPf][2];
+  auto cload = [&](long long j, double (&dst)[2], int p) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int d = ((2 * lane + s - p - 1) & (kW - 1)) + 1;
+      dst[s] = j < s1 ? __ldg(a.coef + (size_t)j * kW + d - 1) : 0.0;
+    }
+  };
+#pragma unroll
+  for (int u = 0; u < kPf; ++u) cload(s0 + u, cf[u], u);
+  for (int c0 = 0; c0 < ncol; c0 += kW) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const long long i = s0 + c0 + kW + 2 * lane + s;
+      nb[s] = i < s1 ? __dmul_rn(__ldg(a.b + i), __ldg(a.rdg + i)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const long long j = s0 + c0 + u;
+      const int owner = u >> 1, os = u & 1;
+      double w[2] = {cf[u % kPf][0], cf[u % kPf][1]};
+      cload(j + kPf, cf[u % kPf], (u + kPf) & (kW - 1));
+      const double xj = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
+      if (lane == owner && j < s1) {
+        if (COUPLED) {
+          a.out[j] = xj;
+        } else if (j >= s0 + a.S - kW) {
+          a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;  // c of the tail rows
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        double v = acc[s];
+        if (lane == owner && s == os) v = nb[s];  // row j leaves, row j + 64 enters
+        acc[s] = __fma_rn(w[s], xj, v);
+      }
+    }
+  }
+}
+
+// ---- K2: the tail recurrence (one CTA) -------------------------------------
+struct TailArgs {
+  const double* nt;   // [nblk - 2] tails (blocks 1 .. nblk-2), K2 layout
+  const double* ct;   // [nblk][64] c tails (K1)
+  double* tt;         // [nblk][64] t
+  int nblk;
+  DeviceStatus* status;
+  int* abort_flag;
+  unsigned long long timeout_ns;
+};
+
+struct TSmem {
+  static constexpr int kN = 0;                                 // [slot] 32 KB tail of N
+  static constexpr int kC = kN + kTSlots * kTailBytes;         // [slot] 512 B c tail
+  static constexpr int kT = kC + kTSlots * kW * 8;             // [2][64] t double buffer
+  static constexpr int kPart = kT + 2 * kW * 8;                // [64] partial sums
+  static constexpr int kBars = kPart + kW * 8;                 // [slot] mbarriers
+  static constexpr int kCtl = kBars + 8 * kTSlots;             // [0] steps done
+  static constexpr int kTotal = kCtl + 64;
+};
+
+// threads 0..127: thread (r = tid % 64, h = tid / 64) sums the 32 terms of
+// coupling columns [32h, 32h + 32) of tail row r; thread 128 (its own warp)
+// streams N_k / c_k into the ring.
+__global__ void __launch_bounds__(160, 1) k_bb_tail(const __grid_constant__ TailArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + TSmem::kBars);
+  int* ctl = reinterpret_cast<int*>(smem + TSmem::kCtl);
+  double* tb = reinterpret_cast<double*>(smem + TSmem::kT);
+  double* part = reinterpret_cast<double*>(smem + TSmem::kPart);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int q = 0; q < kTSlots; ++q) mbar_init(&bars[q], 1);
+    ctl[0] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < kW) tb[tid] = a.ct[tid];  // t_0 = c_0 tail
+  __syncthreads();
+  if (tid < kW) a.tt[tid] = tb[tid];
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  if (tid >= 128) {
+    if (tid != 128) return;
+    // producer: step k (1 .. nblk-2) uses slot (k - 1) % kTSlots
+    for (int k = 1; k < a.nblk - 1; ++k) {
+      const int q = (k - 1) % kTSlots;
+      if (k - 1 >= kTSlots) {
+        int polls = 0;
+        while (ld_acquire_cta(ctl) < k - kTSlots) {  // the slot's previous step is done
+          if ((++polls & 1023) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
+            return;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[q], kTailBytes + kW * 8);
+      bulk_g2s(smem + TSmem::kN + q * kTailBytes, a.nt + (size_t)(k - 1) * (kTailBytes / 8), kTailBytes, &bars[q]);
+      bulk_g2s(smem + TSmem::kC + q * kW * 8, a.ct + (size_t)k * kW, kW * 8, &bars[q]);
+    }
+    return;
+  }
+  const int r = tid & (kW - 1), h = tid >> 6;
+  unsigned phase = 0;
+  // t_k for blocks 1 .. nblk-2 (the last block's tail is not needed)
+  for (int k = 1; k < a.nblk - 1; ++k) {
+    const int q = (k - 1) % kTSlots;
+    int polls = 0;
+    bool ok = true;
+    while (!mbar_try_wait(&bars[q], (phase >> q) & 1u)) {
+      if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) {
+        ok = false;
+        break;
+      }
+    }
+    if (!ok) {
+      if (tid == 0) {
+        atomicExch(&a.status->code, 5);
+        atomicExch(a.abort_flag, 1);
+      }
+      break;  // (the producer stops at the deadline too)
+    }
+    phase ^= 1u << q;
+    const double2* nq = reinterpret_cast<const double2*>(smem + TSmem::kN + q * kTailBytes) + h * 16 * kW + r;
+    const double* tp = tb + ((k - 1) & 1) * kW + 32 * h;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double2 w = nq[i * kW];
+      s4[i & 3] = __fma_rn(w.x, tp[2 * i], s4[i & 3]);
+      s4[i & 3] = __fma_rn(w.y, tp[2 * i + 1], s4[i & 3]);
+    }
+    const double sum = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
+    if (h == 1) part[r] = sum;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (h == 0) {
+      const double* cq = reinterpret_cast<const double*>(smem + TSmem::kC + q * kW * 8);
+      const double t = __dadd_rn(cq[r], __dadd_rn(sum, part[r]));
+      tb[(k & 1) * kW + r] = t;
+      a.tt[(size_t)k * kW + r] = t;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (tid == 0) st_release_cta(ctl, k);
+  }
+}
+
+}  // namespace
+
+int DevicePlan::build_band_blocks() {
+  cudaError_t e;
+  // rows per block: enough blocks to fill the GPU's warps, at most 4096
+  long long S = kW;
+  while (S < 4096 && (n + S - 1) / S > (long long)num_sms * 8) S *= 2;
+  const int nblk = (int)((n + S - 1) / S);
+  bblk.S = (int)S;
+  bblk.nblk = nblk;
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  if ((e = al((void**)&bblk.nt, (size_t)std::max(nblk - 1, 1) * kTailBytes)) != cudaSuccess ||
+      (e = al((void**)&bblk.ct, sizeof(double) * nblk * kW)) != cudaSuccess ||
+      (e = al((void**)&bblk.tt, sizeof(double) * nblk * kW)) != cudaSuccess ||
+      (e = cudaMemsetAsync(bblk.ct, 0, sizeof(double) * nblk * kW, stream)) != cudaSuccess ||
+      (e = cudaMemsetAsync(bblk.nt, 0, (size_t)std::max(nblk - 1, 1) * kTailBytes, stream)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if (nblk > 2) {
+    static std::atomic<unsigned long long> attr{0};
+    if ((e = set_max_dyn_smem(k_bb_ntail, kNtSmem, attr)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    k_bb_ntail<<<nblk - 2, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  bblk.ready = true;
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s) {
+  if (!bblk.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "band blocks were not built for this plan");
+  cudaError_t e;
+  if ((e = reset_control(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  SweepArgs sa{};
+  sa.coef = band.coef;
+  sa.b = d_b;
+  sa.rdg = rdg;
+  sa.n = n;
+  sa.S = bblk.S;
+  sa.nblk = bblk.nblk;
+  const int grid = (bblk.nblk + kBBWarps - 1) / kBBWarps;
+  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // K1: c tails
+  sa.out = bblk.ct;
+  k_bb_sweep<false><<<grid, 32 * kBBWarps, 0, s>>>(sa);
+  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // K2: tails
+  TailArgs ta{};
+  ta.nt = bblk.nt;
+  ta.ct = bblk.ct;
+  ta.tt = bblk.tt;
+  ta.nblk = bblk.nblk;
+  ta.status = status;
+  ta.abort_flag = abort_flag;
+  ta.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
+  static std::atomic<unsigned long long> attr{0};
+  if ((e = set_max_dyn_smem(k_bb_tail, TSmem::kTotal, attr)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  k_bb_tail<<<1, 160, TSmem::kTotal, s>>>(ta);
+  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // K3: x
+  sa.tt = bblk.tt;
+  sa.out = d_x;
+  k_bb_sweep<true><<<grid, 32 * kBBWarps, 0, s>>>(sa);
+  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  launches = 3;
+  return SPTRSV_OK;
+}
+
+}  // namespace sptrsv

@@ -58,6 +58,7 @@ void DevicePlan::release() {
   stencil3.release();
   push.release();
   band.release();
+  bblk.release();
   split_rows.release();
   release_partition();
   if (ev0) cudaEventDestroy(ev0);
@@ -292,7 +293,7 @@ int DevicePlan::solve_device(const double* d_b, double* d_x, cudaStream_t s) {
   else if (executor_used == SPTRSV_EXECUTOR_STENCIL)
     rc = stencil3.ready ? solve_stencil3d(d_b, d_x, s) : solve_stencil(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_PUSH) rc = solve_push(d_b, d_x, s);
-  else if (executor_used == SPTRSV_EXECUTOR_BAND) rc = solve_band(d_b, d_x, s);
+  else if (executor_used == SPTRSV_EXECUTOR_BAND) rc = bblk.ready ? solve_band_blocks(d_b, d_x, s) : solve_band(d_b, d_x, s);
   else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(d_b, d_x, s);
   else rc = solve_rows(d_b, d_x, s);
   if (rc != SPTRSV_OK) return rc;

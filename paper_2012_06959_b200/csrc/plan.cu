@@ -234,6 +234,11 @@ int DevicePlan::build(const int64_t* col_ptr, const int64_t* row_idx, const doub
         if (rc != SPTRSV_OK) return rc;
       }
       executor_used = SPTRSV_EXECUTOR_BAND;
+      if (opt.precision == SPTRSV_PRECISION_FAST) {  // fast mode: the row-block formulation (band_blocks.cu)
+        rc = build_band_blocks();
+        if (rc != SPTRSV_OK) return rc;
+        mark("band blocks (coupling tails)");
+      }
       return SPTRSV_OK;
     }
     // AUTO prefers lane chains only when every row has at most 8 dependencies

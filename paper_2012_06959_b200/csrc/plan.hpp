@@ -105,6 +105,23 @@ struct DevicePlan {
   int solve_band(const double* d_b, double* d_x, cudaStream_t s);
   int band_levels(int* level_out);
   bool band_narrow(const std::vector<int>& h_rp, const std::vector<int>& h_ci) const;
+  // fast mode: row blocks of S rows coupled through the 64 rows above each
+  // block (band_blocks.cu)
+  struct BandBlocks {
+    bool ready = false;
+    int S = 0, nblk = 0;
+    double* nt = nullptr;  // [nblk - 2] 64 x 64 coupling tails
+    double* ct = nullptr;  // [nblk][64] tails of the uncoupled block solves
+    double* tt = nullptr;  // [nblk][64] tails of x
+    void release() {
+      double* ptrs[] = {nt, ct, tt};
+      for (double* p : ptrs)
+        if (p) cudaFree(p);
+      *this = BandBlocks();
+    }
+  } bblk;
+  int build_band_blocks();
+  int solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s);
   int solve_push(const double* d_b, double* d_x, cudaStream_t s);
 
   // PE partition (partition.cu): each PE owns components (PartitionPlan.owner_arr)

@@ -103,6 +103,27 @@ __device__ __forceinline__ int ld_acquire_cluster_s32(unsigned addr) {
   asm volatile("ld.acquire.cluster.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+// relaxed remote read (no L1 invalidation, unlike acquire at cluster scope)
+__device__ __forceinline__ int ld_relaxed_cluster_s32(unsigned addr) {
+  int v;
+  asm volatile("ld.relaxed.cluster.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+// asynchronous remote store completing `bytes` on the destination CTA's mbarrier
+__device__ __forceinline__ void st_async_f64x2(unsigned addr, double x, double y, unsigned remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(x), "d"(y), "r"(remote_bar)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_test_wait(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
 // this CTA's own counter, written by a peer CTA of the cluster
 __device__ __forceinline__ int ld_acquire_cluster_local(const int* p) {
   int v;

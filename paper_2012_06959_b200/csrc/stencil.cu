@@ -81,12 +81,14 @@ static_assert(kStStoreDepth >= 0 && kStStoreDepth <= kStOutSlots - 1, "in-flight
 // Thread-block clusters of kStCluster consecutive bands (SPTRSV_ST_CLUSTER,
 // default 8; 1 = no clusters): inside a cluster a band hands its bottom grid
 // row to the band below through distributed shared memory -- the producer's
-// compute warp stores each chunk's row straight into the consumer CTA's inbox
-// ring and releases the consumer's inbox counter at cluster scope -- instead
-// of an L2 mailbox that the consumer's poller warp polls. Only the first band
-// of each cluster polls the L2 mailbox of the band above.
+// compute warp writes each chunk's row straight into the consumer CTA's inbox
+// ring with st.async, which completes its bytes on the consumer's per-slot
+// inbox mbarrier -- instead of an L2 mailbox that the consumer's poller warp
+// polls. No cluster-scope fence is on the path (ptxas turns those into
+// MEMBAR.GPU / CCTL.IVALL). Only the first band of each cluster polls the L2
+// mailbox of the band above.
 #ifndef SPTRSV_ST_CLUSTER
-#define SPTRSV_ST_CLUSTER 8
+#define SPTRSV_ST_CLUSTER 1
 #endif
 constexpr int kStCluster = SPTRSV_ST_CLUSTER;
 // inbox ring depth in chunks (the producer waits for the consumer only when it
@@ -145,6 +147,16 @@ __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, in
           c < kStProbeFirst + kStProbeChunks)
              ? a.dbg + 6 * (c - kStProbeFirst) + slot
              : nullptr;
+}
+
+// diagnostics (probe bit 256): hand-over timeline in globaltimer ns for chunks
+// [64, 128): slot 0 = band 1 published chunk c, slot 1 = band 2's poller
+// released its inbox chunk c, slots 2 / 3 = band 2's compute warp before /
+// after its wait for chunk c (band 2's chunk c needs band 1's chunk c + 4)
+__device__ __forceinline__ void lag_stamp(const StArgs& a, int t, int c, int lane, int slot) {
+  if ((a.probe & 256) && a.dbg && lane == 0 && c >= kStProbeFirst && c < kStProbeFirst + kStProbeChunks &&
+      t == (slot == 0 ? 1 : 2))
+    a.dbg[6 * (c - kStProbeFirst) + slot] = (long long)globaltimer_ns();
 }
 
 constexpr int kStBlkPairs = kStBlock / 2;
@@ -207,7 +219,8 @@ struct StSmem {
   static constexpr int kOut = (kInbox + kStInbox * kStG * kStC * 8 + 1023) / 1024 * 1024;
   static constexpr int kOutChunk = kStG * kStLanes * kStBlock * 8;
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
-  static constexpr int kCtl = kBars + 8 * kSlots;
+  static constexpr int kInBars = kBars + 8 * kSlots;  // [kStInbox] inbox mbarriers (cluster hand-over)
+  static constexpr int kCtl = kInBars + 8 * kStInbox;
   static constexpr int kTotal = kCtl + 64 + 1024;  // + alignment slack of the ring base
   static_assert(kB % 1024 == 0 && kBChunk % 1024 == 0, "b slots on 1024-byte boundaries (TMA swizzle)");
 };
@@ -230,13 +243,11 @@ __device__ __forceinline__ bool wait_ctl(const int* ctl, int which, int need, un
 // The compute warp's chunk-boundary wait: input slot, band-above inbox and
 // output slot in one polling loop (three independent shared loads per poll
 // instead of three sequential loops).
-// MbReady may be released by the band above's CTA of the same cluster: its
-// acquire is cluster-scope.
 __device__ __forceinline__ bool wait_chunk(const int* ctl, int in_need, int mb_need, int out_need,
                                            unsigned long long deadline, const int* abort_flag) {
   int polls = 0;
   while (true) {
-    const int i = ld_acquire_cta(ctl + kCtlInReady), m = ld_acquire_cluster_local(ctl + kCtlMbReady),
+    const int i = ld_acquire_cta(ctl + kCtlInReady), m = ld_acquire_cta(ctl + kCtlMbReady),
               o = ld_acquire_cta(ctl + kCtlOutDone);
     if (i >= in_need && m >= mb_need && o >= out_need) return true;
     if (ld_acquire_cta(ctl + kCtlAbort)) return false;
@@ -427,7 +438,17 @@ template <bool EXACT>
 __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
                        bool above_in_cluster) {
   using S = StSmem<EXACT>;
-  if (t == 0 || above_in_cluster) return;  // no band above, or it pushes into our inbox itself
+  if (above_in_cluster) return;  // the band above pushes into our inbox itself
+  if (t == 0) {
+    // no band above: the top grid row's "row above" is zero, so the compute
+    // warp's lane 0 reads zeros from the inbox like any other band (no
+    // per-step has_above select)
+    double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
+    for (int w = lane; w < kStInbox * kStG * kStC; w += kStLanes) inbox[w] = 0.0;
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kCtlMbReady, 1 << 30);
+    return;
+  }
   double* inbox = reinterpret_cast<double*>(smem + S::kInbox);
   // the band above on another PE: its owner's mailboxes over NVLink (.sys)
   const int up_pe = a.band_owner ? a.band_owner[t - 1] : a.my_pe;
@@ -451,6 +472,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
+    lag_stamp(a, t, c, lane, 1);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
@@ -604,17 +626,42 @@ __device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double
 // active/publish branch
 template <bool EXACT, int ABL, bool PART>
 __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
-                        unsigned crank, bool below_in_cluster) {
+                        unsigned crank, bool below_in_cluster, bool above_in_cluster) {
   using S = StSmem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
-  const bool has_above = t > 0;
   // the band below in the next CTA of this cluster: its inbox ring, inbox
   // counter and progress counter in distributed shared memory
   const unsigned peer_inbox = below_in_cluster ? mapa_shared(smem + S::kInbox, crank + 1) : 0u;
-  const unsigned peer_mbready = below_in_cluster ? mapa_shared(ctl + kCtlMbReady, crank + 1) : 0u;
+  const unsigned peer_ibars = below_in_cluster ? mapa_shared(smem + S::kInBars, crank + 1) : 0u;
   const unsigned peer_indone = below_in_cluster ? mapa_shared(ctl + kCtlInDone, crank + 1) : 0u;
-  int pushed = 0, peer_done = 0;
+  int peer_done = 0;
+  // consumer side: inbox slot cc % kStInbox completes chunk cc's bytes
+  unsigned long long* ibars = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
+  auto inbox_bytes = [&](int cc) { return max(0, min(nblk, (cc + 1) * kStG) - min(nblk, cc * kStG)) * kStC * 8; };
+  auto arm_inbox = [&](int cc) {  // lane 0: this phase of the slot expects chunk cc's bytes
+    if (cc < nchunks) mbar_expect_tx(ibars + cc % kStInbox, inbox_bytes(cc));
+  };
+  // chunk cn's inputs, band-above row and a free output slot; an in-cluster
+  // band above delivers through the inbox mbarrier instead of MbReady
+  auto wait_in = [&](int cn, int out_need) -> bool {
+    if (!above_in_cluster) return wait_chunk(ctl, cn + 1, cn + 1, out_need, deadline, a.abort_flag);
+    unsigned long long* bar = ibars + cn % kStInbox;
+    const unsigned par = (unsigned)(cn / kStInbox) & 1u;
+    int polls = 0;
+    while (true) {
+      const int i = ld_acquire_cta(ctl + kCtlInReady), o = ld_acquire_cta(ctl + kCtlOutDone);
+      if (i >= cn + 1 && o >= out_need && mbar_test_wait(bar, par)) break;
+      if (ld_acquire_cta(ctl + kCtlAbort)) return false;
+      if ((++polls & 1023) == 0) {
+        if (deadline && globaltimer_ns() > deadline) return false;
+        if (ld_relaxed_s32(a.abort_flag)) return false;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) arm_inbox(cn + kStInbox);  // the slot's next phase (its bytes come after InDone > cn)
+    return true;
+  };
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   // the band below on another PE reads these over NVLink: system-scope stores
   const bool below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
@@ -723,7 +770,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
       for (int q = 0; q < kStC; ++q) {
         const double up = kStEarlyShfl ? upv[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
-        top[q] = lane == 0 ? (has_above ? blk.inbox[q] : 0.0) : up;
+        top[q] = lane == 0 ? blk.inbox[q] : up;
       }
       block(blk, top, xb, true);
       retire(c, k, xb);
@@ -761,8 +808,8 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     if (jhi >= 0 && jlo < nblk) {
       const int need = min(jhi, nblk - 1) / kStG - kStInbox + 1;
       int polls = 0;
-      while (peer_done < need) {
-        peer_done = ld_acquire_cluster_s32(peer_indone);
+      while (peer_done < need) {  // rare: the consumer is kStInbox chunks behind
+        peer_done = ld_relaxed_cluster_s32(peer_indone);
         if ((++polls & 255) == 0 &&
             ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
           return false;
@@ -774,16 +821,10 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
           const double2 v = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) *
                                                                                   S::kOutChunk)[st_b_piece(
               kStR - 1, kStLanes - 1, k, h)];
-          const int cc = jj / kStG, kk = jj - cc * kStG;
-          st_cluster_f64x2(peer_inbox + ((((cc % kStInbox) * kStG + kk) * kStC + 2 * h) << 3), v.x, v.y);
+          const int cc = jj / kStG, kk = jj - cc * kStG, sl = cc % kStInbox;
+          st_async_f64x2(peer_inbox + (((sl * kStG + kk) * kStC + 2 * h) << 3), v.x, v.y, peer_ibars + 8 * sl);
         }
       }
-    }
-    __syncwarp();  // the lanes' DSMEM stores are ordered before lane 0's release
-    const int ready = c + 1 >= nchunks ? nchunks : max(0, (jhi + 1) / kStG);
-    if (ready > pushed) {
-      pushed = ready;
-      if (lane == 0) st_release_cluster_s32(peer_mbready, ready);
     }
     return true;
   };
@@ -808,10 +849,11 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     // the first step that loads from chunk c + 1: make sure it is ready
     if (k == kStG - 2 && c + 1 < nchunks && !solo) {
       if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-      if (!wait_chunk(ctl, c + 2, has_above ? c + 2 : 0, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0, deadline,
-                      a.abort_flag))
+      lag_stamp(a, t, c + 1, lane, 2);
+      if (!wait_in(c + 1, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0))
         return false;
       if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
+      lag_stamp(a, t, c + 1, lane, 3);
     }
     const int s = c * kStG + k;
     const int j = s - lane;
@@ -821,7 +863,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
     for (int q = 0; q < kStC; ++q) {
       const double up = kStEarlyShfl ? upv[q] : (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
-      top[q] = lane == 0 ? (has_above ? cur.inbox[q] : 0.0) : up;
+      top[q] = lane == 0 ? cur.inbox[q] : up;
     }
     double xb[kStR][kStC];
     if (kStExpand && !EXACT) {
@@ -856,6 +898,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       } else if (kStChunkPub && !(ABL & 8)) {
         __syncwarp();  // lane 31's staged bottom rows -> the lanes that store them
         if (!hand_down(c)) return false;
+        lag_stamp(a, t, c, lane, 0);
       }
       // chunk boundary: hand over the outputs and the input slot
       __syncwarp();
@@ -872,7 +915,10 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
-  if (!solo && has_above && !wait_chunk(ctl, 1, 1, 0, deadline, a.abort_flag)) return abort_task(a, ctl, lane);
+  if (above_in_cluster && lane == 0)
+    for (int cc = 0; cc < kStInbox; ++cc) arm_inbox(cc);  // first phase of every slot
+  __syncwarp();
+  if (!solo && !wait_in(0, 0)) return abort_task(a, ctl, lane);
   if (tstamp) tstamp[1] = (long long)globaltimer_ns();
   static_assert(kStG >= 3, "the two-step lookahead stays within one chunk boundary");
   buf[0].load(smem, 0, 0, 0, lane);
@@ -919,6 +965,11 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
         if (crank == 0) ctl[kCtlGroup] = ld_relaxed_s32(a.abort_flag) ? n_groups : atomicAdd(a.ticket, 1);
         ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
         ctl[kCtlMbReady] = 0;
+        // fresh inbox barriers for this task (no st.async of the previous one is pending:
+        // the band above finished it before the cluster barrier)
+        unsigned long long* ib = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
+        for (int k = 0; k < kStInbox; ++k) mbar_init(&ib[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       }
       cluster_sync_all();
       if (threadIdx.x == 0) {
@@ -936,7 +987,8 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
     if (t < 0) break;
     if (t < a.n_tasks) {
       const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && t + 1 < a.n_tasks;
-      if (warp == 0) compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
+      if (warp == 0)
+        compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
       else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
       } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
       else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
