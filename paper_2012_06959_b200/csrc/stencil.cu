@@ -91,6 +91,45 @@ static_assert(kStStoreDepth >= 0 && kStStoreDepth <= kStOutSlots - 1, "in-flight
 #define SPTRSV_ST_CLUSTER 1
 #endif
 constexpr int kStCluster = SPTRSV_ST_CLUSTER;
+
+// Fast mode without the lane-0 select (SPTRSV_ST_NOSEL, default on): lane 0's
+// row above is the band above's bottom row, every other lane's comes from its
+// neighbour by __shfl_up_sync. A per-step select between the two sat on the
+// recurrence (SHFL -> FSEL -> DFMA, +16 cycles of a 72-cycle step in
+// tools/microbench/chain.cu). Instead the packer stores lane 0's top-row
+// coefficient as 0 and the poller folds the band above's value into that
+// row's b in the staged ring, b - L[i,i-nx] x[i-nx], before it hands the chunk
+// over; the compute warp then treats every lane alike (lane 0 multiplies its
+// own shuffled bottom row by 0). Re-associates the top-row sum (fast mode's
+// 1e-12 contract); a non-finite x in lane 0's own bottom row turns into NaN
+// instead of +-inf in the (already non-finite) solution.
+#ifndef SPTRSV_ST_NOSEL
+#define SPTRSV_ST_NOSEL 0
+#endif
+#ifndef SPTRSV_ST_NOSEL_ABL  // timing diagnostics only: 1 = no fold into b, 2 = no wait for the staged b
+#define SPTRSV_ST_NOSEL_ABL 0
+#endif
+constexpr bool kStNoSel = SPTRSV_ST_NOSEL && kStCluster == 1 && kStR == 2 && kStC == 2;
+// chunk counters released before the band-below publish (see step())
+#ifndef SPTRSV_ST_REL_FIRST
+#define SPTRSV_ST_REL_FIRST 1
+#endif
+constexpr bool kStRelFirst = SPTRSV_ST_REL_FIRST;
+// the band-below hand-over is done by the storer warp once the chunk's outputs
+// are handed to it (SPTRSV_ST_STORER_PUB=1) instead of by the compute warp:
+// the compute warp's chunk boundary is then two shared-memory stores
+#ifndef SPTRSV_ST_STORER_PUB
+#define SPTRSV_ST_STORER_PUB 2
+#endif
+// (SPTRSV_ST_STORER_PUB = 2: a fifth, dedicated warp instead: the storer's
+// element-wise stores of the edge chunks delayed the first hand-overs)
+constexpr bool kStStorerPub = SPTRSV_ST_STORER_PUB && kStRelFirst;
+// chunk outputs handed to the storer through per-slot mbarriers (arrive /
+// try_wait) instead of a polled counter (SPTRSV_ST_OUT_BAR=1)
+#ifndef SPTRSV_ST_OUT_BAR
+#define SPTRSV_ST_OUT_BAR 1
+#endif
+constexpr bool kStOutBar = SPTRSV_ST_OUT_BAR && kStRelFirst;
 // inbox ring depth in chunks (the producer waits for the consumer only when it
 // runs kStInbox chunks ahead)
 constexpr int kStInbox = 64;
@@ -139,9 +178,12 @@ struct alignas(64) StArgs {
   int b_tma_bands;  // bands [0, b_tma_bands) gather b with one TMA per chunk (0: cp.async everywhere)
   int x_tma_bands;  // bands [0, x_tma_bands) store interior chunks of x with one TMA store
   unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
+  const double* upc;              // fast mode, kStNoSel: -L[i,i-nx] of every band's top grid row ([n_tasks][nx])
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
+template <bool DG>
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
+  if constexpr (!DG) return nullptr;
   // probe bit 64: stamp task 1 (a band with a band above) instead of task 0
   return (a.dbg && t == ((a.probe & 64) ? 1 : 0) && lane == 0 && c >= kStProbeFirst &&
           c < kStProbeFirst + kStProbeChunks)
@@ -153,14 +195,20 @@ __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, in
 // [64, 128): slot 0 = band 1 published chunk c, slot 1 = band 2's poller
 // released its inbox chunk c, slots 2 / 3 = band 2's compute warp before /
 // after its wait for chunk c (band 2's chunk c needs band 1's chunk c + 4)
+template <bool DG>
 __device__ __forceinline__ void lag_stamp(const StArgs& a, int t, int c, int lane, int slot) {
+  if constexpr (!DG) return;
   if ((a.probe & 256) && a.dbg && lane == 0 && c >= kStProbeFirst && c < kStProbeFirst + kStProbeChunks &&
       t == (slot == 0 ? 1 : 2))
     a.dbg[6 * (c - kStProbeFirst) + slot] = (long long)globaltimer_ns();
 }
 
 constexpr int kStBlkPairs = kStBlock / 2;
-constexpr int kStThreads = 4 * 32;  // compute, loader, storer, poller warps
+constexpr bool kStPubWarp = SPTRSV_ST_STORER_PUB == 2 && kStRelFirst && SPTRSV_ST_OUT_BAR;
+// compute, loader, storer, poller (+ publisher) warps; the publisher shares the
+// compute warp's SM sub-partition but sleeps in mbarrier.try_wait between
+// chunks (~10 instructions per chunk)
+constexpr int kStThreads = (kStPubWarp ? 5 : 4) * 32;
 // Shared-memory rings keep 16-byte pairs lane-innermost ([...][pair][lane]) so
 // every warp-wide 16-byte access touches 512 consecutive bytes (4 wavefronts,
 // no bank conflicts). b pair index of grid row r, chunk step k, column pair h:
@@ -202,7 +250,8 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
 // control words of one task (chunk counters)
 enum {
   kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5, kCtlMbReady = 6,
-  kCtlGroup = 7  // cluster rank 0: the group ticket of the current task
+  kCtlGroup = 7,  // cluster rank 0: the group ticket of the current task
+  kCtlPubDone = 8  // chunks whose band-below row the publisher warp has read out of the out ring
 };
 
 template <bool EXACT>
@@ -221,7 +270,8 @@ struct StSmem {
   static constexpr int kBars = kOut + kStOutSlots * kOutChunk;
   static constexpr int kInBars = kBars + 8 * kSlots;  // [kStInbox] inbox mbarriers (cluster hand-over)
   static constexpr int kCtl = kInBars + 8 * kStInbox;
-  static constexpr int kTotal = kCtl + 64 + 1024;  // + alignment slack of the ring base
+  static constexpr int kOutBars = kCtl + 64;  // [kStOutSlots] out-slot-full mbarriers (compute -> storer)
+  static constexpr int kTotal = kOutBars + 8 * kStOutSlots + 1024;  // + alignment slack of the ring base
   static_assert(kB % 1024 == 0 && kBChunk % 1024 == 0, "b slots on 1024-byte boundaries (TMA swizzle)");
 };
 
@@ -302,14 +352,16 @@ struct StBlk {
         bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
       }
     }
-    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (islot * kStG + k) * kStC;
+    if (EXACT || !kStNoSel) {
+      const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (islot * kStG + k) * kStC;
 #pragma unroll
-    for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
+      for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
+    }
   }
 };
 
 // ---- warp 1: stream coefficients and b, poll the band above -----------------
-template <bool EXACT>
+template <bool EXACT, bool DG>
 __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned& phase_bits,
                        unsigned long long deadline) {
   using S = StSmem<EXACT>;
@@ -396,14 +448,14 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // hand-over waits on the band-above mailbox.
   int issued = 0;
   for (int c = 0; c < nchunks; ++c) {
-    if (long long* p = st_stamp(a, t, c, lane, 2)) *p = clock64();
+    if (long long* p = st_stamp<DG>(a, t, c, lane, 2)) *p = clock64();
     const int done = ld_acquire_cta(ctl + kCtlInDone);
     while (issued < nchunks && issued < done + NB) issue(issued++);
     while (ok && issued <= c) {  // chunk c itself must be in flight: wait for its slot
       ok = wait_ctl(ctl, kCtlInDone, issued - NB + 1, deadline, a.nap);
       if (ok) issue(issued++);
     }
-    if (long long* p = st_stamp(a, t, c, lane, 3)) *p = clock64();
+    if (long long* p = st_stamp<DG>(a, t, c, lane, 3)) *p = clock64();
     if (ok) ok = settle(c);
     if (ok && c * kStG < kStLanes) {
       // steps before this lane's first block: b must read as exact zeros
@@ -417,7 +469,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 #pragma unroll
             for (int h = 0; h < kStC / 2; ++h) dst[st_b_piece(r, lane, k, h)] = make_double2(0.0, 0.0);
     }
-    if (long long* p = st_stamp(a, t, c, lane, 4)) *p = clock64();
+    if (long long* p = st_stamp<DG>(a, t, c, lane, 4)) *p = clock64();
     ok = __all_sync(0xffffffffu, ok);
     if (!ok) {
       abort_task(a, ctl, lane);
@@ -425,7 +477,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       return;
     }
     if (lane == 0) st_release_cta(ctl + kCtlInReady, c + 1);
-    if (long long* p = st_stamp(a, t, c, lane, 5)) *p = clock64();
+    if (long long* p = st_stamp<DG>(a, t, c, lane, 5)) *p = clock64();
   }
 }
 
@@ -434,7 +486,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
 // one value per lane (one L2 round trip per chunk), polled value-is-flag and
 // handed over through the inbox ring. Kept apart from the loader so the
 // round trip overlaps the loader's copies instead of adding to them.
-template <bool EXACT>
+template <bool EXACT, bool DG>
 __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
                        bool above_in_cluster) {
   using S = StSmem<EXACT>;
@@ -457,6 +509,65 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int k = lane / kStC, q = lane % kStC;
   unsigned long long spins = 0;
+  if constexpr (!EXACT && kStNoSel) {
+    // lane (k, q): column j*C + q of the band above's bottom row, folded into
+    // lane 0's top-row b of step k once the loader staged the chunk
+    const double* upc = a.upc + (size_t)t * a.nx;
+    // the factors stream from HBM kPre chunks ahead (a load per chunk in line
+    // with the poll would cost the poller a DRAM round trip per chunk)
+    constexpr int kPre = 4;
+    auto fac = [&](int cc) {
+      const int jj = cc * kStG + k;
+      return (lane < kStG * kStC && jj < nblk) ? __ldg(upc + jj * kStC + q) : 0.0;
+    };
+    double wq[kPre];
+#pragma unroll
+    for (int p = 0; p < kPre; ++p) wq[p] = fac(p);
+    // chunk c with its factor in `wf` (loaded kPre chunks earlier), which then
+    // receives chunk c + kPre's; the loop is unrolled kPre times so the
+    // factor registers never move (a move would wait for the load in flight)
+    auto one = [&](int c, double& wf) -> bool {
+      bool ok = true;
+      const int j = c * kStG + k;
+      const bool mine = lane < kStG * kStC && j < nblk;
+      unsigned long long u = 0;
+      if (mine) {
+        // spin inline first (a call would wait for the factor loads in flight)
+        const unsigned long long* src = above + j * kStC + q;
+        u = remote ? ld_relaxed_sys_u64(src) : ld_relaxed_u64(src);
+        for (int polls = 0; u == kStNotReady && polls < 256; ++polls) {
+          u = remote ? ld_relaxed_sys_u64(src) : ld_relaxed_u64(src);
+          ++spins;
+        }
+        if (u == kStNotReady)
+          u = st_poll(src, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote, spins);
+        if (u == kStNotReady) ok = false;
+      }
+      if (!(SPTRSV_ST_NOSEL_ABL & 2) && ok && !wait_ctl(ctl, kCtlInReady, c + 1, deadline, a.nap)) ok = false;
+      if (!__all_sync(0xffffffffu, ok)) return false;
+      if (mine && !(SPTRSV_ST_NOSEL_ABL & 1)) {
+        double* e = reinterpret_cast<double*>(smem + S::kB + (c % S::kSlots) * S::kBChunk) +
+                    2 * st_b_piece(0, 0, k, q / 2) + (q & 1);
+        *e = __fma_rn(wf, __longlong_as_double((long long)u), *e);
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
+      // after the release: its MEMBAR.CTA would wait for this DRAM load
+      wf = fac(c + kPre);
+      lag_stamp<DG>(a, t, c, lane, 1);
+      return true;
+    };
+    for (int c0 = 0; c0 < nchunks; c0 += kPre) {
+#pragma unroll
+      for (int u = 0; u < kPre; ++u)
+        if (c0 + u < nchunks && !one(c0 + u, wq[u])) return abort_task(a, ctl, lane);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
+    if (lane == 0 && spins) atomicAdd(&a.status->spins, spins);
+    if (remote && lane == 0) atomicAdd(&a.status->remote_reads, (unsigned long long)a.nx);
+    return;
+  }
   for (int c = 0; c < nchunks; ++c) {
     // inbox slot c % kStInbox is free once the compute warp finished chunk c - kStInbox
     if (c >= kStInbox && !wait_ctl(ctl, kCtlInDone, c - kStInbox + 1, deadline, a.nap))
@@ -472,7 +583,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     }
     if (!__all_sync(0xffffffffu, ok)) return abort_task(a, ctl, lane);
     if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
-    lag_stamp(a, t, c, lane, 1);
+    lag_stamp<DG>(a, t, c, lane, 1);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
@@ -480,10 +591,114 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   if (remote && lane == 0) atomicAdd(&a.status->remote_reads, (unsigned long long)a.nx);
 }
 
-// ---- warp 2: solved blocks from shared memory to x --------------------------
-template <bool EXACT>
-__device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline) {
+// ---- the band-below hand-over (compute warp, or the storer with kStStorerPub)
+// Per chunk, lane 31's bottom grid row as staged in the out ring goes to the
+// band below: value-is-flag stores into its L2 mailbox (polled by its poller
+// warp; .sys stores when it lives on another PE), or -- the band below in the
+// next CTA of this cluster -- st.async straight into its inbox ring, completing
+// on the consumer's per-slot inbox mbarrier. Chunk c's lane-31 blocks are
+// columns j = cG - 31 .. cG - 24, i.e. the tail of the consumer's chunk c - 4
+// and the head of c - 3; an inbox slot is rewritten only once the consumer
+// finished the chunk kStInbox before it.
+template <bool EXACT, bool PART>
+struct HandDown {
   using S = StSmem<EXACT>;
+  const StArgs& a;
+  const unsigned char* out;
+  unsigned long long* below;
+  int t, nblk;
+  bool below_in_cluster, below_remote;
+  unsigned peer_inbox = 0, peer_ibars = 0, peer_indone = 0;
+  int peer_done = 0;
+  __device__ HandDown(const StArgs& args, unsigned char* smem, int* ctl, int task, unsigned crank, bool in_cluster)
+      : a(args), out(smem + S::kOut), below(args.mbox + (size_t)task * args.nx), t(task), nblk(args.nx / kStC),
+        below_in_cluster(in_cluster) {
+    below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
+    if (in_cluster) {
+      peer_inbox = mapa_shared(smem + S::kInbox, crank + 1);
+      peer_ibars = mapa_shared(smem + S::kInBars, crank + 1);
+      peer_indone = mapa_shared(ctl + kCtlInDone, crank + 1);
+    }
+  }
+  __device__ __forceinline__ double2 bottom(int c, int k, int h) const {
+    return reinterpret_cast<const double2*>(out + (c % kStOutSlots) * S::kOutChunk)[st_b_piece(kStR - 1, kStLanes - 1,
+                                                                                               k, h)];
+  }
+  __device__ __forceinline__ void publish(int c, int lane) const {
+    constexpr int kHalves = kStC / 2;
+    if (t + 1 >= a.n_tasks || lane >= kStG * kHalves) return;
+    const int k = lane / kHalves, h = lane % kHalves;
+    const int jj = c * kStG + k - (kStLanes - 1);
+    if (jj < 0 || jj >= nblk) return;
+    const double2 v = bottom(c, k, h);
+    unsigned long long* w = below + (size_t)jj * kStC + 2 * h;
+    if (PART && below_remote) {
+      st_relaxed_sys_u64_if(w, as_u64(v.x), true);
+      st_relaxed_sys_u64_if(w + 1, as_u64(v.y), true);
+    } else {
+      st_relaxed_u64_if(w, as_u64(v.x), true);
+      st_relaxed_u64_if(w + 1, as_u64(v.y), true);
+    }
+  }
+  __device__ __forceinline__ bool push(int c, int lane, unsigned long long deadline) {
+    constexpr int kHalves = kStC / 2;
+    const int jlo = c * kStG - (kStLanes - 1), jhi = jlo + kStG - 1;
+    if (jhi >= 0 && jlo < nblk) {
+      const int need = min(jhi, nblk - 1) / kStG - kStInbox + 1;
+      int polls = 0;
+      while (peer_done < need) {  // rare: the consumer is kStInbox chunks behind
+        peer_done = ld_relaxed_cluster_s32(peer_indone);
+        if ((++polls & 255) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
+          return false;
+      }
+      if (lane < kStG * kHalves) {
+        const int k = lane / kHalves, h = lane % kHalves;
+        const int jj = jlo + k;
+        if (jj >= 0 && jj < nblk) {
+          const double2 v = bottom(c, k, h);
+          const int cc = jj / kStG, kk = jj - cc * kStG, sl = cc % kStInbox;
+          st_async_f64x2(peer_inbox + (((sl * kStG + kk) * kStC + 2 * h) << 3), v.x, v.y, peer_ibars + 8 * sl);
+        }
+      }
+    }
+    return true;
+  }
+  __device__ __forceinline__ bool run(int c, int lane, unsigned long long deadline) {
+    if (below_in_cluster) return push(c, lane, deadline);
+    publish(c, lane);
+    return true;
+  }
+};
+
+// ---- warp 4 (kStPubWarp): the band-below hand-over ---------------------------
+template <bool EXACT, bool PART, bool DG>
+__device__ void publisher(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
+                          unsigned crank, bool below_in_cluster) {
+  using S = StSmem<EXACT>;
+  HandDown<EXACT, PART> hd(a, smem, ctl, t, crank, below_in_cluster);
+  const int nchunks = a.steps / kStG;
+  const bool any = t + 1 < a.n_tasks;
+  for (int c = 0; c < nchunks; ++c) {
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + S::kOutBars) + c % kStOutSlots;
+    const unsigned par = (unsigned)(c / kStOutSlots) & 1u;
+    int polls = 0;
+    while (!mbar_try_wait(bar, par)) {
+      if (ld_acquire_cta(ctl + kCtlAbort)) return abort_task(a, ctl, lane);
+      if ((++polls & 63) == 0 && deadline && globaltimer_ns() > deadline) return abort_task(a, ctl, lane);
+    }
+    if (any && !hd.run(c, lane, deadline)) return abort_task(a, ctl, lane);
+    lag_stamp<DG>(a, t, c, lane, 0);
+    __syncwarp();
+    if (lane == 0) st_release_cta(ctl + kCtlPubDone, c + 1);
+  }
+}
+
+// ---- warp 2: solved blocks from shared memory to x --------------------------
+template <bool EXACT, bool PART, bool DG>
+__device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
+                       unsigned crank, bool below_in_cluster) {
+  using S = StSmem<EXACT>;
+  HandDown<EXACT, PART> hd(a, smem, ctl, t, crank, below_in_cluster);
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
   // this band's row of the other mailbox half (last read by the previous
@@ -499,7 +714,24 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // are handed back (edge chunks are stored synchronously and drain the rest)
   int released = 0;
   for (int c = 0; c < nchunks; ++c) {
-    if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) return abort_task(a, ctl, lane);
+    if (kStOutBar) {
+      // the compute warp arrives on the slot's mbarrier; try_wait suspends this
+      // warp in hardware until then, so it wakes without a polling interval
+      unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + S::kOutBars) + c % kStOutSlots;
+      const unsigned par = (unsigned)(c / kStOutSlots) & 1u;
+      int polls = 0;
+      while (!mbar_try_wait(bar, par)) {
+        if (ld_acquire_cta(ctl + kCtlAbort)) return abort_task(a, ctl, lane);
+        if ((++polls & 63) == 0 && deadline && globaltimer_ns() > deadline) return abort_task(a, ctl, lane);
+      }
+    } else if (!wait_ctl(ctl, kCtlOutReady, c + 1, deadline, a.nap)) {
+      return abort_task(a, ctl, lane);
+    }
+    if (kStStorerPub && !kStPubWarp) {
+      // the band below first: its hand-over is on the critical path, x is not
+      if (!hd.run(c, lane, deadline)) return abort_task(a, ctl, lane);
+      lag_stamp<DG>(a, t, c, lane, 0);
+    }
     bool async_store = false;
     unsigned char* slot = smem + S::kOut + (c % kStOutSlots) * S::kOutChunk;
     const double2* src = reinterpret_cast<const double2*>(slot);
@@ -546,6 +778,8 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     __syncwarp();
     const int done = async_store ? c + 1 - kStStoreDepth : c + 1;
     if (done > released) {
+      // the publisher warp reads the same slot (normally long done)
+      if (kStPubWarp && !wait_ctl(ctl, kCtlPubDone, done, deadline, a.nap)) return abort_task(a, ctl, lane);
       released = done;
       if (lane == 0) st_release_cta(ctl + kCtlOutDone, done);
     }
@@ -624,7 +858,7 @@ __device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double
 // ABL: compile-time ablations for timing experiments only (0 in production):
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
 // active/publish branch
-template <bool EXACT, int ABL, bool PART>
+template <bool EXACT, int ABL, bool PART, bool DG>
 __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
                         unsigned crank, bool below_in_cluster, bool above_in_cluster) {
   using S = StSmem<EXACT>;
@@ -632,10 +866,6 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   // the band below in the next CTA of this cluster: its inbox ring, inbox
   // counter and progress counter in distributed shared memory
-  const unsigned peer_inbox = below_in_cluster ? mapa_shared(smem + S::kInbox, crank + 1) : 0u;
-  const unsigned peer_ibars = below_in_cluster ? mapa_shared(smem + S::kInBars, crank + 1) : 0u;
-  const unsigned peer_indone = below_in_cluster ? mapa_shared(ctl + kCtlInDone, crank + 1) : 0u;
-  int peer_done = 0;
   // consumer side: inbox slot cc % kStInbox completes chunk cc's bytes
   unsigned long long* ibars = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
   auto inbox_bytes = [&](int cc) { return max(0, min(nblk, (cc + 1) * kStG) - min(nblk, cc * kStG)) * kStC * 8; };
@@ -776,63 +1006,8 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       retire(c, k, xb);
     }
   };
-  // lane 31's bottom rows of chunk c, staged in the out ring, to the band below
-  auto publish_chunk = [&](int c) {
-    constexpr int kHalves = kStC / 2;
-    if (t + 1 >= a.n_tasks || lane >= kStG * kHalves) return;
-    const int k = lane / kHalves, h = lane % kHalves;
-    const int jj = c * kStG + k - (kStLanes - 1);
-    if (jj < 0 || jj >= nblk) return;
-    const double2 v = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) *
-                                                                            S::kOutChunk)[st_b_piece(
-        kStR - 1, kStLanes - 1, k, h)];
-    unsigned long long* w = below + (size_t)jj * kStC + 2 * h;
-    if (PART && below_remote) {
-      st_relaxed_sys_u64_if(w, as_u64(v.x), true);
-      st_relaxed_sys_u64_if(w + 1, as_u64(v.y), true);
-    } else {
-      st_relaxed_u64_if(w, as_u64(v.x), true);
-      st_relaxed_u64_if(w + 1, as_u64(v.y), true);
-    }
-  };
-
-  // the same rows straight into the inbox ring of the band below (next CTA of
-  // the cluster): chunk c's lane-31 blocks are columns j = cG - 31 .. cG - 24,
-  // i.e. the tail of the consumer's chunk c - 4 and the head of c - 3; the
-  // consumer's inbox counter then covers every chunk whose columns all
-  // arrived. A ring slot is rewritten only once the consumer finished the
-  // chunk kStInbox before it.
-  auto push_chunk = [&](int c) -> bool {
-    constexpr int kHalves = kStC / 2;
-    const int jlo = c * kStG - (kStLanes - 1), jhi = jlo + kStG - 1;
-    if (jhi >= 0 && jlo < nblk) {
-      const int need = min(jhi, nblk - 1) / kStG - kStInbox + 1;
-      int polls = 0;
-      while (peer_done < need) {  // rare: the consumer is kStInbox chunks behind
-        peer_done = ld_relaxed_cluster_s32(peer_indone);
-        if ((++polls & 255) == 0 &&
-            ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
-          return false;
-      }
-      if (lane < kStG * kHalves) {
-        const int k = lane / kHalves, h = lane % kHalves;
-        const int jj = jlo + k;
-        if (jj >= 0 && jj < nblk) {
-          const double2 v = reinterpret_cast<const double2*>(smem + S::kOut + (c % kStOutSlots) *
-                                                                                  S::kOutChunk)[st_b_piece(
-              kStR - 1, kStLanes - 1, k, h)];
-          const int cc = jj / kStG, kk = jj - cc * kStG, sl = cc % kStInbox;
-          st_async_f64x2(peer_inbox + (((sl * kStG + kk) * kStC + 2 * h) << 3), v.x, v.y, peer_ibars + 8 * sl);
-        }
-      }
-    }
-    return true;
-  };
-  auto hand_down = [&](int c) -> bool {
-    if (below_in_cluster) return push_chunk(c);
-    publish_chunk(c);
-    return true;
-  };
+  HandDown<EXACT, PART> hd(a, smem, ctl, t, crank, below_in_cluster);
+  auto hand_down = [&](int c) -> bool { return kStStorerPub || hd.run(c, lane, deadline); };
 
   // step k of chunk c; `nxt` receives the next step's inputs
   // step k of chunk c computes from `cur` (loaded two steps earlier) and
@@ -848,12 +1023,12 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     };
     // the first step that loads from chunk c + 1: make sure it is ready
     if (k == kStG - 2 && c + 1 < nchunks && !solo) {
-      if (long long* p = st_stamp(a, t, c + 1, lane, 0)) *p = clock64();
-      lag_stamp(a, t, c + 1, lane, 2);
+      if (long long* p = st_stamp<DG>(a, t, c + 1, lane, 0)) *p = clock64();
+      lag_stamp<DG>(a, t, c + 1, lane, 2);
       if (!wait_in(c + 1, c + 1 >= kStOutSlots ? c + 2 - kStOutSlots : 0))
         return false;
-      if (long long* p = st_stamp(a, t, c + 1, lane, 1)) *p = clock64();
-      lag_stamp(a, t, c + 1, lane, 3);
+      if (long long* p = st_stamp<DG>(a, t, c + 1, lane, 1)) *p = clock64();
+      lag_stamp<DG>(a, t, c + 1, lane, 3);
     }
     const int s = c * kStG + k;
     const int j = s - lane;
@@ -863,7 +1038,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
     for (int q = 0; q < kStC; ++q) {
       const double up = kStEarlyShfl ? upv[q] : (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
-      top[q] = lane == 0 ? cur.inbox[q] : up;
+      top[q] = (!EXACT && kStNoSel) ? up : lane == 0 ? cur.inbox[q] : up;
     }
     double xb[kStR][kStC];
     if (kStExpand && !EXACT) {
@@ -887,7 +1062,29 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       }
     }
     if (!kStEarlyShfl) load_ahead();
-    if (k == kStG - 1) {
+    if (k == kStG - 1 && kStRelFirst) {
+      // chunk boundary: hand the outputs and the input slot over BEFORE the
+      // band-below publish -- the release's MEMBAR.CTA would otherwise wait
+      // for the publish's global stores to be acknowledged
+      if (kStSpec) {
+        if (__any_sync(0xffffffffu, spec_bad)) redo_chunk(c);
+        spec_bad = false;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (kStOutBar) {
+          st_release_cta(ctl + kCtlInDone, c + 1);
+          mbar_arrive(reinterpret_cast<unsigned long long*>(smem + S::kOutBars) + c % kStOutSlots);
+        } else {
+          st_release_cta(ctl + kCtlOutReady, c + 1);
+          st_release_cta(ctl + kCtlInDone, c + 1);
+        }
+      }
+      if ((kStChunkPub || kStSpec) && !(ABL & 8) && !kStStorerPub) {
+        if (!hand_down(c)) return false;
+        lag_stamp<DG>(a, t, c, lane, 0);
+      }
+    } else if (k == kStG - 1) {
       if (kStSpec) {
         // a guard failed somewhere in this chunk: recompute it with IEEE
         // division (rare: operands outside Markstein's exponent window)
@@ -898,7 +1095,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
       } else if (kStChunkPub && !(ABL & 8)) {
         __syncwarp();  // lane 31's staged bottom rows -> the lanes that store them
         if (!hand_down(c)) return false;
-        lag_stamp(a, t, c, lane, 0);
+        lag_stamp<DG>(a, t, c, lane, 0);
       }
       // chunk boundary: hand over the outputs and the input slot
       __syncwarp();
@@ -911,7 +1108,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   };
 
   // diagnostics: per-task globaltimer stamps (start, first chunk ready, end)
-  long long* tstamp = (a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
+  long long* tstamp = (DG && a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
   StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
@@ -937,7 +1134,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
-template <bool EXACT, int ABL, bool PART, int CL>
+template <bool EXACT, int ABL, bool PART, int CL, bool DG>
 __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_constant__ StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -954,6 +1151,13 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
   unsigned phase_bits = 0;
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
   const unsigned crank = CL > 1 ? cluster_ctarank() : 0u;
+  // fresh out-slot barriers per task (every arrival of the previous task was
+  // consumed by its storer before the task-end __syncthreads)
+  auto init_out_bars = [&]() {
+    if (!kStOutBar) return;
+    unsigned long long* ob = reinterpret_cast<unsigned long long*>(smem + S::kOutBars);
+    for (int k = 0; k < kStOutSlots; ++k) mbar_init(&ob[k], 1);
+  };
   const int n_groups = (a.n_tasks + CL - 1) / CL;
   while (true) {
     if (CL > 1) {
@@ -964,7 +1168,8 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
       if (threadIdx.x == 0) {
         if (crank == 0) ctl[kCtlGroup] = ld_relaxed_s32(a.abort_flag) ? n_groups : atomicAdd(a.ticket, 1);
         ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
-        ctl[kCtlMbReady] = 0;
+        ctl[kCtlMbReady] = ctl[kCtlPubDone] = 0;
+        init_out_bars();
         // fresh inbox barriers for this task (no st.async of the previous one is pending:
         // the band above finished it before the cluster barrier)
         unsigned long long* ib = reinterpret_cast<unsigned long long*>(smem + S::kInBars);
@@ -980,7 +1185,8 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
       const int k = atomicAdd(a.ticket, 1);  // ascending: the progress rule (engine.py:30-35)
       ctl[kCtlTask] = k >= a.n_my_tasks ? -1 : (a.my_tasks ? a.my_tasks[k] : k);
       ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
-      ctl[kCtlMbReady] = 0;
+      ctl[kCtlMbReady] = ctl[kCtlPubDone] = 0;
+      init_out_bars();
     }
     __syncthreads();
     const int t = ctl[kCtlTask];
@@ -988,11 +1194,12 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
     if (t < a.n_tasks) {
       const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && t + 1 < a.n_tasks;
       if (warp == 0)
-        compute<EXACT, ABL, PART>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
+        compute<EXACT, ABL, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
       else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
-      } else if (warp == 1) loader<EXACT>(a, smem, ctl, t, lane, phase_bits, deadline);
-      else if (warp == 2) storer<EXACT>(a, smem, ctl, t, lane, deadline);
-      else poller<EXACT>(a, smem, ctl, t, lane, deadline, CL > 1 && crank > 0);
+      } else if (warp == 1) loader<EXACT, DG>(a, smem, ctl, t, lane, phase_bits, deadline);
+      else if (warp == 2) storer<EXACT, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
+      else if (warp == 4) publisher<EXACT, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
+      else poller<EXACT, DG>(a, smem, ctl, t, lane, deadline, CL > 1 && crank > 0);
     }
     __syncthreads();
     if (CL == 1 && ctl[kCtlAbort]) break;  // (clusters leave together, through the ticket)
@@ -1026,17 +1233,17 @@ int max_active_clusters(K kernel, int cl, int smem_bytes) {
   return n;
 }
 
-template <bool EXACT, int ABL, bool PART = false, int CL = 1>
+template <bool EXACT, int ABL, bool PART = false, int CL = 1, bool DG = false>
 cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART, CL>, StSmem<EXACT>::kTotal, attr); e != cudaSuccess)
+  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART, CL, DG>, StSmem<EXACT>::kTotal, attr); e != cudaSuccess)
     return e;
   if (CL == 1) {
-    k_stencil2d<EXACT, ABL, PART, CL><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
+    k_stencil2d<EXACT, ABL, PART, CL, DG><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
     return cudaGetLastError();
   }
   const int groups = (a.n_tasks + CL - 1) / CL;
-  const int fit = max_active_clusters(k_stencil2d<EXACT, ABL, PART, CL>, CL, StSmem<EXACT>::kTotal);
+  const int fit = max_active_clusters(k_stencil2d<EXACT, ABL, PART, CL, DG>, CL, StSmem<EXACT>::kTotal);
   if (fit < 1) return cudaErrorLaunchOutOfResources;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL * std::min(groups, fit), 1, 1);
@@ -1050,7 +1257,7 @@ cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_stencil2d<EXACT, ABL, PART, CL>, a);
+  return cudaLaunchKernelEx(&cfg, k_stencil2d<EXACT, ABL, PART, CL, DG>, a);
 }
 
 // probe bits 12..15 select an ablation variant of the fast kernel (timing only)
@@ -1067,6 +1274,11 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
       case 15: return launch_stencil_v<EXACT, 15>(a, blocks, s);
       default: break;
     }
+  }
+  // probe bit 16: the diagnostics build of the kernel (clock / globaltimer stamps)
+  if (a.dbg) {
+    if (kStCluster > 1 && a.n_tasks > 1) return launch_stencil_v<EXACT, 0, false, kStCluster, true>(a, blocks, s);
+    return launch_stencil_v<EXACT, 0, false, 1, true>(a, blocks, s);
   }
   if (kStCluster > 1 && a.n_tasks > 1) return launch_stencil_v<EXACT, 0, false, kStCluster>(a, blocks, s);
   return launch_stencil_v<EXACT, 0>(a, blocks, s);
@@ -1102,7 +1314,8 @@ __global__ void k_st_pack(const int* __restrict__ rp, const double* __restrict__
         if (j >= 0 && j < nblk && y < ny) {
           const long long i = y * nx + (long long)j * kStC + c;
           int kk = rp[i];
-          const double fu = y > 0 ? val[kk++] : 0.0;
+          double fu = y > 0 ? val[kk++] : 0.0;
+          if (!exact && kStNoSel && l == 0 && r == 0) fu = 0.0;  // folded into b by the poller
           const double fl = (j * kStC + c) > 0 ? val[kk] : 0.0;
           f[0] = fu, f[1] = fl;
           if (exact) f[2] = dg[i], f[3] = rdg[i];
@@ -1111,6 +1324,19 @@ __global__ void k_st_pack(const int* __restrict__ rp, const double* __restrict__
         for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
       }
     }
+  }
+}
+
+// -L[i, i-nx] of every band's top grid row (fast mode, kStNoSel): the
+// poller's factor for the band above's value. Band 0 has no row above (0).
+__global__ void k_st_upc(const int* __restrict__ rp, const double* __restrict__ cv, int nx, int ny, int n_tasks,
+                         double* __restrict__ upc) {
+  const long long items = (long long)n_tasks * nx;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(it / nx), x = (int)(it % nx);
+    const long long y = (long long)t * kStBand;
+    upc[it] = (t > 0 && y < ny) ? -cv[rp[y * nx + x]] : 0.0;
   }
 }
 
@@ -1231,6 +1457,13 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
     const int grid = (int)std::min<long long>((items + 255) / 256, 148 * 64);
     k_st_pack<<<grid, 256, 0, stream>>>(rp, exact ? cv : wv, dg, rdg, nx, stencil.ny, stencil.n_tasks,
                                         stencil.steps_per_task, exact ? 1 : 0, stencil.stream);
+    if (!exact && kStNoSel) {
+      if ((e = al((void**)&stencil.upc, sizeof(double) * (size_t)stencil.n_tasks * nx)) != cudaSuccess)
+        return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+      const long long m = (long long)stencil.n_tasks * nx;
+      k_st_upc<<<(int)std::min<long long>((m + 255) / 256, 148 * 16), 256, 0, stream>>>(rp, cv, nx, stencil.ny,
+                                                                                        stencil.n_tasks, stencil.upc);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
@@ -1268,6 +1501,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   StArgs a{};
   a.stream = stencil.stream;
+  a.upc = stencil.upc;
   a.mbox = stencil.mbox + par * half;
   a.mbox_next = stencil.mbox + (1 - par) * half;
   a.mbox_half = par * half;

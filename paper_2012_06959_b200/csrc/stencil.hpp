@@ -58,6 +58,10 @@ struct StencilPlan {
   long long stream_bytes = 0;
   double build_ms = 0.0;
   unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
+  // fast mode without the lane-0 select (stencil.cu kStNoSel): -L[i, i-nx] of
+  // every band's top grid row, [n_tasks][nx]; the poller folds the band
+  // above's value into that row's b (b - L[i,i-nx] x[i-nx])
+  double* upc = nullptr;
   unsigned long long* mbox = nullptr;  // [n_tasks][nx] bottom grid row of each task (value-is-flag)
   // streamed host solves (sptrsv_solve): per-band b-arrived flags written by
   // the copy stream, per-band x-stored flags written by the kernel; both
@@ -103,10 +107,11 @@ struct StencilPlan {
   }
   void release() {
     release_part();
-    void* ptrs[] = {stream, mbox, bflag, xflag};
+    void* ptrs[] = {stream, mbox, bflag, xflag, upc};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
+    upc = nullptr;
     mbox = nullptr;
     bflag = xflag = nullptr;
     epoch = 0;

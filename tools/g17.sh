@@ -1,0 +1,6 @@
+mkdir -p gpurun_out; rm -f gpurun_out/g17.txt
+for v in "" ns0 nsa1 nsa2; do
+  if [ -n "$v" ]; then export SPTRSV_LIB=$PWD/paper_2012_06959_b200/libsptrsv_b200_$v.so; else unset SPTRSV_LIB; fi
+  timeout 120 python tools/variant_bench.py >> gpurun_out/g17.txt 2>&1
+  timeout 120 python tools/stencil_timeline.py fast >> gpurun_out/g17.txt 2>&1
+done
