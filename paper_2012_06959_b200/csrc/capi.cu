@@ -277,6 +277,16 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
     a.part_sum = split_rows.part_sum;
     a.part_done = split_rows.part_done;
   }
+  if (opt.probe_flags & 512) {
+    // diagnostics: globaltimer of every row's publish (tools/rows_levels.py)
+    if (!probe_buf || probe_words < n) {
+      if (probe_buf) cudaFree(probe_buf);
+      probe_buf = nullptr;
+      CUDA_TRY(dalloc(&probe_buf, std::max<long long>(n, kProbeWords)));
+      probe_words = std::max<long long>(n, kProbeWords);
+    }
+    a.stamps = probe_buf;
+  }
   CUDA_TRY(cudaEventRecord(evk0, s));
   CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
   CUDA_TRY(cudaEventRecord(evk1, s));
@@ -706,7 +716,7 @@ int sptrsv_plan_probe_read(const sptrsv_plan* plan, int64_t* out, int32_t count)
   if (!p || !out) return fail(SPTRSV_E_ARGUMENT, "null argument");
   if (!p->probe_buf) return fail(SPTRSV_E_ARGUMENT, "no probe data: set options.probe_flags");
   CUDA_TRY(cudaSetDevice(p->device));
-  CUDA_TRY(cudaMemcpy(out, p->probe_buf, sizeof(long long) * std::min<int>(count, DevicePlan::kProbeWords),
+  CUDA_TRY(cudaMemcpy(out, p->probe_buf, sizeof(long long) * std::min<long long>(count, p->probe_words),
                       cudaMemcpyDeviceToHost));
   return SPTRSV_OK;
 }

@@ -72,6 +72,7 @@ struct RowsArgs {
   const int* heavy_parts;
   double* part_sum;
   int* part_done;
+  long long* stamps;  // diagnostics (probe bit 512): globaltimer at each row's publish
 };
 
 cudaError_t launch_rows(int mode, const RowsArgs& a, int blocks, cudaStream_t s);

@@ -149,6 +149,7 @@ struct DevicePlan {
   // [0, 384), then per-task globaltimer stamps [384, 384 + 3 * 1024)
   static constexpr int kProbeWords = 6 * 64 + 3 * 1024;
   long long* probe_buf = nullptr;
+  long long probe_words = kProbeWords;  // (rows executor, probe bit 512: one stamp per row)
   int executor_used = SPTRSV_EXECUTOR_ROWS;
 
   double setup_ms = 0.0;

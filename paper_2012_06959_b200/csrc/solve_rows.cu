@@ -131,6 +131,7 @@ __device__ __forceinline__ void publish_u64(const RowsArgs& a, int i, double v) 
   unsigned long long* p = a.xseg[a.owner ? a.my_pe : 0] + i;
   if (a.owner) st_relaxed_sys_u64(p, publishable(v));
   else st_relaxed_u64(p, publishable(v));
+  if (a.stamps) a.stamps[i] = (long long)globaltimer_ns();
 }
 
 // One lane, one row, floating point.
