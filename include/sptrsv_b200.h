@@ -62,7 +62,10 @@ enum {
 /* plan flags */
 enum {
   SPTRSV_PLAN_STRUCTURE_ONLY = 1, /* analysis only: diagonal may be missing/zero, values may be NULL */
-  SPTRSV_PLAN_NO_STREAMED_IO = 4  /* sptrsv_solve: copy all of b in, solve, copy all of x out (no overlap) */
+  SPTRSV_PLAN_NO_STREAMED_IO = 4, /* sptrsv_solve: copy all of b in, solve, copy all of x out (no overlap) */
+  SPTRSV_PLAN_PUSH_MANAGED = 8    /* executor "push": left sums and in-degree counters in cudaMallocManaged
+                                     (unified) memory, updated with system-scope atomics -- the paper's
+                                     Unified-Memory baseline, for the push/pull comparison */
 };
 
 typedef struct sptrsv_options {

@@ -25,6 +25,7 @@ EXECUTOR = {"auto": 0, "rows": 1, "chains": 2, "stencil": 3, "push": 4, "band": 
 EXECUTOR_NAME = {v: k for k, v in EXECUTOR.items()}
 PLAN_STRUCTURE_ONLY = 1
 PLAN_NO_STREAMED_IO = 4
+PLAN_PUSH_MANAGED = 8  # executor='push': shared state in unified memory, system-scope atomics
 
 
 class Options(C.Structure):
@@ -196,7 +197,7 @@ class NativePlan:
 
     def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
                  timeout=60.0, spin_initial=1024, spin_max_ns=64, structure_only=False, chain_lanes=32,
-                 probe_flags=0, streamed_io=True):
+                 probe_flags=0, streamed_io=True, push_managed=False):
         lib = require_gpu()
         self._lib = lib
         self.n = int(n)
@@ -207,7 +208,8 @@ class NativePlan:
         opt.precision = PRECISION[precision]
         opt.executor = EXECUTOR[executor]
         opt.device = int(device)
-        opt.flags = (PLAN_STRUCTURE_ONLY if structure_only else 0) | (0 if streamed_io else PLAN_NO_STREAMED_IO)
+        opt.flags = ((PLAN_STRUCTURE_ONLY if structure_only else 0) | (0 if streamed_io else PLAN_NO_STREAMED_IO)
+                     | (PLAN_PUSH_MANAGED if push_managed else 0))
         opt.timeout_s = float(timeout)
         opt.spin_initial = int(spin_initial)
         opt.spin_max_ns = int(spin_max_ns)

@@ -59,10 +59,18 @@ __device__ __forceinline__ int ld_acquire_gpu_s32(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_acquire_sys_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 constexpr int kPushBatch = 8;
 
-template <bool FAST>
+// SYS: the shared state is unified (managed) memory updated with
+// system-scope atomics and polled with system-scope acquires (the paper's
+// Unified-Memory design; SPTRSV_PLAN_PUSH_MANAGED)
+template <bool FAST, bool SYS>
 __global__ void __launch_bounds__(256) k_push(PushArgs a) {
   const int lane = threadIdx.x & 31;
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
@@ -83,7 +91,7 @@ __global__ void __launch_bounds__(256) k_push(PushArgs a) {
       // lock-wait on the in-degree counter (engine.py:497-521 / 367-380)
       const int need = a.indeg[j];
       int polls = 0, sleep_ns = 32;
-      while (ld_acquire_gpu_s32(a.count + j) < need) {
+      while ((SYS ? ld_acquire_sys_s32(a.count + j) : ld_acquire_gpu_s32(a.count + j)) < need) {
         ++spins;
         if (++polls > a.spin_initial) {
           if ((polls & 63) == 0) {
@@ -108,10 +116,17 @@ __global__ void __launch_bounds__(256) k_push(PushArgs a) {
     if (!__shfl_sync(0xffffffffu, ok, 0)) break;
     xj = __shfl_sync(0xffffffffu, xj, 0);
     const int beg = a.cp[j], end = a.cp[j + 1];
-    for (int k = beg + lane; k < end; k += 32) atomicAdd(a.left + __ldg(a.ri + k), __ldg(a.val + k) * xj);
+    for (int k = beg + lane; k < end; k += 32) {
+      if (SYS) atomicAdd_system(a.left + __ldg(a.ri + k), __ldg(a.val + k) * xj);
+      else atomicAdd(a.left + __ldg(a.ri + k), __ldg(a.val + k) * xj);
+    }
     __syncwarp();
-    __threadfence();  // every left-sum update before any counter increment
-    for (int k = beg + lane; k < end; k += 32) atomicAdd(a.count + __ldg(a.ri + k), 1);
+    if (SYS) __threadfence_system();
+    else __threadfence();  // every left-sum update before any counter increment
+    for (int k = beg + lane; k < end; k += 32) {
+      if (SYS) atomicAdd_system(a.count + __ldg(a.ri + k), 1);
+      else atomicAdd(a.count + __ldg(a.ri + k), 1);
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
@@ -139,6 +154,11 @@ __global__ void k_gather_csc(const int* __restrict__ entry, const int* __restric
 
 int DevicePlan::build_push() {
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  // the shared state: unified memory for the Unified-Memory baseline
+  const bool managed = (opt.flags & SPTRSV_PLAN_PUSH_MANAGED) != 0;
+  auto alm = [&](void** p, size_t b) {
+    return managed ? cudaMallocManaged(p, b < 16 ? 16 : b, cudaMemAttachGlobal) : cudaMalloc(p, b < 16 ? 16 : b);
+  };
   cudaError_t e;
   int *row_of = nullptr, *iota = nullptr, *keys_s = nullptr, *entry_s = nullptr;
   const int grid = (int)std::min<long long>(std::max<long long>(noff, n) / 256 + 1, 148 * 32);
@@ -153,8 +173,8 @@ int DevicePlan::build_push() {
       (e = al((void**)&push.ri, sizeof(int) * noff)) != cudaSuccess ||
       (e = al((void**)&push.v_exact, sizeof(double) * noff)) != cudaSuccess ||
       (e = al((void**)&push.v_fast, sizeof(double) * noff)) != cudaSuccess ||
-      (e = al((void**)&push.left, sizeof(double) * n)) != cudaSuccess ||
-      (e = al((void**)&push.count, sizeof(int) * n)) != cudaSuccess ||
+      (e = alm((void**)&push.left, sizeof(double) * n)) != cudaSuccess ||
+      (e = alm((void**)&push.count, sizeof(int) * n)) != cudaSuccess ||
       (e = al((void**)&row_of, sizeof(int) * noff)) != cudaSuccess ||
       (e = al((void**)&iota, sizeof(int) * noff)) != cudaSuccess ||
       (e = al((void**)&keys_s, sizeof(int) * noff)) != cudaSuccess ||
@@ -216,13 +236,14 @@ int DevicePlan::solve_push(const double* d_b, double* d_x, cudaStream_t s) {
   a.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
+  const bool sys = (opt.flags & SPTRSV_PLAN_PUSH_MANAGED) != 0;
   int per_sm = 0;
-  if (fast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<true>, 256, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<false>, 256, 0);
+  if (fast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<true, false>, 256, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<false, false>, 256, 0);
   const int blocks = std::max(1, num_sms * std::max(per_sm, 1));
   if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  if (fast) k_push<true><<<blocks, 256, 0, s>>>(a);
-  else k_push<false><<<blocks, 256, 0, s>>>(a);
+  if (fast) sys ? k_push<true, true><<<blocks, 256, 0, s>>>(a) : k_push<true, false><<<blocks, 256, 0, s>>>(a);
+  else sys ? k_push<false, true><<<blocks, 256, 0, s>>>(a) : k_push<false, false><<<blocks, 256, 0, s>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;

@@ -83,3 +83,20 @@ def test_watchdog_on_push():
     with pytest.raises(SolveTimeout):
         plan.solve(b)
     plan.close()
+
+
+@pytest.mark.parametrize("name", sorted(MID_SIZE))
+def test_managed_push_within_tolerance(name):
+    """The Unified-Memory baseline (SPTRSV_PLAN_PUSH_MANAGED: left sums and
+    in-degree counters in cudaMallocManaged memory, system-scope atomics,
+    PAPER.md:226-232) solves the same systems to the same tolerance."""
+    l = MID_SIZE[name]()
+    b = np.random.default_rng(5).uniform(-1.0, 1.0, size=l.n)
+    ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="fast", executor="push",
+                              push_managed=True)
+    for _ in range(2):  # the shared state is reset between solves
+        x, st = plan.solve(b)
+        assert st["executor"] == "push"
+        assert sp.compare_solutions(x, ref, TOL).within_tol
+    plan.close()
