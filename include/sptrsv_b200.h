@@ -34,7 +34,8 @@ enum {
   SPTRSV_E_INVALID_PE = 6,       /* InvalidPeCount           errors.py:68   */
   SPTRSV_E_CUDA = 7,             /* CUDA runtime failure (no reference class) */
   SPTRSV_E_ARGUMENT = 8,         /* ValueError                               */
-  SPTRSV_E_UNSUPPORTED = 9
+  SPTRSV_E_UNSUPPORTED = 9,
+  SPTRSV_E_DEBUG_CHECK = 10     /* AssertionError: a SPTRSV_PLAN_DEBUG device check failed (engine.py:154-169) */
 };
 
 /* Arithmetic of the solve. EXACT reproduces solve_serial (reference.py:20-35)
@@ -63,9 +64,13 @@ enum {
 enum {
   SPTRSV_PLAN_STRUCTURE_ONLY = 1, /* analysis only: diagonal may be missing/zero, values may be NULL */
   SPTRSV_PLAN_NO_STREAMED_IO = 4, /* sptrsv_solve: copy all of b in, solve, copy all of x out (no overlap) */
-  SPTRSV_PLAN_PUSH_MANAGED = 8    /* executor "push": left sums and in-degree counters in cudaMallocManaged
+  SPTRSV_PLAN_PUSH_MANAGED = 8,   /* executor "push": left sums and in-degree counters in cudaMallocManaged
                                      (unified) memory, updated with system-scope atomics -- the paper's
                                      Unified-Memory baseline, for the push/pull comparison */
+  SPTRSV_PLAN_DEBUG = 16          /* device checks of the publication protocol (SolverConfig.debug,
+                                     engine.py:154-169 / 510-513): every published x slot / mailbox word is
+                                     written once, from its sentinel, by its owner PE; a violation stops the
+                                     solve with SPTRSV_E_DEBUG_CHECK */
 };
 
 typedef struct sptrsv_options {

@@ -26,6 +26,7 @@ EXECUTOR_NAME = {v: k for k, v in EXECUTOR.items()}
 PLAN_STRUCTURE_ONLY = 1
 PLAN_NO_STREAMED_IO = 4
 PLAN_PUSH_MANAGED = 8  # executor='push': shared state in unified memory, system-scope atomics
+PLAN_DEBUG = 16  # device checks: owner-only, write-once publication (SolverConfig.debug)
 
 
 class Options(C.Structure):
@@ -197,7 +198,7 @@ class NativePlan:
 
     def __init__(self, col_ptr, row_idx, values, n: int, *, precision="exact", executor="auto", device=0,
                  timeout=60.0, spin_initial=1024, spin_max_ns=64, structure_only=False, chain_lanes=32,
-                 probe_flags=0, streamed_io=True, push_managed=False):
+                 probe_flags=0, streamed_io=True, push_managed=False, debug=False):
         lib = require_gpu()
         self._lib = lib
         self.n = int(n)
@@ -209,7 +210,7 @@ class NativePlan:
         opt.executor = EXECUTOR[executor]
         opt.device = int(device)
         opt.flags = ((PLAN_STRUCTURE_ONLY if structure_only else 0) | (0 if streamed_io else PLAN_NO_STREAMED_IO)
-                     | (PLAN_PUSH_MANAGED if push_managed else 0))
+                     | (PLAN_PUSH_MANAGED if push_managed else 0) | (PLAN_DEBUG if debug else 0))
         opt.timeout_s = float(timeout)
         opt.spin_initial = int(spin_initial)
         opt.spin_max_ns = int(spin_max_ns)

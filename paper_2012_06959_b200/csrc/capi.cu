@@ -277,6 +277,7 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
     a.part_sum = split_rows.part_sum;
     a.part_done = split_rows.part_done;
   }
+  a.debug = (opt.flags & SPTRSV_PLAN_DEBUG) ? ((opt.probe_flags & 1024) ? 2 : 1) : 0;
   if (opt.probe_flags & 512) {
     // diagnostics: globaltimer of every row's publish (tools/rows_levels.py)
     if (!probe_buf || probe_words < n) {
@@ -502,6 +503,9 @@ int DevicePlan::finish(sptrsv_stats* st) {
   }
   if (hs.code == SPTRSV_E_TIMEOUT)
     return fail(SPTRSV_E_TIMEOUT, "solve exceeded " + std::to_string(opt.timeout_s) + "s (device watchdog)");
+  if (hs.code == SPTRSV_E_DEBUG_CHECK)
+    return fail(SPTRSV_E_DEBUG_CHECK, "debug check failed: publication of component " + std::to_string(hs.detail) +
+                                          " was not a single owner write over its sentinel");
   return SPTRSV_OK;
 }
 

@@ -105,8 +105,8 @@ __device__ __forceinline__ double div_exact(double a, double d, double rd) {
 
 // Device-side status word shared by all kernels of one launch.
 struct DeviceStatus {
-  int code;          // 0 ok, 5 timeout (matches SPTRSV_E_TIMEOUT)
-  int pad;
+  int code;          // 0 ok, 5 timeout (matches SPTRSV_E_TIMEOUT), 10 debug check failed
+  int detail;        // debug check: the first violating component (or mailbox word)
   unsigned long long spins;       // polls that found a dependency not ready
   unsigned long long remote_reads;  // dependency loads that crossed a PE boundary
 };

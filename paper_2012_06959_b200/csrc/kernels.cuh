@@ -73,6 +73,7 @@ struct RowsArgs {
   double* part_sum;
   int* part_done;
   long long* stamps;  // diagnostics (probe bit 512): globaltimer at each row's publish
+  int debug;          // SPTRSV_PLAN_DEBUG: check owner-only, write-once publication
 };
 
 cudaError_t launch_rows(int mode, const RowsArgs& a, int blocks, cudaStream_t s);

@@ -152,6 +152,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   if (e == cudaSuccess) e = reset_control(s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   RowsArgs a{};
+  a.debug = (opt.flags & SPTRSV_PLAN_DEBUG) ? ((opt.probe_flags & 1024) ? 2 : 1) : 0;
   a.n = (int)n;
   a.rp = rp;
   a.ci = ci;

@@ -127,10 +127,26 @@ __device__ __forceinline__ const int* slot_s32(const RowsArgs& a, int j, bool& r
   return a.lseg[p] + j;
 }
 
+// SPTRSV_PLAN_DEBUG: the reference's debug assertions (engine.py:154-169,
+// 510-513) restated for the pull protocol -- a slot is written only by the PE
+// that owns the component, and only once, over its not-ready sentinel (a
+// published value is final, the pull analogue of "counters never fall").
+__device__ __noinline__ void debug_violation(const RowsArgs& a, int i) {
+  if (atomicCAS(&a.status->code, 0, 10) == 0) a.status->detail = i;
+  atomicExch(a.abort_flag, 1);
+}
+
 __device__ __forceinline__ void publish_u64(const RowsArgs& a, int i, double v) {
   unsigned long long* p = a.xseg[a.owner ? a.my_pe : 0] + i;
+  if (a.debug && ((a.owner && a.owner[i] != a.my_pe) || ld_relaxed_u64(p) != kNotReady)) debug_violation(a, i);
   if (a.owner) st_relaxed_sys_u64(p, publishable(v));
   else st_relaxed_u64(p, publishable(v));
+  // fault injection (probe bit 1024): row 0 published a second time -- its
+  // check must find the slot already written
+  if (a.debug == 2 && i == 0) {
+    if (ld_relaxed_u64(p) != kNotReady) debug_violation(a, i);
+    st_relaxed_u64(p, publishable(v));
+  }
   if (a.stamps) a.stamps[i] = (long long)globaltimer_ns();
 }
 

@@ -179,6 +179,7 @@ struct alignas(64) StArgs {
   int x_tma_bands;  // bands [0, x_tma_bands) store interior chunks of x with one TMA store
   unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
   const double* upc;              // fast mode, kStNoSel: -L[i,i-nx] of every band's top grid row ([n_tasks][nx])
+  int debug;                      // SPTRSV_PLAN_DEBUG: every mailbox word is written once, over its sentinel
 };
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 template <bool DG>
@@ -632,6 +633,14 @@ struct HandDown {
     if (jj < 0 || jj >= nblk) return;
     const double2 v = bottom(c, k, h);
     unsigned long long* w = below + (size_t)jj * kStC + 2 * h;
+    if (a.debug) {  // (engine.py:510-513: published state only moves forward)
+      const unsigned long long o0 = PART && below_remote ? ld_relaxed_sys_u64(w) : ld_relaxed_u64(w);
+      const unsigned long long o1 = PART && below_remote ? ld_relaxed_sys_u64(w + 1) : ld_relaxed_u64(w + 1);
+      if (o0 != kStNotReady || o1 != kStNotReady) {
+        if (atomicCAS(&a.status->code, 0, 10) == 0) a.status->detail = (int)(t * (long long)a.nx + jj * kStC);
+        atomicExch(a.abort_flag, 1);
+      }
+    }
     if (PART && below_remote) {
       st_relaxed_sys_u64_if(w, as_u64(v.x), true);
       st_relaxed_sys_u64_if(w + 1, as_u64(v.y), true);
@@ -1502,6 +1511,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   StArgs a{};
   a.stream = stencil.stream;
   a.upc = stencil.upc;
+  a.debug = (opt.flags & SPTRSV_PLAN_DEBUG) != 0;
   a.mbox = stencil.mbox + par * half;
   a.mbox_next = stencil.mbox + (1 - par) * half;
   a.mbox_half = par * half;

@@ -22,8 +22,10 @@ Config mapping (SURVEY.md §8a N2): ``n_pes`` -> PE segments / GPUs;
 ``remote_read_caching`` -> accepted (a pulled x value is final, so a remote
 slot is never re-read once seen); ``capture_state`` -> post-solve
 ``EngineState`` in the reference's push-variant convention (below);
-``debug`` -> owner-only writes are structural in the kernel (each PE stores
-only into its own segment).
+``debug`` -> device checks of the publication protocol (SPTRSV_PLAN_DEBUG):
+every published x slot / mailbox word is written once, over its sentinel, by
+the PE that owns it -- the reference's write-locality and monotone-counter
+assertions (engine.py:154-169, 510-513) -- raising AssertionError.
 """
 
 from __future__ import annotations
@@ -278,6 +280,8 @@ def _run(l: CscMatrix, b, plan: PartitionPlan, cfg: SolverConfig, expected: Engi
         spin_initial=64 * cfg.spin_backoff.initial_pause,
         spin_max_ns=max(16, cfg.spin_backoff.max_pause // 8),
     )
+    if cfg.debug:
+        knobs["debug"] = True
     if expected is Engine.PARTITIONED_READ_ONLY and cfg.n_pes > 1:
         # one published segment per PE (owner-only writes, read-only peers):
         # one PE per GPU when several are visible, else the PEs share the

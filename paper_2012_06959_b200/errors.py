@@ -102,6 +102,7 @@ STATUS_INVALID_PE = 6
 STATUS_CUDA = 7
 STATUS_ARGUMENT = 8
 STATUS_UNSUPPORTED = 9
+STATUS_DEBUG_CHECK = 10  # a SPTRSV_PLAN_DEBUG device check failed
 
 
 def raise_for_status(status: int, detail: str = "", col: int = -1) -> None:
@@ -122,4 +123,7 @@ def raise_for_status(status: int, detail: str = "", col: int = -1) -> None:
         raise InvalidPeCount(detail)
     if status == STATUS_ARGUMENT:
         raise ValueError(detail)
+    if status == STATUS_DEBUG_CHECK:
+        # the reference's debug mode raises AssertionError (engine.py:163-168, 511-513)
+        raise AssertionError(detail)
     raise SptrsvError(f"native status {status}: {detail}")

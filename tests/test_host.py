@@ -131,6 +131,8 @@ def test_status_codes_map_to_reference_classes():
         errors.raise_for_status(errors.STATUS_MISSING_DIAGONAL, "", 1)
     with pytest.raises(errors.SolveTimeout):
         errors.raise_for_status(errors.STATUS_TIMEOUT, "x")
+    with pytest.raises(AssertionError):  # SolverConfig.debug device checks (engine.py:163-168)
+        errors.raise_for_status(errors.STATUS_DEBUG_CHECK, "x")
     errors.raise_for_status(errors.STATUS_OK)
 
 
