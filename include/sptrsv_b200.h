@@ -159,6 +159,14 @@ int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* st
  * `stream` a cudaStream_t (0 = the plan's stream). Asynchronous. */
 int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x, void* stream);
 
+/* k right-hand sides, b and x laid out [k][n] (row-major: right-hand side r
+ * at offset r * n). The 2D stencil executor stacks up to 16 of them into one
+ * launch (its 64-band wavefront leaves most SMs idle; stacked copies fill
+ * them); every other executor solves them one after another. Replaces the
+ * host loop of extensions.solve_many (reference: one solve() per b). */
+int sptrsv_solve_device_many_async(sptrsv_plan* plan, const double* d_b, double* d_x, int32_t k, void* stream);
+int sptrsv_solve_many(sptrsv_plan* plan, const double* b, double* x, int32_t k, sptrsv_stats* stats);
+
 /* Wait for the plan's work and report the device status of the last solve
  * (SPTRSV_E_TIMEOUT if the watchdog tripped). */
 int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats);

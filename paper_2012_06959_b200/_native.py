@@ -124,6 +124,10 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_solve.restype = C.c_int
     lib.sptrsv_solve_device_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.sptrsv_solve_device_async.restype = C.c_int
+    lib.sptrsv_solve_device_many_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
+    lib.sptrsv_solve_device_many_async.restype = C.c_int
+    lib.sptrsv_solve_many.argtypes = [C.c_void_p, _PD, _PD, C.c_int32, C.POINTER(Stats)]
+    lib.sptrsv_solve_many.restype = C.c_int
     lib.sptrsv_synchronize.argtypes = [C.c_void_p, C.POINTER(Stats)]
     lib.sptrsv_synchronize.restype = C.c_int
     lib.sptrsv_plan_destroy.argtypes = [C.c_void_p]
@@ -312,6 +316,26 @@ class NativePlan:
         d = st.as_dict()
         d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
         return x, d
+
+    def solve_many(self, bs: np.ndarray, out: np.ndarray | None = None) -> tuple[np.ndarray, dict]:
+        """k right-hand sides, ``bs`` shaped (k, n) (one per row): one stacked
+        launch on the 2D stencil executor, else k solves on the device."""
+        bs = np.ascontiguousarray(bs, dtype=np.float64)
+        if bs.ndim != 2 or bs.shape[1] != self.n:
+            raise ValueError(f"right-hand sides must be shaped (k, {self.n}), got {bs.shape}")
+        x = out if out is not None else np.empty_like(bs)
+        st = Stats()
+        rc = self._lib.sptrsv_solve_many(self._h, _ptr(bs, C.c_double), _ptr(x, C.c_double), bs.shape[0],
+                                         C.byref(st))
+        raise_for_status(rc, _err(self._lib))
+        d = st.as_dict()
+        d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
+        return x, d
+
+    def solve_device_many_async(self, d_b: int, d_x: int, k: int, stream: int = 0) -> None:
+        rc = self._lib.sptrsv_solve_device_many_async(self._h, C.c_void_p(d_b), C.c_void_p(d_x), int(k),
+                                                      C.c_void_p(stream))
+        raise_for_status(rc, _err(self._lib))
 
     def solve_device_async(self, d_b: int, d_x: int, stream: int = 0) -> None:
         rc = self._lib.sptrsv_solve_device_async(self._h, C.c_void_p(d_b), C.c_void_p(d_x), C.c_void_p(stream))

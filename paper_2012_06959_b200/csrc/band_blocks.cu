@@ -314,7 +314,7 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   sa.S = bblk.S;
   sa.nblk = bblk.nblk;
   const int grid = (bblk.nblk + kBBWarps - 1) / kBBWarps;
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   // K1: c tails
   sa.out = bblk.ct;
   k_bb_sweep<false><<<grid, 32 * kBBWarps, 0, s>>>(sa);

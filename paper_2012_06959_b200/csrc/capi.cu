@@ -288,10 +288,48 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
     }
     a.stamps = probe_buf;
   }
-  CUDA_TRY(cudaEventRecord(evk0, s));
+  CUDA_TRY(record_k0(s));
   CUDA_TRY(launch_rows(mode, a, rows_grid(mode), s));
   CUDA_TRY(cudaEventRecord(evk1, s));
   launches = 1;
+  return SPTRSV_OK;
+}
+
+int DevicePlan::solve_device_many(const double* d_b, double* d_x, int k, cudaStream_t s) {
+  if (structure_only) return fail(SPTRSV_E_ARGUMENT, "plan was created structure-only; it cannot solve");
+  if (k == 1) return solve_device(d_b, d_x, s);
+  // the 2D stencil stacks up to kMaxStack right-hand sides per launch: its
+  // 64 bands use 64 of the 148 SMs, so stacked copies fill the idle SMs and
+  // each copy's bands start as soon as an SM frees up
+  constexpr int kMaxStack = 16;
+  const bool stack = executor_used == SPTRSV_EXECUTOR_STENCIL && !stencil3.ready && stencil.ready && !stencil.part &&
+                     !seg_table && stencil.ny % 64 == 0;
+  CUDA_TRY(cudaEventRecord(ev0, s));
+  int total_launches = 0;
+  for (int r = 0; r < k;) {
+    const int c = stack ? std::min(kMaxStack, k - r) : 1;
+    const double* b = d_b + (size_t)r * n;
+    double* x = d_x + (size_t)r * n;
+    int rc;
+    if (stack && c > 1) rc = solve_stencil(b, x, s, false, false, c);
+    else if (executor_used == SPTRSV_EXECUTOR_STENCIL)
+      rc = stencil3.ready ? solve_stencil3d(b, x, s) : solve_stencil(b, x, s);
+    else if (executor_used == SPTRSV_EXECUTOR_PUSH) rc = solve_push(b, x, s);
+    else if (executor_used == SPTRSV_EXECUTOR_BAND) rc = bblk.ready ? solve_band_blocks(b, x, s) : solve_band(b, x, s);
+    else if (executor_used == SPTRSV_EXECUTOR_CHAINS) rc = solve_chains(b, x, s);
+    else rc = solve_rows(b, x, s);
+    batch_k0 = true;  // the kernel events span every launch of the batch
+    if (rc != SPTRSV_OK) {
+      batch_k0 = false;
+      return rc;
+    }
+    total_launches += launches;
+    r += c;
+  }
+  launches = total_launches;
+  batch_k0 = false;
+  CUDA_TRY(cudaEventRecord(ev1, s));
+  pending = true;
   return SPTRSV_OK;
 }
 
@@ -664,6 +702,43 @@ int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* st
     stats->e2e_ms = ms_since(t0);
   }
   return SPTRSV_OK;
+}
+
+int sptrsv_solve_device_many_async(sptrsv_plan* plan, const double* d_b, double* d_x, int32_t k, void* stream) {
+  g_err.clear();
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || k < 0) return fail(SPTRSV_E_ARGUMENT, "null plan or negative k");
+  if (p->n == 0 || k == 0) return SPTRSV_OK;
+  if (!d_b || !d_x) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = stream ? reinterpret_cast<cudaStream_t>(stream) : p->stream;
+  return p->solve_device_many(d_b, d_x, k, s);
+}
+
+int sptrsv_solve_many(sptrsv_plan* plan, const double* b, double* x, int32_t k, sptrsv_stats* stats) {
+  g_err.clear();
+  auto* p = reinterpret_cast<DevicePlan*>(plan);
+  if (!p || k < 0) return fail(SPTRSV_E_ARGUMENT, "null plan or negative k");
+  if (p->n == 0 || k == 0) return p->finish(stats);
+  if (!b || !x) return fail(SPTRSV_E_ARGUMENT, "null argument");
+  CUDA_TRY(cudaSetDevice(p->device));
+  const size_t bytes = sizeof(double) * (size_t)p->n * k;
+  double *db = nullptr, *dx = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&db, bytes, p->stream));
+  CUDA_TRY(cudaMallocAsync((void**)&dx, bytes, p->stream));
+  auto t0 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, p->stream));
+  int rc = p->solve_device_many(db, dx, k, p->stream);
+  if (rc == SPTRSV_OK) rc = p->finish(stats);
+  if (rc == SPTRSV_OK) {
+    CUDA_TRY(cudaMemcpyAsync(x, dx, bytes, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    if (stats) stats->e2e_ms = ms_since(t0);
+  }
+  cudaFreeAsync(db, p->stream);
+  cudaFreeAsync(dx, p->stream);
+  cudaStreamSynchronize(p->stream);
+  return rc;
 }
 
 int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x, void* stream) {

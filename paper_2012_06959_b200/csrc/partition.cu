@@ -180,7 +180,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   // grid_cap: this PE's share of the SMs when several PEs' kernels share the device
   int blocks = std::max(1, (grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms) * std::max(per_sm, 1));
   blocks = std::max(n_pe_local, blocks - blocks % n_pe_local);
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = launch_rows(mode, a, blocks, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if (d_x) {

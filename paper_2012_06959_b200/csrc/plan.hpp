@@ -20,6 +20,8 @@ struct DevicePlan {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;    // whole solve (resets + kernel)
   cudaEvent_t evk0 = nullptr, evk1 = nullptr;  // the solve kernel alone
+  bool batch_k0 = false;  // solve_device_many: evk0 stays at the batch's first launch
+  cudaError_t record_k0(cudaStream_t s) { return batch_k0 ? cudaSuccess : cudaEventRecord(evk0, s); }
 
   // CSR of off-diagonals + diagonal (preprocess.cu)
   int* rp = nullptr;
@@ -168,7 +170,11 @@ struct DevicePlan {
   int build_chains(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
   bool chains_preferred() const;
   int build_stencil(const std::vector<int>& h_rp, const std::vector<int>& h_ci);
-  int solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags = false, bool x_flags = false);
+  int solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags = false, bool x_flags = false,
+                    int copies = 1);
+  // k right-hand sides ([k][n] in d_b / d_x): one stacked launch where the
+  // executor supports it (2D stencil, whole bands), else k solves in order
+  int solve_device_many(const double* d_b, double* d_x, int k, cudaStream_t s);
   // host-buffer solve with band-granular H2D of b / D2H of x overlapping the
   // stencil kernel (copy streams + stream memory operations on band flags)
   cudaStream_t cs_in = nullptr, cs_out = nullptr;

@@ -315,7 +315,7 @@ int DevicePlan::solve_band(const double* d_b, double* d_x, cudaStream_t s) {
   a.nchunks = band.nchunks;
   a.exact = opt.precision != SPTRSV_PRECISION_FAST;
   const int mode = a.exact ? 1 : 0;
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = launch_band(a, mode, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 1;

@@ -386,7 +386,7 @@ int DevicePlan::solve_chains(const double* d_b, double* d_x, cudaStream_t s) {
   }
   // one warp per CTA, at most 2 CTAs per SM (shared-memory budget)
   const int blocks = std::max(1, std::min(chains.n_tasks, num_sms * 2));
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   const int w = chains.max_width;
   if (chains.exact) e = probe ? launch_width<true, true>(w, a, blocks, s) : launch_width<true, false>(w, a, blocks, s);
   else e = probe ? launch_width<false, true>(w, a, blocks, s) : launch_width<false, false>(w, a, blocks, s);

@@ -241,7 +241,7 @@ int DevicePlan::solve_push(const double* d_b, double* d_x, cudaStream_t s) {
   if (fast) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<true, false>, 256, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_push<false, false>, 256, 0);
   const int blocks = std::max(1, num_sms * std::max(per_sm, 1));
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if (fast) sys ? k_push<true, true><<<blocks, 256, 0, s>>>(a) : k_push<true, false><<<blocks, 256, 0, s>>>(a);
   else sys ? k_push<false, true><<<blocks, 256, 0, s>>>(a) : k_push<false, false><<<blocks, 256, 0, s>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));

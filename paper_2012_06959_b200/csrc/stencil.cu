@@ -180,7 +180,16 @@ struct alignas(64) StArgs {
   unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
   const double* upc;              // fast mode, kStNoSel: -L[i,i-nx] of every band's top grid row ([n_tasks][nx])
   int debug;                      // SPTRSV_PLAN_DEBUG: every mailbox word is written once, over its sentinel
+  // several right-hand sides in one launch (solve_many): b and x are k
+  // stacked [ny][nx] grids, i.e. one grid of k * ny rows whose tasks t are
+  // band t % bands of right-hand side t / bands -- every copy reads the same
+  // coefficient stream, and the first band of a copy has no band above
+  int bands;
 };
+// task t has a band below it in the same right-hand side
+__device__ __forceinline__ bool st_has_below(const StArgs& a, int t) {
+  return t + 1 < a.n_tasks && (t + 1) % a.bands != 0;
+}
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 template <bool DG>
 __device__ __forceinline__ long long* st_stamp(const StArgs& a, int t, int c, int lane, int slot) {
@@ -370,7 +379,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int y0 = t * kStBand + kStR * lane;
-  const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+  const unsigned char* tstream = a.stream + (size_t)(t % a.bands) * a.steps * S::kStep;
   const bool b_tma = kStBTma && t < a.b_tma_bands;
   bool ok = true;
   // chunk c: its coefficient block and, per lane and grid row, the b segment of
@@ -492,7 +501,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
                        bool above_in_cluster) {
   using S = StSmem<EXACT>;
   if (above_in_cluster) return;  // the band above pushes into our inbox itself
-  if (t == 0) {
+  if (t % a.bands == 0) {
     // no band above: the top grid row's "row above" is zero, so the compute
     // warp's lane 0 reads zeros from the inbox like any other band (no
     // per-step has_above select)
@@ -627,7 +636,7 @@ struct HandDown {
   }
   __device__ __forceinline__ void publish(int c, int lane) const {
     constexpr int kHalves = kStC / 2;
-    if (t + 1 >= a.n_tasks || lane >= kStG * kHalves) return;
+    if (!st_has_below(a, t) || lane >= kStG * kHalves) return;
     const int k = lane / kHalves, h = lane % kHalves;
     const int jj = c * kStG + k - (kStLanes - 1);
     if (jj < 0 || jj >= nblk) return;
@@ -686,7 +695,7 @@ __device__ void publisher(const StArgs& a, unsigned char* smem, int* ctl, int t,
   using S = StSmem<EXACT>;
   HandDown<EXACT, PART> hd(a, smem, ctl, t, crank, below_in_cluster);
   const int nchunks = a.steps / kStG;
-  const bool any = t + 1 < a.n_tasks;
+  const bool any = st_has_below(a, t);
   for (int c = 0; c < nchunks; ++c) {
     unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + S::kOutBars) + c % kStOutSlots;
     const unsigned par = (unsigned)(c / kStOutSlots) & 1u;
@@ -904,7 +913,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   unsigned long long* below = a.mbox + (size_t)t * a.nx;
   // the band below on another PE reads these over NVLink: system-scope stores
   const bool below_remote = a.band_owner && t + 1 < a.n_tasks && a.band_owner[t + 1] != a.my_pe;
-  const bool publish = lane == kStLanes - 1 && t + 1 < a.n_tasks && !below_remote;
+  const bool publish = lane == kStLanes - 1 && st_has_below(a, t) && !below_remote;
   const bool publish_sys = lane == kStLanes - 1 && below_remote;
   const bool solo = (a.probe & 32) != 0;  // diagnostics: run without the helper warps
   constexpr bool kStSpec = EXACT && SPTRSV_ST_SPEC && kStC % 2 == 0;
@@ -1201,7 +1210,7 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
     const int t = ctl[kCtlTask];
     if (t < 0) break;
     if (t < a.n_tasks) {
-      const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && t + 1 < a.n_tasks;
+      const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && st_has_below(a, t);
       if (warp == 0)
         compute<EXACT, ABL, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
       else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
@@ -1494,11 +1503,39 @@ cudaError_t stencil_release_flags(unsigned* f, int n, unsigned v, cudaStream_t s
   return cudaGetLastError();
 }
 
-int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags) {
+int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags,
+                              int copies) {
   if (!stencil.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 2D five-point lower structured");
   cudaError_t e;
-  const long long half = (long long)stencil.n_tasks * stencil.nx;
-  const int par = (int)(stencil.solves & 1);
+  // k right-hand sides stacked into one grid of k * ny rows (full bands only)
+  const bool many = copies > 1;
+  if (many && (stencil.part || b_flags || x_flags || stencil.ny % kStBand != 0))
+    return plan_fail(SPTRSV_E_UNSUPPORTED, "stacked right-hand sides need whole bands and a one-PE plan");
+  if (many && copies > stencil.many_k) {
+    if (stencil.mbox_many) cudaFree(stencil.mbox_many);
+    stencil.mbox_many = nullptr;
+    stencil.many_k = 0;
+    const long long words = 2ll * copies * stencil.n_tasks * stencil.nx;
+    if ((e = cudaMalloc((void**)&stencil.mbox_many, sizeof(unsigned long long) * words)) != cudaSuccess ||
+        (e = fill_not_ready(stencil.mbox_many, words, s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    stencil.many_k = copies;
+    stencil.many_solves = 0;
+    stencil.many_last = copies;
+  }
+  if (many && copies != stencil.many_last) {
+    // each solve re-arms (for the next one) only the rows its own copies used
+    if ((e = fill_not_ready(stencil.mbox_many, 2ll * stencil.many_k * stencil.n_tasks * stencil.nx, s)) !=
+        cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    stencil.many_last = copies;
+    stencil.many_solves = 0;
+  }
+  const int n_tasks = stencil.n_tasks * (many ? copies : 1);
+  unsigned long long* mbox = many ? stencil.mbox_many : stencil.mbox;
+  // (the stacked mailboxes keep their halves at the allocated size)
+  const long long half = (long long)(many ? stencil.many_k * stencil.n_tasks : stencil.n_tasks) * stencil.nx;
+  const int par = (int)((many ? stencil.many_solves : stencil.solves) & 1);
   if (stencil.part) {
     for (int t : stencil.host_my_tasks)
       if (t > 0 && !stencil.host_pe_mbox[stencil.host_band_owner[t - 1]])
@@ -1512,11 +1549,11 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.stream = stencil.stream;
   a.upc = stencil.upc;
   a.debug = (opt.flags & SPTRSV_PLAN_DEBUG) != 0;
-  a.mbox = stencil.mbox + par * half;
-  a.mbox_next = stencil.mbox + (1 - par) * half;
+  a.mbox = mbox + par * half;
+  a.mbox_next = mbox + (1 - par) * half;
   a.mbox_half = par * half;
   a.ticket = ticket;
-  a.n_my_tasks = stencil.n_tasks;
+  a.n_my_tasks = n_tasks;
   a.my_pe = -1;
   if (stencil.part) {
     a.my_tasks = stencil.my_tasks;
@@ -1533,14 +1570,15 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.nx = stencil.nx;
-  a.ny = stencil.ny;
-  a.n_tasks = stencil.n_tasks;
+  a.ny = stencil.ny * (many ? copies : 1);
+  a.n_tasks = n_tasks;
+  a.bands = stencil.n_tasks;
   a.steps = stencil.steps_per_task;
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
-  a.b_tma_bands = (kStBTma && a.b_aligned) ? encode_b_map(&a.bmap, d_b, stencil.nx, stencil.ny) : 0;
+  a.b_tma_bands = (kStBTma && a.b_aligned) ? encode_b_map(&a.bmap, d_b, stencil.nx, a.ny) : 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
-  a.x_tma_bands = (SPTRSV_ST_X_TMA && kStBTma && a.x_aligned) ? encode_b_map(&a.xmap, d_x, stencil.nx, stencil.ny) : 0;
+  a.x_tma_bands = (SPTRSV_ST_X_TMA && kStBTma && a.x_aligned) ? encode_b_map(&a.xmap, d_x, stencil.nx, a.ny) : 0;
   if (b_flags) a.bflag = stencil.bflag;
   if (x_flags) a.xflag = stencil.xflag;
   a.epoch = stencil.epoch;
@@ -1553,8 +1591,8 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     a.dbg = probe_buf;
   }
   const int blocks = std::max(1, std::min(a.n_my_tasks, grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms));
-  ++stencil.solves;
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  ++(many ? stencil.many_solves : stencil.solves);
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));

@@ -77,6 +77,12 @@ struct StencilPlan {
   // a PE never resets a half a peer may still be reading (consecutive solves
   // are separated by a barrier across PEs).
   long long solves = 0;
+  // several right-hand sides per launch (solve_many): mailboxes of k stacked
+  // copies, [2][k * n_tasks][nx], grown on demand, with their own parity
+  unsigned long long* mbox_many = nullptr;
+  int many_k = 0;
+  int many_last = 0;  // copies of the previous stacked solve (a different count re-arms every word)
+  long long many_solves = 0;
   // PE partition, one PE per process (set_partition with my_pe >= 0 on a
   // band-aligned owner map): this PE solves its own bands (ascending), reads
   // the band above a PE boundary from the owning peer's mailboxes (CUDA IPC
@@ -107,12 +113,16 @@ struct StencilPlan {
   }
   void release() {
     release_part();
-    void* ptrs[] = {stream, mbox, bflag, xflag, upc};
+    void* ptrs[] = {stream, mbox, bflag, xflag, upc, mbox_many};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
     upc = nullptr;
     mbox = nullptr;
+    mbox_many = nullptr;
+    many_k = 0;
+    many_last = 0;
+    many_solves = 0;
     bflag = xflag = nullptr;
     epoch = 0;
     solves = 0;

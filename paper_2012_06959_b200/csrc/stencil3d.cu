@@ -832,7 +832,7 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, 
   }
   const int blocks = std::max(1, std::min(P.n_tasks, num_sms));
   ++P.solves;
-  if ((e = cudaEventRecord(evk0, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = P.exact ? launch_s3<true>(a, blocks, s) : launch_s3<false>(a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));

@@ -56,16 +56,21 @@ def solve_upper(u: CscMatrix, b, *, precision: str = "exact", executor: str = "a
 
 
 def solve_many(l: CscMatrix, bs, *, precision: str = "exact", executor: str = "auto", device: int | None = None):
-    """``L X = B`` for the columns of ``bs`` (n x k), one cached device plan, k solves."""
+    """``L X = B`` for the columns of ``bs`` (n x k) through one cached device
+    plan and one native call (``sptrsv_solve_many``): the 2D stencil executor
+    solves up to 16 right-hand sides per launch, stacked into one grid (its
+    64-band wavefront leaves most of the 148 SMs idle), every other executor
+    solves them back to back on the device. Each column's x is what ``solve``
+    gives for it (bitwise in exact mode)."""
     bs = np.asarray(bs, dtype=np.float64)
     if bs.ndim != 2 or bs.shape[0] != l.n:
         raise DimensionMismatch(f"rhs block has shape {bs.shape}, matrix is {l.n}x{l.n}")
+    if bs.shape[1] == 0 or l.n == 0:
+        return np.zeros_like(bs)
     dev = _native.env_device() if device is None else device
     plan = _native.plan_for(l, precision=precision, executor=executor, device=dev)
-    out = np.empty_like(bs)
-    for k in range(bs.shape[1]):
-        out[:, k], _ = plan.solve(np.ascontiguousarray(bs[:, k]))
-    return out
+    x, _ = plan.solve_many(np.ascontiguousarray(bs.T))
+    return np.ascontiguousarray(x.T)
 
 
 _rev: dict = {}

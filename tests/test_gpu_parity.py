@@ -519,3 +519,32 @@ def test_levels_fast_paths_bit_exact(name):
     assert n_levels == nl
     np.testing.assert_array_equal(level_of, lv)
     plan.close()
+
+
+@pytest.mark.parametrize("shape,k", [((128, 192), 5), ((256, 64), 17), ((96, 128), 1), ((64, 100), 3)])
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_solve_many_stacked_stencil(shape, k, precision):
+    """Several right-hand sides through one stacked 2D-stencil launch (whole
+    bands: 192 / 64 rows; k = 17 takes two launches of <= 16), or one solve
+    after another when the last band is partial (100 rows): each column is
+    bitwise the oracle's (exact) / within 1e-12 (fast), repeated so the
+    stacked mailboxes are re-armed between solves and between k's."""
+    l = synth.lap2d(*shape)
+    rng = np.random.default_rng(k)
+    for kk in (k, max(1, k - 2), k):
+        bs = rng.uniform(-1, 1, (l.n, kk))
+        xs = sp.solve_many(l, bs, precision=precision, executor="stencil")
+        for c in range(kk):
+            ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, bs[:, c].copy())
+            if precision == "exact":
+                assert xs[:, c].tobytes() == ref.tobytes(), (kk, c)
+            else:
+                assert sp.compare_solutions(xs[:, c], ref, FAST_TOL).within_tol, (kk, c)
+
+
+def test_solve_many_rows_executor():
+    l = synth.rmat(11, 8, 2)
+    bs = np.random.default_rng(9).uniform(-1, 1, (l.n, 4))
+    xs = sp.solve_many(l, bs, precision="exact", executor="rows")
+    for c in range(4):
+        assert xs[:, c].tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, bs[:, c].copy()).tobytes()
