@@ -25,7 +25,8 @@ configured matrix with b = ones (the reference CLI default, cli.py:139-140).
 * ``cpu_baseline``: the C port of the reference ``solve_serial`` (oracle/) on
   one host core, full matrix (rank 0, N = 1 only).
 
-N > 1 (torchrun, one process per GPU): block_partition(n, N) — every GPU owns a
+N > 1 (torchrun, one process per GPU): block_partition(n, N) (``--partition
+nnz``, the default for rmat: slabs of equal nnz, nnz_block_partition) — every GPU owns a
 contiguous slab of rows (for lap2d-4096: whole 64-grid-row bands of the
 stencil executor) and its x; the peer state (stencil mailboxes, or component
 segments) is opened over CUDA IPC and read with one-sided loads inside the
@@ -166,6 +167,9 @@ def main():
     ap.add_argument("--precision", choices=["fast", "exact"], default="fast")
     ap.add_argument("--executor", choices=["auto", "rows", "chains", "stencil", "push", "band"], default="auto")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--partition", choices=["auto", "block", "nnz"], default="auto",
+                    help="N > 1 owner map: block_partition (reference), or contiguous slabs of equal nnz "
+                         "(64-row aligned); auto: nnz for configs without grid structure (rmat), else block")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--l2", choices=["auto", "flush", "warm"], default="auto",
                     help="auto: flush a 256 MB scratch buffer between timed solves when the solve's inputs are "
@@ -211,7 +215,12 @@ def main():
     if ws > 1:
         from paper_2012_06959_b200 import multi
 
-        partition = multi.rank_partition(n, ws, "block")
+        kind = args.partition
+        if kind == "auto":
+            kind = "block" if args.config.startswith(("lap2d", "lap3d", "banded")) else "nnz"
+        # rows' entry counts (CSC column counts of the transpose = row counts)
+        row_w = np.bincount(np.asarray(l.row_idx), minlength=n).astype(np.float64) if kind == "nnz" else None
+        partition = multi.rank_partition(n, ws, kind, row_weight=row_w, align=64)
         solver = multi.DistributedSolver(l, partition, rank, device=dev, precision=args.precision)
         plan = solver.native
         owned = torch.from_numpy((partition.owner_arr == rank).astype(np.float64)).to(f"cuda:{dev}")
@@ -397,7 +406,8 @@ def main():
             "rhs": "ones",
             "precision": args.precision,
             "executor": info["executor"],
-            "parallelism": f"column-block x{ws} (block_partition), IPC peer segments" if ws > 1 else "single GPU",
+            "parallelism": (f"column-block x{ws} ({partition.kind} partition), IPC peer segments" if ws > 1
+                            else "single GPU"),
             "l2": (f"flushed: 256 MB scratch write between timed solves (solve inputs {alg / 1e6:.0f} MB vs "
                    f"{l2_bytes / 1e6:.0f} MB L2)") if flush else
                   f"back-to-back: solve inputs {alg / 1e6:.0f} MB vs {l2_bytes / 1e6:.0f} MB L2",

@@ -23,13 +23,19 @@ from __future__ import annotations
 
 import numpy as np
 
-from .partition import PartitionPlan, block_partition, task_round_robin_partition
+from .partition import PartitionPlan, block_partition, nnz_block_partition, task_round_robin_partition
 
 
-def rank_partition(n: int, world: int, kind: str = "block", tasks_per_pe: int = 1) -> PartitionPlan:
-    """The partition every rank must agree on (deterministic in its arguments)."""
+def rank_partition(n: int, world: int, kind: str = "block", tasks_per_pe: int = 1, row_weight=None,
+                   align: int = 1) -> PartitionPlan:
+    """The partition every rank must agree on (deterministic in its arguments).
+
+    ``kind="nnz"``: contiguous slabs of equal total ``row_weight`` (entries per
+    row), boundaries on multiples of ``align`` rows."""
     if kind == "block":
         return block_partition(n, world)
+    if kind == "nnz":
+        return nnz_block_partition(np.ones(n) if row_weight is None else row_weight, world, align)
     return task_round_robin_partition(n, world, tasks_per_pe)
 
 

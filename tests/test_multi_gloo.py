@@ -32,7 +32,8 @@ def _worker(rank, world, port, kind, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         l = synth.lap2d(16, 12)
-        plan = multi.rank_partition(l.n, world, kind, tasks_per_pe=3)
+        w = np.diff(np.asarray(l.col_ptr))  # entries per column: a skewed weight
+        plan = multi.rank_partition(l.n, world, kind, tasks_per_pe=3, row_weight=w)
         # a fake 64-byte "IPC handle" per rank
         handle = bytes([rank]) * 64
         handles = multi.exchange_handles(handle)
@@ -47,7 +48,7 @@ def _worker(rank, world, port, kind, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["block", "round-robin"])
+@pytest.mark.parametrize("kind", ["block", "round-robin", "nnz"])
 def test_two_ranks_exchange_handles_and_assemble_x(kind):
     world = 2
     ctx = mp.get_context("spawn")
@@ -77,3 +78,29 @@ def test_rank_partition_is_deterministic():
     b = multi.rank_partition(1000, 8)
     np.testing.assert_array_equal(a.owner_arr, b.owner_arr)
     assert np.bincount(a.owner_arr).tolist() == [125] * 8
+
+
+def test_nnz_block_partition_balances_work():
+    """Contiguous slabs of equal total weight (block_partition
+    leaves rmat's power-law rows 8.4x imbalanced over 8 PEs)."""
+    import paper_2012_06959_b200 as sp
+    rng = np.random.default_rng(0)
+    w = np.floor(rng.pareto(1.2, 200_000) + 1)  # power-law row weights
+    w[:5000] *= 50  # a heavy head, like low-numbered rmat rows
+    for pes in (2, 4, 8):
+        blk = sp.block_partition(w.size, pes)
+        nnz = sp.nnz_block_partition(w, pes)
+        load_blk = np.bincount(blk.owner_arr, weights=w)
+        load_nnz = np.bincount(nnz.owner_arr, weights=w)
+        # within one row's weight of the mean (contiguous slabs cannot do better)
+        assert load_nnz.max() <= load_nnz.mean() + w.max()
+        assert load_nnz.max() / load_nnz.mean() < load_blk.max() / load_blk.mean()
+        # contiguous, ascending, every row owned once
+        assert np.all(np.diff(nnz.owner_arr) >= 0) and nnz.owner_arr.size == w.size
+        assert [t.owner_pe for t in nnz.tasks] == list(range(pes))
+    # band alignment: every boundary on a multiple of 64 rows
+    al = sp.nnz_block_partition(w[:64 * 1000], 8, align=64)
+    assert all(t.first % 64 == 0 for t in al.tasks)
+    from paper_2012_06959_b200.errors import InvalidPeCount
+    with pytest.raises(InvalidPeCount):
+        sp.nnz_block_partition(np.ones(3), 4)
