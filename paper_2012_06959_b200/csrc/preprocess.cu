@@ -21,31 +21,72 @@ namespace sptrsv {
 // and records the first lower-triangular violation as key = col*4 + kind, kind:
 // 0 MissingDiagonal, 1 UpperTriangularEntry, 2 ZeroDiagonal, which is the
 // reference's (col, kind-name) order (matrix.py:150).
+// One warp per 32 consecutive columns: short columns (<= kShortCol entries)
+// one per lane, longer ones by the whole warp in lane order afterwards -- a
+// power-law column (rmat-4M's largest hold ~10^5 entries) walked by a single
+// thread left the whole launch waiting on that thread (2 s of plan setup).
+constexpr int kShortCol = 64;
 __global__ void k_expand_validate(const long long* __restrict__ cp, const long long* __restrict__ ri64,
                                   const double* __restrict__ val, int n, int* __restrict__ colE,
                                   int* __restrict__ ri32, unsigned long long* __restrict__ first_violation,
                                   int* __restrict__ structure_bad, int need_diag) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    long long lo = cp[j], hi = cp[j + 1];
-    bool has_diag = false, upper = false, zero = false;
-    long long prev = -1;
-    for (long long k = lo; k < hi; ++k) {
-      long long r = ri64[k];
-      if (r < 0 || r >= n || r <= prev) { atomicExch(structure_bad, 1); }
-      prev = r;
-      colE[k] = j;
-      ri32[k] = (int)r;
-      if (r < j) upper = true;
-      if (r == j) {
-        has_diag = true;
-        if (val != nullptr && val[k] == 0.0) zero = true;
+  const int lane = threadIdx.x & 31;
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * 32 < n; w += warps) {
+    const long long j0 = w * 32;
+    const int j = (int)(j0 + lane);
+    long long lo = 0, hi = 0;
+    if (j < n) lo = cp[j], hi = cp[j + 1];
+    const bool is_long = j < n && hi - lo > kShortCol;
+    auto verdict = [&](int col, bool has_diag, bool upper, bool zero) {
+      unsigned long long key = ~0ull;
+      if (need_diag && !has_diag) key = 4ull * col + 0;
+      else if (upper) key = 4ull * col + 1;
+      else if (need_diag && zero) key = 4ull * col + 2;
+      if (key != ~0ull) atomicMin(first_violation, key);
+    };
+    if (j < n && !is_long) {
+      bool has_diag = false, upper = false, zero = false;
+      long long prev = -1;
+      for (long long k = lo; k < hi; ++k) {
+        long long r = ri64[k];
+        if (r < 0 || r >= n || r <= prev) { atomicExch(structure_bad, 1); }
+        prev = r;
+        colE[k] = j;
+        ri32[k] = (int)r;
+        if (r < j) upper = true;
+        if (r == j) {
+          has_diag = true;
+          if (val != nullptr && val[k] == 0.0) zero = true;
+        }
       }
+      verdict(j, has_diag, upper, zero);
     }
-    unsigned long long key = ~0ull;
-    if (need_diag && !has_diag) key = 4ull * j + 0;
-    else if (upper) key = 4ull * j + 1;
-    else if (need_diag && zero) key = 4ull * j + 2;
-    if (key != ~0ull) atomicMin(first_violation, key);
+    unsigned longs = __ballot_sync(0xffffffffu, is_long);
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const int col = (int)(j0 + src);
+      const long long clo = __shfl_sync(0xffffffffu, lo, src), chi = __shfl_sync(0xffffffffu, hi, src);
+      bool has_diag = false, upper = false, zero = false, bad = false;
+      for (long long k = clo + lane; k < chi; k += 32) {
+        const long long r = ri64[k];
+        const long long prev = k > clo ? ri64[k - 1] : -1;
+        if (r < 0 || r >= n || r <= prev) bad = true;
+        colE[k] = col;
+        ri32[k] = (int)r;
+        if (r < col) upper = true;
+        if (r == col) {
+          has_diag = true;
+          if (val != nullptr && val[k] == 0.0) zero = true;
+        }
+      }
+      if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(structure_bad, 1);
+      has_diag = __any_sync(0xffffffffu, has_diag);
+      upper = __any_sync(0xffffffffu, upper);
+      zero = __any_sync(0xffffffffu, zero);
+      if (lane == 0) verdict(col, has_diag, upper, zero);
+    }
   }
 }
 
@@ -135,7 +176,8 @@ static inline int grid_for(long long work, int block) {
 cudaError_t launch_expand_validate(const long long* cp, const long long* ri64, const double* val, int n, int* colE,
                                    int* ri32, unsigned long long* first_violation, int* structure_bad, int need_diag,
                                    cudaStream_t s) {
-  k_expand_validate<<<grid_for(n, 256), 256, 0, s>>>(cp, ri64, val, n, colE, ri32, first_violation, structure_bad, need_diag);
+  k_expand_validate<<<grid_for((n + 31) / 32 * 32, 256), 256, 0, s>>>(cp, ri64, val, n, colE, ri32, first_violation,
+                                                                        structure_bad, need_diag);
   return cudaGetLastError();
 }
 
