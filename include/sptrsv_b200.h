@@ -159,6 +159,13 @@ int sptrsv_solve(sptrsv_plan* plan, const double* b, double* x, sptrsv_stats* st
  * `stream` a cudaStream_t (0 = the plan's stream). Asynchronous. */
 int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x, void* stream);
 
+/* The device counters of this plan's last finished solve: dependency polls
+ * that found the value not yet published, and dependency loads that crossed a
+ * PE boundary. After sptrsv_solve_group each PE's plan holds its own -- the
+ * measured per-PE lock_wait_spins / remote_reads_issued of SolveReport.per_pe
+ * (reference PeStats, engine.py:100-111). */
+int sptrsv_plan_last_counters(const sptrsv_plan* plan, int64_t* spins, int64_t* remote_reads);
+
 /* k right-hand sides, b and x laid out [k][n] (row-major: right-hand side r
  * at offset r * n). The 2D stencil executor stacks up to 16 of them into one
  * launch (its 64-band wavefront leaves most SMs idle; stacked copies fill

@@ -124,6 +124,8 @@ def _bind(lib: C.CDLL) -> None:
     lib.sptrsv_solve.restype = C.c_int
     lib.sptrsv_solve_device_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.sptrsv_solve_device_async.restype = C.c_int
+    lib.sptrsv_plan_last_counters.argtypes = [C.c_void_p, _P64, _P64]
+    lib.sptrsv_plan_last_counters.restype = C.c_int
     lib.sptrsv_solve_device_many_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]
     lib.sptrsv_solve_device_many_async.restype = C.c_int
     lib.sptrsv_solve_many.argtypes = [C.c_void_p, _PD, _PD, C.c_int32, C.POINTER(Stats)]
@@ -337,6 +339,13 @@ class NativePlan:
                                                       C.c_void_p(stream))
         raise_for_status(rc, _err(self._lib))
 
+    def last_counters(self) -> dict:
+        """Device counters of this plan's last finished solve."""
+        sp_, rr = np.zeros(1, dtype=np.int64), np.zeros(1, dtype=np.int64)
+        rc = self._lib.sptrsv_plan_last_counters(self._h, _ptr(sp_, C.c_int64), _ptr(rr, C.c_int64))
+        raise_for_status(rc, _err(self._lib))
+        return {"spins": int(sp_[0]), "remote_reads": int(rr[0])}
+
     def solve_device_async(self, d_b: int, d_x: int, stream: int = 0) -> None:
         rc = self._lib.sptrsv_solve_device_async(self._h, C.c_void_p(d_b), C.c_void_p(d_x), C.c_void_p(stream))
         raise_for_status(rc, _err(self._lib))
@@ -448,6 +457,7 @@ class PeGroup:
         d["executor"] = EXECUTOR_NAME.get(d["executor"], "?")
         d["pe_mode"] = self.mode
         d["devices"] = list(self.devices)
+        d["per_pe"] = [p.last_counters() for p in self.plans]  # measured, one plan per PE
         return x, d
 
     def close(self) -> None:

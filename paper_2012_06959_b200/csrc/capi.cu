@@ -529,6 +529,8 @@ int DevicePlan::finish(sptrsv_stats* st) {
   }
   pending = false;
   last_solve_ms = ms;
+  last_spins = (long long)hs.spins;
+  last_remote = (long long)hs.remote_reads;
   if (st) {
     st->setup_ms = setup_ms;
     st->solve_ms = ms;
@@ -749,6 +751,15 @@ int sptrsv_solve_device_async(sptrsv_plan* plan, const double* d_b, double* d_x,
   CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t s = stream ? reinterpret_cast<cudaStream_t>(stream) : p->stream;
   return p->solve_device(d_b, d_x, s);
+}
+
+int sptrsv_plan_last_counters(const sptrsv_plan* plan, int64_t* spins, int64_t* remote_reads) {
+  g_err.clear();
+  auto* p = reinterpret_cast<const DevicePlan*>(plan);
+  if (!p) return fail(SPTRSV_E_ARGUMENT, "null plan");
+  if (spins) *spins = p->last_spins;
+  if (remote_reads) *remote_reads = p->last_remote;
+  return SPTRSV_OK;
 }
 
 int sptrsv_synchronize(sptrsv_plan* plan, sptrsv_stats* stats) {

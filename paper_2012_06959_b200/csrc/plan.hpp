@@ -184,6 +184,7 @@ struct DevicePlan {
   int stencil_sync_peers();
   int solve_device(const double* d_b, double* d_x, cudaStream_t s);
   int finish(sptrsv_stats* st);
+  long long last_spins = 0, last_remote = 0;  // of the last finished solve (sptrsv_plan_last_counters)
   void release();
 };
 

@@ -219,14 +219,24 @@ def _per_pe_stats(l: CscMatrix, plan: PartitionPlan, cfg: SolverConfig, dev: dic
         per_row_skip = (P - 1) - touched
         skipped = np.bincount(plan.owner_arr, weights=per_row_skip, minlength=P).astype(np.int64)
     spins = int(dev.get("spins", 0))
+    # one plan per PE (PeGroup): each PE's kernel counted its own polls and
+    # cross-PE dependency loads; otherwise one kernel served every PE and its
+    # polls are reported on PE 0
+    measured = dev.get("per_pe")
+    if measured is not None and len(measured) == P:
+        pe_spins = [int(m["spins"]) for m in measured]
+        pe_remote = [int(m["remote_reads"]) for m in measured]
+    else:
+        pe_spins = [spins if p == 0 else 0 for p in range(P)]
+        pe_remote = [int(v) for v in rem_reads]
     out = []
     for p in range(P):
         out.append(
             PeStats(
                 pe=p,
                 components_solved=int(solved[p]),
-                lock_wait_spins=spins if p == 0 else 0,
-                remote_reads_issued=int(rem_reads[p]),
+                lock_wait_spins=pe_spins[p],
+                remote_reads_issued=pe_remote[p],
                 remote_reads_skipped=int(skipped[p]),
                 local_updates=int(loc[p]),
                 remote_updates=int(rem[p]),

@@ -208,3 +208,25 @@ def test_stencil_partition_falls_back_when_bands_split():
     plan.set_partition(owner, 2, 0)
     assert plan.info()["executor"] == "rows"
     plan.close()
+
+
+def test_per_pe_counters_are_measured_by_each_pes_kernel():
+    """With one plan per PE (PeGroup), SolveReport.per_pe carries each PE
+    kernel's own counters (sptrsv_plan_last_counters): remote_reads_issued is
+    the number of cross-PE dependency loads the kernel issued -- one per
+    entry (i, j) with owner(i) = p != owner(j) -- and lock_wait_spins its own
+    polls, no longer all booked to PE 0 (reference PeStats, engine.py:100-111)."""
+    l = synth.rmat(12, 8, 5)
+    b = np.random.default_rng(1).uniform(-1, 1, l.n)
+    part = sp.task_round_robin_partition(l.n, 3, 4)
+    cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=3, precision="exact", executor="rows")
+    x, rep = sp.solve(l, b, part, cfg)
+    assert x.tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b).tobytes()
+    cols = l.entry_columns()
+    off = l.row_idx != cols
+    own = part.owner_arr
+    rows, cols = l.row_idx[off], cols[off]
+    cross = own[rows] != own[cols]
+    expect = np.bincount(own[rows][cross], minlength=3)
+    assert [s.remote_reads_issued for s in rep.per_pe] == expect.tolist()
+    assert sum(s.lock_wait_spins for s in rep.per_pe) >= 0
