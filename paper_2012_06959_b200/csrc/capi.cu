@@ -378,7 +378,13 @@ constexpr unsigned kWaitGeq = 0;  // CU_STREAM_WAIT_VALUE_GEQ
 }  // namespace
 
 bool DevicePlan::streamed_io_ok() const {
-  return executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !stencil.part &&
+  // a CUDA tool attached through the injection interface (Nsight Compute,
+  // compute-sanitizer) serialises kernels and copies: the kernel would wait
+  // for b flags that only a concurrent copy stream writes (until the watchdog)
+  static const bool tool = std::getenv("CUDA_INJECTION64_PATH") != nullptr ||
+                           std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||   // ncu
+                           std::getenv("NV_SANITIZER_INJECTION_TRANSPORT_TYPE") != nullptr;  // compute-sanitizer
+  return !tool && executor_used == SPTRSV_EXECUTOR_STENCIL && !seg_table && !stencil.part &&
          !(opt.flags & SPTRSV_PLAN_NO_STREAMED_IO) &&
          (stencil3.ready ? stencil3.bflag != nullptr : stencil.bflag != nullptr) && stream_memops();
 }
