@@ -1,5 +1,5 @@
 mkdir -p gpurun_out; rm -f gpurun_out/g18.txt
-for v in "" cl2 cl4 cl8; do
+for v in "" pp0; do
   if [ -n "$v" ]; then export SPTRSV_LIB=$PWD/paper_2012_06959_b200/libsptrsv_b200_$v.so; else unset SPTRSV_LIB; fi
   timeout 120 python tools/variant_bench.py >> gpurun_out/g18.txt 2>&1
   timeout 120 python tools/stencil_timeline.py fast >> gpurun_out/g18.txt 2>&1
