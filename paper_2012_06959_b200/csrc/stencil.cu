@@ -92,24 +92,6 @@ static_assert(kStStoreDepth >= 0 && kStStoreDepth <= kStOutSlots - 1, "in-flight
 #endif
 constexpr int kStCluster = SPTRSV_ST_CLUSTER;
 
-// Fast mode without the lane-0 select (SPTRSV_ST_NOSEL, default on): lane 0's
-// row above is the band above's bottom row, every other lane's comes from its
-// neighbour by __shfl_up_sync. A per-step select between the two sat on the
-// recurrence (SHFL -> FSEL -> DFMA, +16 cycles of a 72-cycle step in
-// tools/microbench/chain.cu). Instead the packer stores lane 0's top-row
-// coefficient as 0 and the poller folds the band above's value into that
-// row's b in the staged ring, b - L[i,i-nx] x[i-nx], before it hands the chunk
-// over; the compute warp then treats every lane alike (lane 0 multiplies its
-// own shuffled bottom row by 0). Re-associates the top-row sum (fast mode's
-// 1e-12 contract); a non-finite x in lane 0's own bottom row turns into NaN
-// instead of +-inf in the (already non-finite) solution.
-#ifndef SPTRSV_ST_NOSEL
-#define SPTRSV_ST_NOSEL 0
-#endif
-#ifndef SPTRSV_ST_NOSEL_ABL  // timing diagnostics only: 1 = no fold into b, 2 = no wait for the staged b
-#define SPTRSV_ST_NOSEL_ABL 0
-#endif
-constexpr bool kStNoSel = SPTRSV_ST_NOSEL && kStCluster == 1 && kStR == 2 && kStC == 2;
 // chunk counters released before the band-below publish (see step())
 #ifndef SPTRSV_ST_REL_FIRST
 #define SPTRSV_ST_REL_FIRST 1
@@ -178,13 +160,27 @@ struct alignas(64) StArgs {
   int b_tma_bands;  // bands [0, b_tma_bands) gather b with one TMA per chunk (0: cp.async everywhere)
   int x_tma_bands;  // bands [0, x_tma_bands) store interior chunks of x with one TMA store
   unsigned long long* mbox_next;  // the other mailbox half: the storer resets each band's row for the next solve
-  const double* upc;              // fast mode, kStNoSel: -L[i,i-nx] of every band's top grid row ([n_tasks][nx])
   int debug;                      // SPTRSV_PLAN_DEBUG: every mailbox word is written once, over its sentinel
   // several right-hand sides in one launch (solve_many): b and x are k
   // stacked [ny][nx] grids, i.e. one grid of k * ny rows whose tasks t are
   // band t % bands of right-hand side t / bands -- every copy reads the same
   // coefficient stream, and the first band of a copy has no band above
   int bands;
+  // fast mode, pre-scaled right-hand side (BD kernels): the first prep_tasks
+  // tickets go to prep tasks that write bd = b * (1/d) for every band in band
+  // order (bd_done[t] counts the prep tasks through band t; the last one
+  // raises bdflag[t] = bd_epoch); the loaders stream bd instead of b and only
+  // the wu / wl fields of the coefficient stream, and the compute warp's
+  // element is two FMAs (the rd field's loads and multiply leave the
+  // critical step). b_in is the caller's b (also the host-copy flags' b).
+  int prep_tasks;
+  const double* b_in;
+  double* bd;
+  const double* rdg;
+  unsigned* bdflag;
+  int* bd_done;
+  unsigned bd_epoch;
+  long long n_copy;  // elements of one right-hand side (rd index = i % n_copy)
 };
 // task t has a band below it in the same right-hand side
 __device__ __forceinline__ bool st_has_below(const StArgs& a, int t) {
@@ -261,7 +257,8 @@ __device__ __noinline__ unsigned long long st_poll(const unsigned long long* p, 
 enum {
   kCtlTask = 0, kCtlInReady = 1, kCtlInDone = 2, kCtlOutReady = 3, kCtlOutDone = 4, kCtlAbort = 5, kCtlMbReady = 6,
   kCtlGroup = 7,  // cluster rank 0: the group ticket of the current task
-  kCtlPubDone = 8  // chunks whose band-below row the publisher warp has read out of the out ring
+  kCtlPubDone = 8,  // chunks whose band-below row the publisher warp has read out of the out ring
+  kCtlPrep = 9      // BD kernels: this CTA's prep task (-1: a band or nothing)
 };
 
 template <bool EXACT>
@@ -328,7 +325,7 @@ __device__ __forceinline__ void abort_task(const StArgs& a, int* ctl, int lane) 
 }
 
 // One lane's inputs of one step, loaded a step ahead into registers.
-template <bool EXACT>
+template <bool EXACT, bool BD = false>
 struct StBlk {
   double wu[kStBlock], wl[kStBlock], rd[kStBlock], dd[kStBlock], bv[kStBlock];
   double inbox[kStC];
@@ -348,7 +345,7 @@ struct StBlk {
         const double2 r = cs[(3 * kStBlkPairs + p) * kStLanes + lane];
         dd[2 * p] = d.x, dd[2 * p + 1] = d.y;
         rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
-      } else {
+      } else if (!BD) {
         const double2 r = cs[(2 * kStBlkPairs + p) * kStLanes + lane];
         rd[2 * p] = r.x, rd[2 * p + 1] = r.y;
       }
@@ -362,16 +359,22 @@ struct StBlk {
         bv[r * kStC + c] = v.x, bv[r * kStC + c + 1] = v.y;
       }
     }
-    if (EXACT || !kStNoSel) {
-      const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (islot * kStG + k) * kStC;
+    const double* ib = reinterpret_cast<const double*>(smem + S::kInbox) + (islot * kStG + k) * kStC;
 #pragma unroll
-      for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
-    }
+    for (int c = 0; c < kStC; ++c) inbox[c] = ib[c];
   }
 };
 
 // ---- warp 1: stream coefficients and b, poll the band above -----------------
-template <bool EXACT, bool DG>
+// the host-copy flag that covers band t's b: the copy stream flags the last
+// band of each chunk of 1, 2, 4, ... bands (b_chunk_max > 0), else every band
+__device__ __forceinline__ int st_b_flag_band(const StArgs& a, int t) {
+  if (a.b_chunk_max <= 0) return t;
+  for (int t0b = 0, w = 1;; t0b += w, w = min(2 * w, a.b_chunk_max))
+    if (t < t0b + w) return min(a.n_tasks, t0b + w) - 1;
+}
+
+template <bool EXACT, bool DG, bool BD = false>
 __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned& phase_bits,
                        unsigned long long deadline) {
   using S = StSmem<EXACT>;
@@ -394,8 +397,19 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     const int j0 = c * kStG - lane;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(&bars[slot], S::kCoefChunk + (b_tma ? S::kBChunk : 0));
-      bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk, &bars[slot]);
+      if (BD) {
+        // the wu and wl fields of every step (the rd field stays behind)
+        constexpr int kFields2 = 2 * kStBlkPairs * kStLanes * 16;
+        mbar_expect_tx(&bars[slot], kStG * kFields2 + (b_tma ? S::kBChunk : 0));
+#pragma unroll
+        for (int k = 0; k < kStG; ++k)
+          bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk + k * S::kStep,
+                   tstream + (size_t)c * S::kCoefChunk + k * S::kStep, kFields2, &bars[slot]);
+      } else {
+        mbar_expect_tx(&bars[slot], S::kCoefChunk + (b_tma ? S::kBChunk : 0));
+        bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk,
+                 &bars[slot]);
+      }
       if (b_tma) tma_load_4d(smem + S::kB + slot * S::kBChunk, &a.bmap, c * kStG * kStC, 0, 0, t, &bars[slot]);
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk);
@@ -432,18 +446,25 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     phase_bits ^= 1u << slot;
     return true;
   };
-  // overlapped host solve: this band's b may still be on its way over PCIe
-  if (a.bflag) {
+  // BD: this band's bd is written by the prep tasks (which themselves wait
+  // for the host copies of b)
+  if (BD) {
     int polls = 0;
-    // the copy stream flags the last band of each chunk (1, 2, 4, ... bands)
-    int flag_band = t;
-    if (a.b_chunk_max > 0) {
-      for (int t0b = 0, w = 1;; t0b += w, w = min(2 * w, a.b_chunk_max))
-        if (t < t0b + w) {
-          flag_band = min(a.n_tasks, t0b + w) - 1;
-          break;
-        }
+    while ((int)(ld_acquire_gpu_u32(a.bdflag + t) - a.bd_epoch) < 0) {
+      if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
+      if (!__all_sync(0xffffffffu, ok)) {
+        abort_task(a, ctl, lane);
+        return;
+      }
+      __nanosleep(64);
     }
+    // generic-proxy stores of other SMs -> this SM's TMA reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  // overlapped host solve: this band's b may still be on its way over PCIe
+  if (a.bflag && !BD) {
+    int polls = 0;
+    const int flag_band = st_b_flag_band(a, t);
     while ((int)(ld_acquire_sys_u32(a.bflag + flag_band) - a.epoch) < 0) {
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
       if (!__all_sync(0xffffffffu, ok)) {
@@ -519,65 +540,6 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
   const int k = lane / kStC, q = lane % kStC;
   unsigned long long spins = 0;
-  if constexpr (!EXACT && kStNoSel) {
-    // lane (k, q): column j*C + q of the band above's bottom row, folded into
-    // lane 0's top-row b of step k once the loader staged the chunk
-    const double* upc = a.upc + (size_t)t * a.nx;
-    // the factors stream from HBM kPre chunks ahead (a load per chunk in line
-    // with the poll would cost the poller a DRAM round trip per chunk)
-    constexpr int kPre = 4;
-    auto fac = [&](int cc) {
-      const int jj = cc * kStG + k;
-      return (lane < kStG * kStC && jj < nblk) ? __ldg(upc + jj * kStC + q) : 0.0;
-    };
-    double wq[kPre];
-#pragma unroll
-    for (int p = 0; p < kPre; ++p) wq[p] = fac(p);
-    // chunk c with its factor in `wf` (loaded kPre chunks earlier), which then
-    // receives chunk c + kPre's; the loop is unrolled kPre times so the
-    // factor registers never move (a move would wait for the load in flight)
-    auto one = [&](int c, double& wf) -> bool {
-      bool ok = true;
-      const int j = c * kStG + k;
-      const bool mine = lane < kStG * kStC && j < nblk;
-      unsigned long long u = 0;
-      if (mine) {
-        // spin inline first (a call would wait for the factor loads in flight)
-        const unsigned long long* src = above + j * kStC + q;
-        u = remote ? ld_relaxed_sys_u64(src) : ld_relaxed_u64(src);
-        for (int polls = 0; u == kStNotReady && polls < 256; ++polls) {
-          u = remote ? ld_relaxed_sys_u64(src) : ld_relaxed_u64(src);
-          ++spins;
-        }
-        if (u == kStNotReady)
-          u = st_poll(src, a.abort_flag, a.status, a.spin_initial, a.spin_max_ns, deadline, remote, spins);
-        if (u == kStNotReady) ok = false;
-      }
-      if (!(SPTRSV_ST_NOSEL_ABL & 2) && ok && !wait_ctl(ctl, kCtlInReady, c + 1, deadline, a.nap)) ok = false;
-      if (!__all_sync(0xffffffffu, ok)) return false;
-      if (mine && !(SPTRSV_ST_NOSEL_ABL & 1)) {
-        double* e = reinterpret_cast<double*>(smem + S::kB + (c % S::kSlots) * S::kBChunk) +
-                    2 * st_b_piece(0, 0, k, q / 2) + (q & 1);
-        *e = __fma_rn(wf, __longlong_as_double((long long)u), *e);
-      }
-      __syncwarp();
-      if (lane == 0) st_release_cta(ctl + kCtlMbReady, c + 1);
-      // after the release: its MEMBAR.CTA would wait for this DRAM load
-      wf = fac(c + kPre);
-      lag_stamp<DG>(a, t, c, lane, 1);
-      return true;
-    };
-    for (int c0 = 0; c0 < nchunks; c0 += kPre) {
-#pragma unroll
-      for (int u = 0; u < kPre; ++u)
-        if (c0 + u < nchunks && !one(c0 + u, wq[u])) return abort_task(a, ctl, lane);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) spins += __shfl_xor_sync(0xffffffffu, spins, off);
-    if (lane == 0 && spins) atomicAdd(&a.status->spins, spins);
-    if (remote && lane == 0) atomicAdd(&a.status->remote_reads, (unsigned long long)a.nx);
-    return;
-  }
   for (int c = 0; c < nchunks; ++c) {
     // inbox slot c % kStInbox is free once the compute warp finished chunk c - kStInbox
     if (c >= kStInbox && !wait_ctl(ctl, kCtlInDone, c - kStInbox + 1, deadline, a.nap))
@@ -849,8 +811,8 @@ constexpr bool kStChunkPub = SPTRSV_ST_CHUNK_PUB;
 static_assert(kStChunkPub || kStCluster == 1, "cluster hand-overs push whole chunks");
 constexpr bool kStEarlyShfl = SPTRSV_ST_EARLY_SHFL;
 
-template <bool EXACT>
-__device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double (&up)[kStC],
+template <bool EXACT, bool BD>
+__device__ __forceinline__ void expand_block(const StBlk<EXACT, BD>& b, const double (&up)[kStC],
                                              const double (&left)[kStR], double (&x)[kStR][kStC]) {
   if constexpr (kStR == 2 && kStC == 2) {
     const double *wu = b.wu, *wl = b.wl;
@@ -876,7 +838,7 @@ __device__ __forceinline__ void expand_block(const StBlk<EXACT>& b, const double
 // ABL: compile-time ablations for timing experiments only (0 in production):
 // 1 = no output staging, 2 = no next-step loads, 4 = no shuffle, 8 = no
 // active/publish branch
-template <bool EXACT, int ABL, bool PART, bool DG>
+template <bool EXACT, int ABL, bool PART, bool DG, bool BD = false>
 __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, int lane, unsigned long long deadline,
                         unsigned crank, bool below_in_cluster, bool above_in_cluster) {
   using S = StSmem<EXACT>;
@@ -926,7 +888,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 
   // One 2 x C block. exact: Markstein division with its operand-range guards
   // folded into the returned flag (ieee: IEEE division); fast: pre-scaled FMAs.
-  auto block = [&](const StBlk<EXACT>& blk, const double (&top)[kStC], double (&xb)[kStR][kStC],
+  auto block = [&](const StBlk<EXACT, BD>& blk, const double (&top)[kStC], double (&xb)[kStR][kStC],
                    bool ieee) -> bool {
     bool bad = false;
 #pragma unroll
@@ -958,9 +920,9 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
         } else if (q == 0) {
           // left comes from the previous step (early): the late operand
           // (up, possibly straight off the shuffle) goes in the outer FMA
-          xb[r][q] = __fma_rn(blk.wu[e], up, __fma_rn(blk.wl[e], left, __dmul_rn(blk.bv[e], blk.rd[e])));
+          xb[r][q] = __fma_rn(blk.wu[e], up, __fma_rn(blk.wl[e], left, BD ? blk.bv[e] : __dmul_rn(blk.bv[e], blk.rd[e])));
         } else {
-          xb[r][q] = __fma_rn(blk.wl[e], left, __fma_rn(blk.wu[e], up, __dmul_rn(blk.bv[e], blk.rd[e])));
+          xb[r][q] = __fma_rn(blk.wl[e], left, __fma_rn(blk.wu[e], up, BD ? blk.bv[e] : __dmul_rn(blk.bv[e], blk.rd[e])));
         }
       }
     }
@@ -1012,7 +974,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
     for (int q = 0; q < kStC; ++q) bottom[q] = sv_bottom[q], upv[q] = sv_upv[q];
 #pragma unroll 1
     for (int k = 0; k < kStG; ++k) {
-      StBlk<EXACT> blk;
+      StBlk<EXACT, BD> blk;
       blk.load(smem, c % NB, c % kStInbox, k, lane);
       double top[kStC], xb[kStR][kStC];
 #pragma unroll
@@ -1031,7 +993,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   // step k of chunk c computes from `cur` (loaded two steps earlier) and
   // loads step k + 2 into `nxt2`: a full step of slack hides the shared-memory
   // latency that a one-step lookahead leaves exposed
-  auto step = [&](int c, int k, const StBlk<EXACT>& cur, StBlk<EXACT>& nxt2) -> bool {
+  auto step = [&](int c, int k, const StBlk<EXACT, BD>& cur, StBlk<EXACT, BD>& nxt2) -> bool {
     auto load_ahead = [&]() {
       if (k + 2 < kStG) {
         if (!(ABL & 2)) nxt2.load(smem, c % NB, c % kStInbox, k + 2, lane);
@@ -1056,7 +1018,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
 #pragma unroll
     for (int q = 0; q < kStC; ++q) {
       const double up = kStEarlyShfl ? upv[q] : (ABL & 4) ? bottom[q] : __shfl_up_sync(0xffffffffu, bottom[q], 1);
-      top[q] = (!EXACT && kStNoSel) ? up : lane == 0 ? cur.inbox[q] : up;
+      top[q] = lane == 0 ? cur.inbox[q] : up;
     }
     double xb[kStR][kStC];
     if (kStExpand && !EXACT) {
@@ -1128,7 +1090,7 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   // diagnostics: per-task globaltimer stamps (start, first chunk ready, end)
   long long* tstamp = (DG && a.dbg && lane == 0 && t < 1024) ? a.dbg + 6 * kStProbeChunks + 3 * t : nullptr;
   if (tstamp) tstamp[0] = (long long)globaltimer_ns();
-  StBlk<EXACT> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
+  StBlk<EXACT, BD> buf[3];  // step s uses buf[s % 3] (indices static after unrolling)
   if (!solo && !wait_ctl(ctl, kCtlInReady, 1, deadline)) return abort_task(a, ctl, lane);
   if (above_in_cluster && lane == 0)
     for (int cc = 0; cc < kStInbox; ++cc) arm_inbox(cc);  // first phase of every slot
@@ -1152,7 +1114,86 @@ __device__ void compute(const StArgs& a, unsigned char* smem, int* ctl, int t, i
   if (tstamp) tstamp[2] = (long long)globaltimer_ns();
 }
 
-template <bool EXACT, int ABL, bool PART, int CL, bool DG>
+// ---- prep tasks (BD kernels): bd = b * (1/d), band by band ------------------
+// Prep task p of P takes every P-th double pair of each band, bands in order,
+// so every band's bd is written by all prep CTAs at once (band 0 in ~2 us)
+// and the wavefront (a band every ~5.7 us) never catches up. After its share
+// of band t a CTA counts itself in bd_done[t]; the last one raises
+// bdflag[t]. Prep tasks wait on nothing but the host copies of b (streamed
+// host solves), so handing them out before any band keeps the pool
+// deadlock-free.
+__device__ void prep_task(const StArgs& a, int p, unsigned long long deadline) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const long long stride = (long long)a.prep_tasks * nthr;
+  // (BD kernels solve one right-hand side: rd index = element index)
+  const double* __restrict__ bin = a.b_in;
+  const double* __restrict__ rdg = a.rdg;
+  double* __restrict__ bd = a.bd;
+  const bool pairs = ((reinterpret_cast<uintptr_t>(bin) & 15) == 0) && (a.nx % 2 == 0);
+  constexpr int kU = 8;  // loads in flight per thread (a loop of dependent load/store pairs paid a DRAM
+                         // round trip per pair: ~7.6 us per band, slower than the wavefront)
+  for (int t = 0; t < a.n_tasks; ++t) {
+    if (a.bflag) {  // streamed host solve: band t's b may still be on its way
+      __shared__ int ok_s;
+      if (tid == 0) {
+        const int fb = st_b_flag_band(a, t);
+        int polls = 0, ok = 1;
+        while ((int)(ld_acquire_sys_u32(a.bflag + fb) - a.epoch) < 0) {
+          if ((++polls & 255) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag))) {
+            ok = 0;
+            break;
+          }
+          __nanosleep(256);
+        }
+        ok_s = ok;
+      }
+      __syncthreads();
+      if (!ok_s) return;
+    }
+    const long long e0 = (long long)t * kStBand * a.nx, e1 = min((long long)(t + 1) * kStBand, (long long)a.ny) * a.nx;
+    if (pairs) {
+      const double2* b2 = reinterpret_cast<const double2*>(bin);
+      const double2* r2 = reinterpret_cast<const double2*>(rdg);
+      double2* d2 = reinterpret_cast<double2*>(bd);
+      for (long long base = e0 / 2 + (long long)p * nthr + tid; base < e1 / 2; base += kU * stride) {
+        double2 bv[kU], rv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const long long e = base + u * stride;
+          if (e < e1 / 2) bv[u] = __ldg(b2 + e), rv[u] = __ldg(r2 + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const long long e = base + u * stride;
+          if (e < e1 / 2) d2[e] = make_double2(__dmul_rn(bv[u].x, rv[u].x), __dmul_rn(bv[u].y, rv[u].y));
+        }
+      }
+    } else {
+      for (long long base = e0 + (long long)p * nthr + tid; base < e1; base += kU * stride) {
+        double bv[kU], rv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const long long e = base + u * stride;
+          if (e < e1) bv[u] = bin[e], rv[u] = __ldg(rdg + e);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const long long e = base + u * stride;
+          if (e < e1) bd[e] = __dmul_rn(bv[u], rv[u]);
+        }
+      }
+    }
+    // the CTA's stores of band t, then one fence + count by thread 0 (the
+    // other threads go on with band t + 1)
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(a.bd_done + t, 1) == a.prep_tasks - 1) st_release_gpu_u32(a.bdflag + t, a.bd_epoch);
+    }
+  }
+}
+
+template <bool EXACT, int ABL, bool PART, int CL, bool DG, bool BD = false>
 __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_constant__ StArgs a) {
   using S = StSmem<EXACT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1200,21 +1241,36 @@ __global__ void __launch_bounds__(kStThreads, 1) k_stencil2d(const __grid_consta
         ctl[kCtlTask] = g >= n_groups ? -1 : min(g * CL + (int)crank, a.n_tasks);  // n_tasks: idle this round
       }
     } else if (threadIdx.x == 0) {
-      const int k = atomicAdd(a.ticket, 1);  // ascending: the progress rule (engine.py:30-35)
-      ctl[kCtlTask] = k >= a.n_my_tasks ? -1 : (a.my_tasks ? a.my_tasks[k] : k);
+      // ascending tickets: the progress rule (engine.py:30-35); BD kernels hand
+      // out their prep tasks first (they wait on nothing the bands produce)
+      const int k = atomicAdd(a.ticket, 1);
+#if SPTRSV_ST_BD_BANDS_FIRST  // placement experiment only (not deadlock-safe without co-residency)
+      const int kb = k;
+      ctl[kCtlPrep] = (BD && k >= a.n_my_tasks && k < a.n_my_tasks + a.prep_tasks) ? k - a.n_my_tasks : -1;
+      ctl[kCtlTask] = kb >= a.n_my_tasks ? -1 : (a.my_tasks ? a.my_tasks[kb] : kb);
+#else
+      const int kb = BD ? k - a.prep_tasks : k;
+      ctl[kCtlPrep] = (BD && k < a.prep_tasks) ? k : -1;
+      ctl[kCtlTask] = kb >= a.n_my_tasks ? -1 : kb < 0 ? a.n_tasks : (a.my_tasks ? a.my_tasks[kb] : kb);
+#endif
       ctl[kCtlInReady] = ctl[kCtlInDone] = ctl[kCtlOutReady] = ctl[kCtlOutDone] = ctl[kCtlAbort] = 0;
       ctl[kCtlMbReady] = ctl[kCtlPubDone] = 0;
       init_out_bars();
     }
     __syncthreads();
+    if (BD && CL == 1 && ctl[kCtlPrep] >= 0) {
+      prep_task(a, ctl[kCtlPrep], deadline);
+      __syncthreads();
+      continue;
+    }
     const int t = ctl[kCtlTask];
     if (t < 0) break;
     if (t < a.n_tasks) {
       const bool below_in_cluster = CL > 1 && crank + 1 < (unsigned)CL && st_has_below(a, t);
       if (warp == 0)
-        compute<EXACT, ABL, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
+        compute<EXACT, ABL, PART, DG, BD>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster, CL > 1 && crank > 0);
       else if (a.probe & 32) {  // diagnostics: the compute warp alone, on stale shared memory
-      } else if (warp == 1) loader<EXACT, DG>(a, smem, ctl, t, lane, phase_bits, deadline);
+      } else if (warp == 1) loader<EXACT, DG, BD>(a, smem, ctl, t, lane, phase_bits, deadline);
       else if (warp == 2) storer<EXACT, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
       else if (warp == 4) publisher<EXACT, PART, DG>(a, smem, ctl, t, lane, deadline, crank, below_in_cluster);
       else poller<EXACT, DG>(a, smem, ctl, t, lane, deadline, CL > 1 && crank > 0);
@@ -1251,13 +1307,14 @@ int max_active_clusters(K kernel, int cl, int smem_bytes) {
   return n;
 }
 
-template <bool EXACT, int ABL, bool PART = false, int CL = 1, bool DG = false>
+template <bool EXACT, int ABL, bool PART = false, int CL = 1, bool DG = false, bool BD = false>
 cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART, CL, DG>, StSmem<EXACT>::kTotal, attr); e != cudaSuccess)
+  if (cudaError_t e = set_max_dyn_smem(k_stencil2d<EXACT, ABL, PART, CL, DG, BD>, StSmem<EXACT>::kTotal, attr);
+      e != cudaSuccess)
     return e;
   if (CL == 1) {
-    k_stencil2d<EXACT, ABL, PART, CL, DG><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
+    k_stencil2d<EXACT, ABL, PART, CL, DG, BD><<<blocks, kStThreads, StSmem<EXACT>::kTotal, s>>>(a);
     return cudaGetLastError();
   }
   const int groups = (a.n_tasks + CL - 1) / CL;
@@ -1292,6 +1349,10 @@ cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
       case 15: return launch_stencil_v<EXACT, 15>(a, blocks, s);
       default: break;
     }
+  }
+  if (!EXACT && a.prep_tasks > 0) {  // pre-scaled right-hand side (BD)
+    if (a.dbg) return launch_stencil_v<EXACT, 0, false, 1, true, true>(a, blocks, s);
+    return launch_stencil_v<EXACT, 0, false, 1, false, true>(a, blocks, s);
   }
   // probe bit 16: the diagnostics build of the kernel (clock / globaltimer stamps)
   if (a.dbg) {
@@ -1332,8 +1393,7 @@ __global__ void k_st_pack(const int* __restrict__ rp, const double* __restrict__
         if (j >= 0 && j < nblk && y < ny) {
           const long long i = y * nx + (long long)j * kStC + c;
           int kk = rp[i];
-          double fu = y > 0 ? val[kk++] : 0.0;
-          if (!exact && kStNoSel && l == 0 && r == 0) fu = 0.0;  // folded into b by the poller
+          const double fu = y > 0 ? val[kk++] : 0.0;
           const double fl = (j * kStC + c) > 0 ? val[kk] : 0.0;
           f[0] = fu, f[1] = fl;
           if (exact) f[2] = dg[i], f[3] = rdg[i];
@@ -1342,19 +1402,6 @@ __global__ void k_st_pack(const int* __restrict__ rp, const double* __restrict__
         for (int fld = 0; fld < NF; ++fld) stepbuf[((fld * pairs + k) * kStLanes + l) * 2 + half] = f[fld];
       }
     }
-  }
-}
-
-// -L[i, i-nx] of every band's top grid row (fast mode, kStNoSel): the
-// poller's factor for the band above's value. Band 0 has no row above (0).
-__global__ void k_st_upc(const int* __restrict__ rp, const double* __restrict__ cv, int nx, int ny, int n_tasks,
-                         double* __restrict__ upc) {
-  const long long items = (long long)n_tasks * nx;
-  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
-       it += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(it / nx), x = (int)(it % nx);
-    const long long y = (long long)t * kStBand;
-    upc[it] = (t > 0 && y < ny) ? -cv[rp[y * nx + x]] : 0.0;
   }
 }
 
@@ -1475,13 +1522,6 @@ int DevicePlan::build_stencil(const std::vector<int>& h_rp, const std::vector<in
     const int grid = (int)std::min<long long>((items + 255) / 256, 148 * 64);
     k_st_pack<<<grid, 256, 0, stream>>>(rp, exact ? cv : wv, dg, rdg, nx, stencil.ny, stencil.n_tasks,
                                         stencil.steps_per_task, exact ? 1 : 0, stencil.stream);
-    if (!exact && kStNoSel) {
-      if ((e = al((void**)&stencil.upc, sizeof(double) * (size_t)stencil.n_tasks * nx)) != cudaSuccess)
-        return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-      const long long m = (long long)stencil.n_tasks * nx;
-      k_st_upc<<<(int)std::min<long long>((m + 255) / 256, 148 * 16), 256, 0, stream>>>(rp, cv, nx, stencil.ny,
-                                                                                        stencil.n_tasks, stencil.upc);
-    }
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
@@ -1547,7 +1587,6 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   StArgs a{};
   a.stream = stencil.stream;
-  a.upc = stencil.upc;
   a.debug = (opt.flags & SPTRSV_PLAN_DEBUG) != 0;
   a.mbox = mbox + par * half;
   a.mbox_next = mbox + (1 - par) * half;
@@ -1561,6 +1600,31 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     a.pe_mbox = stencil.pe_mbox;
     a.band_owner = stencil.band_owner;
     a.my_pe = stencil.my_pe;
+  }
+  // fast mode, one right-hand side, one PE: the BD kernel (its prep tasks
+  // write bd = b * (1/d) on the SMs the 64 bands leave idle; SPTRSV_NO_BD=1
+  // keeps the multiply in the step, diagnostics)
+  static const bool no_bd = std::getenv("SPTRSV_NO_BD") != nullptr;
+  const bool bd_mode = !stencil.exact && !many && !stencil.part && kStCluster == 1 && !no_bd;
+  if (bd_mode) {
+    if (!stencil.bd) {
+      if ((e = cudaMalloc((void**)&stencil.bd, sizeof(double) * (size_t)n)) != cudaSuccess ||
+          (e = cudaMalloc((void**)&stencil.bdflag, sizeof(unsigned) * stencil.n_tasks)) != cudaSuccess ||
+          (e = cudaMalloc((void**)&stencil.bd_done, sizeof(int) * stencil.n_tasks)) != cudaSuccess ||
+          (e = cudaMemsetAsync(stencil.bdflag, 0, sizeof(unsigned) * stencil.n_tasks, s)) != cudaSuccess)
+        return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    }
+    if ((e = cudaMemsetAsync(stencil.bd_done, 0, sizeof(int) * stencil.n_tasks, s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    a.b_in = d_b;
+    a.bd = stencil.bd;
+    a.rdg = rdg;
+    a.bdflag = stencil.bdflag;
+    a.bd_done = stencil.bd_done;
+    a.bd_epoch = ++stencil.bd_epoch;
+    if (a.bd_epoch == 0) a.bd_epoch = ++stencil.bd_epoch;  // (0 is the flags' initial value)
+    a.n_copy = n;
+    d_b = stencil.bd;  // the loaders stream bd (aligned) instead of b
   }
   a.b = d_b;
   a.x = d_x;
@@ -1590,7 +1654,13 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
     a.dbg = probe_buf;
   }
-  const int blocks = std::max(1, std::min(a.n_my_tasks, grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms));
+  int blocks = std::max(1, std::min(a.n_my_tasks, grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms));
+  if (bd_mode) {
+    // the SMs the bands leave idle do the prep (at least 16 prep tasks)
+    const int sms = grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms;
+    a.prep_tasks = std::max(16, sms - std::min(a.n_my_tasks, sms));
+    blocks = std::min(a.n_my_tasks + a.prep_tasks, std::max(sms, a.prep_tasks + 1));
+  }
   ++(many ? stencil.many_solves : stencil.solves);
   if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);

@@ -58,10 +58,6 @@ struct StencilPlan {
   long long stream_bytes = 0;
   double build_ms = 0.0;
   unsigned char* stream = nullptr;     // [task][step][field][pair][lane] 16-byte pairs
-  // fast mode without the lane-0 select (stencil.cu kStNoSel): -L[i, i-nx] of
-  // every band's top grid row, [n_tasks][nx]; the poller folds the band
-  // above's value into that row's b (b - L[i,i-nx] x[i-nx])
-  double* upc = nullptr;
   unsigned long long* mbox = nullptr;  // [n_tasks][nx] bottom grid row of each task (value-is-flag)
   // streamed host solves (sptrsv_solve): per-band b-arrived flags written by
   // the copy stream, per-band x-stored flags written by the kernel; both
@@ -80,6 +76,12 @@ struct StencilPlan {
   // several right-hand sides per launch (solve_many): mailboxes of k stacked
   // copies, [2][k * n_tasks][nx], grown on demand, with their own parity
   unsigned long long* mbox_many = nullptr;
+  // fast mode, one right-hand side: b * (1/d) written by the kernel's prep
+  // tasks (stencil.cu BD kernels) with per-band flags and prep counters
+  double* bd = nullptr;
+  unsigned* bdflag = nullptr;  // [n_tasks], compared with bd_epoch
+  int* bd_done = nullptr;      // [n_tasks], zeroed per solve
+  unsigned bd_epoch = 0;
   int many_k = 0;
   int many_last = 0;  // copies of the previous stacked solve (a different count re-arms every word)
   long long many_solves = 0;
@@ -113,13 +115,16 @@ struct StencilPlan {
   }
   void release() {
     release_part();
-    void* ptrs[] = {stream, mbox, bflag, xflag, upc, mbox_many};
+    void* ptrs[] = {stream, mbox, bflag, xflag, mbox_many, bd, bdflag, bd_done};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
-    upc = nullptr;
     mbox = nullptr;
     mbox_many = nullptr;
+    bd = nullptr;
+    bdflag = nullptr;
+    bd_done = nullptr;
+    bd_epoch = 0;
     many_k = 0;
     many_last = 0;
     many_solves = 0;

@@ -548,3 +548,26 @@ def test_solve_many_rows_executor():
     xs = sp.solve_many(l, bs, precision="exact", executor="rows")
     for c in range(4):
         assert xs[:, c].tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, bs[:, c].copy()).tobytes()
+
+
+@pytest.mark.parametrize("shape", [(128, 70), (256, 128)])
+def test_stencil_fast_unaligned_and_partial_bands(shape):
+    """Fast mode's pre-scaled right-hand side (the kernel's prep tasks write
+    b * (1/d) band by band): b only 8-byte aligned (scalar prep path), a
+    partial last band (70 rows), repeated solves (per-solve flag epochs)."""
+    torch = pytest.importorskip("torch")
+    l = _random_coefficients(synth.lap2d(*shape), 9)
+    plan = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision="fast", executor="stencil")
+    for rep in range(3):
+        b = np.random.default_rng(rep).uniform(-1, 1, l.n)
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        db = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+        db[1:] = torch.from_numpy(b).cuda()
+        dx = torch.zeros(l.n + 1, dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        plan.solve_device_async(db[1:].data_ptr(), dx[1:].data_ptr(), torch.cuda.current_stream().cuda_stream)
+        plan.synchronize()
+        assert sp.compare_solutions(dx[1:].cpu().numpy(), ref, FAST_TOL).within_tol
+        x, _ = plan.solve(b)  # host buffers (pageable: copy, solve, copy)
+        assert sp.compare_solutions(x, ref, FAST_TOL).within_tol
+    plan.close()
