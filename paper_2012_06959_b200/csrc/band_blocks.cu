@@ -37,9 +37,41 @@ namespace {
 
 constexpr int kW = 64;           // bandwidth = window
 constexpr int kBBWarps = 4;      // sweep warps per CTA (one block each)
-constexpr int kPf = 16;          // coefficient prefetch distance (columns)
-constexpr int kTSlots = 4;       // K2 ring depth (steps)
+// the sweeps read the packed band (SPTRSV_BB_PACKED=1: the stored entries
+// only, located through the presence mask staged per window in shared memory
+// -- half the bytes, 2.3 GB per sweep, but the data-dependent gathers made
+// K1 2.14 ms against 1.13 ms on the dense band) or the dense one (default)
+#ifndef SPTRSV_BB_PACKED
+#define SPTRSV_BB_PACKED 0
+#endif
+constexpr bool kBBPacked = SPTRSV_BB_PACKED;
+#ifndef SPTRSV_BB_PF
+#define SPTRSV_BB_PF 16
+#endif
+constexpr int kPf = SPTRSV_BB_PF;  // coefficient prefetch distance (columns)
+#ifndef SPTRSV_BB_TSLOTS
+#define SPTRSV_BB_TSLOTS 4
+#endif
+constexpr int kTSlots = SPTRSV_BB_TSLOTS;  // K2 ring depth (steps)
 constexpr int kTailBytes = kW * kW * 8;
+
+// ---- setup: the packed band ------------------------------------------------
+__global__ void k_bb_popc(const unsigned long long* __restrict__ mask, long long n, int* __restrict__ cnt) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    cnt[j] = __popcll(mask[j]);
+}
+__global__ void k_bb_pack(const double* __restrict__ coef, const unsigned long long* __restrict__ mask,
+                          const int* __restrict__ off, long long n, double* __restrict__ pk) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    unsigned long long m = mask[j];
+    int o = off[j];
+    while (m) {
+      const int bit = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      pk[o++] = coef[(size_t)j * kW + bit];
+    }
+  }
+}
 
 // ---- setup: N_k tail ------------------------------------------------------
 // One CTA of two warps per block; lane m (of warp h) follows coupling column
@@ -95,6 +127,9 @@ __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef
 // ---- K1 / K3: one warp per block, the band window sweep --------------------
 struct SweepArgs {
   const double* coef;  // [n_pad][64]: w(j + d, j) at [j][d - 1] (pre-scaled, fast mode)
+  const double* pk;    // packed: column j's stored entries in row order at pk[off[j] ..]
+  const int* off;
+  const unsigned long long* mask;  // bit d - 1 of mask[j]: (j + d, j) is stored
   const double* b;
   const double* rdg;
   const double* tt;    // K3: t_k = x of block k's tail rows, [nblk][64] (null in K1)
@@ -131,16 +166,61 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constan
   const int ncol = (int)(s1 - s0);
   // coefficient register ring: column j's two entries of this lane, kPf columns ahead
   double cf[kPf][2];
+  // packed: the presence masks and offsets of windows w .. w + 2 staged in
+  // this warp's shared-memory ring by cp.async two windows ahead, so a
+  // column's entry loads do not wait on a global load of its mask
+  __shared__ unsigned long long s_mask[kBBWarps][3][kW];
+  __shared__ int s_off[kBBWarps][3][kW];
+  const int wq = threadIdx.x >> 5;
+  auto stage = [&](int w) {  // window w's masks / offsets (columns beyond n are never read)
+    if (kBBPacked) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const long long col = s0 + (long long)w * kW + h * 32 + lane;
+        if (col < a.n) {
+          cp_async8(&s_mask[wq][w % 3][h * 32 + lane], a.mask + col);
+          cp_async4(&s_off[wq][w % 3][h * 32 + lane], a.off + col);
+        }
+      }
+      cp_async_commit();
+    }
+  };
   auto cload = [&](long long j, double (&dst)[2], int p) {
+    if (kBBPacked) {
+      // the column's presence mask and offset (broadcast shared loads), then
+      // the lane's entries from the packed stream
+      const int rel = (int)(j - s0), ws = (rel / kW) % 3, wi = rel % kW;
+      const unsigned long long m = j < s1 ? s_mask[wq][ws][wi] : 0ull;
+      const int o = j < s1 ? s_off[wq][ws][wi] : 0;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int bit = (2 * lane + s - p - 1) & (kW - 1);
+        const bool present = (m >> bit) & 1ull;
+        dst[s] = present ? __ldg(a.pk + o + __popcll(m & ((1ull << bit) - 1ull))) : 0.0;
+      }
+      return;
+    }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const int d = ((2 * lane + s - p - 1) & (kW - 1)) + 1;
       dst[s] = j < s1 ? __ldg(a.coef + (size_t)j * kW + d - 1) : 0.0;
     }
   };
+  stage(0);
+  stage(1);
+  cp_async_wait<0>();
+  __syncwarp();
 #pragma unroll
   for (int u = 0; u < kPf; ++u) cload(s0 + u, cf[u], u);
   for (int c0 = 0; c0 < ncol; c0 += kW) {
+    if (kBBPacked && c0 > 0) {
+      // window w + 1 (staged a window ago) must have landed; window w + 2 starts
+      stage(c0 / kW + 2);
+      cp_async_wait<1>();
+      __syncwarp();
+    } else if (kBBPacked) {
+      stage(2);
+    }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       const long long i = s0 + c0 + kW + 2 * lane + s;
@@ -298,6 +378,23 @@ int DevicePlan::build_band_blocks() {
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
+  if (kBBPacked) {
+    // off = exclusive scan of the per-column entry counts; pk in row order
+    int* cnt = nullptr;
+    if ((e = al((void**)&cnt, sizeof(int) * (n + 1))) != cudaSuccess ||
+        (e = al((void**)&bblk.off, sizeof(int) * (n + 1))) != cudaSuccess ||
+        (e = al((void**)&bblk.pk, sizeof(double) * std::max<long long>(noff, 1))) != cudaSuccess ||
+        (e = cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    const int g = (int)std::min<long long>((n + 255) / 256, 148 * 32);
+    k_bb_popc<<<g, 256, 0, stream>>>(band.mask, n, cnt);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = scan_exclusive(cnt, bblk.off, (int)n + 1, stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    k_bb_pack<<<g, 256, 0, stream>>>(band.coef, band.mask, bblk.off, n, bblk.pk);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    cudaFree(cnt);
+  }
   bblk.ready = true;
   return SPTRSV_OK;
 }
@@ -308,6 +405,9 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   if ((e = reset_control(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   SweepArgs sa{};
   sa.coef = band.coef;
+  sa.pk = bblk.pk;
+  sa.off = bblk.off;
+  sa.mask = band.mask;
   sa.b = d_b;
   sa.rdg = rdg;
   sa.n = n;

@@ -115,9 +115,14 @@ struct DevicePlan {
     double* nt = nullptr;  // [nblk - 2] 64 x 64 coupling tails
     double* ct = nullptr;  // [nblk][64] tails of the uncoupled block solves
     double* tt = nullptr;  // [nblk][64] tails of x
+    // the band's stored entries packed per column in row order (pk[off[j] ..]),
+    // located through the presence mask: the sweeps stream ~half the bytes of
+    // the dense 64-wide band
+    double* pk = nullptr;
+    int* off = nullptr;  // [n_pad + 1]
     void release() {
-      double* ptrs[] = {nt, ct, tt};
-      for (double* p : ptrs)
+      void* ptrs[] = {nt, ct, tt, pk, off};
+      for (void* p : ptrs)
         if (p) cudaFree(p);
       *this = BandBlocks();
     }
