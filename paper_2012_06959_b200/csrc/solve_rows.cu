@@ -150,6 +150,13 @@ __device__ __forceinline__ void publish_u64(const RowsArgs& a, int i, double v) 
   if (a.stamps) a.stamps[i] = (long long)globaltimer_ns();
 }
 
+// dependencies per round of a thread's row: their column indices / values,
+// then their x slots, all in flight before the first wait
+#ifndef SPTRSV_ROW_GROUP
+#define SPTRSV_ROW_GROUP 4
+#endif
+constexpr int kRowGroup = SPTRSV_ROW_GROUP;
+
 // One lane, one row, floating point.
 template <int MODE>
 __device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
@@ -158,21 +165,21 @@ __device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
   int k = a.rp[i];
   const int end = a.rp[i + 1];
   const bool multi = a.owner != nullptr;
-  for (; k < end; k += 4) {
-    int j[4];
-    double v[4];
-    unsigned long long u[4];
-    const unsigned long long* p[4];
-    bool rem[4];
+  for (; k < end; k += kRowGroup) {
+    int j[kRowGroup];
+    double v[kRowGroup];
+    unsigned long long u[kRowGroup];
+    const unsigned long long* p[kRowGroup];
+    bool rem[kRowGroup];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kRowGroup; ++q) {
       if (k + q < end) {
         j[q] = __ldg(a.ci + k + q);
         v[q] = __ldg(a.val + k + q);
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kRowGroup; ++q) {
       if (k + q < end) {
         p[q] = slot_u64<MODE>(a, j[q], rem[q]);
         u[q] = rem[q] ? ld_relaxed_sys_u64(p[q]) : ld_relaxed_u64(p[q]);
@@ -180,7 +187,7 @@ __device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kRowGroup; ++q) {
       if (k + q < end) {
         if (!poll.wait_u64(p[q], rem[q], u[q])) return false;
         acc.add(v[q], as_f64(u[q]));
@@ -345,6 +352,53 @@ __device__ bool solve_row_warp(const RowsArgs& a, Poller& poll, int i, int lane)
       }
       if (__any_sync(0xffffffffu, !ok)) return false;
     }
+  }
+  if (MODE == kModeExact) {
+    // Exact: kLongUnroll rounds of 32 entries in flight at once, their products
+    // v * x_j parked in this warp's shared-memory slots in entry order, then
+    // lane 0 adds them one after another (the serial oracle's ascending
+    // column order: the sum is inherently sequential, but one DADD chain
+    // from shared memory instead of a shuffle round trip per entry and a
+    // memory round trip per 32 entries)
+    constexpr int kLongUnroll = SPTRSV_LONG_UNROLL;
+    __shared__ double s_prod[8][kWarp * SPTRSV_LONG_UNROLL];
+    double* sp = s_prod[(threadIdx.x >> 5) & 7];
+    for (; base < end; base += kWarp * kLongUnroll) {
+      int j[kLongUnroll];
+      double v[kLongUnroll];
+      unsigned long long u[kLongUnroll];
+      const unsigned long long* p[kLongUnroll];
+      bool rem[kLongUnroll];
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q) {
+        const int k = base + q * kWarp + lane;
+        j[q] = k < end ? __ldg(a.ci + k) : -1;
+        v[q] = k < end ? __ldg(a.val + k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q) {
+        if (j[q] >= 0) {
+          p[q] = slot_u64<MODE>(a, j[q], rem[q]);
+          u[q] = rem[q] ? ld_relaxed_sys_u64(p[q]) : ld_relaxed_u64(p[q]);
+          if (rem[q]) ++poll.remote;
+        }
+      }
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < kLongUnroll; ++q)
+        if (j[q] >= 0) {
+          ok = ok && poll.wait_u64(p[q], rem[q], u[q]);
+          sp[q * kWarp + lane] = __dmul_rn(v[q], as_f64(u[q]));
+        }
+      if (__any_sync(0xffffffffu, !ok)) return false;
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = min(kWarp * kLongUnroll, end - base);
+        for (int q = 0; q < cnt; ++q) s = __dadd_rn(s, sp[q]);
+      }
+      __syncwarp();  // the slots are rewritten by the next round
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
   }
   for (; base < end; base += kWarp) {
     int k = base + lane;
