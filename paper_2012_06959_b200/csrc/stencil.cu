@@ -1132,7 +1132,10 @@ __device__ void prep_task(const StArgs& a, int p, unsigned long long deadline) {
   const bool pairs = ((reinterpret_cast<uintptr_t>(bin) & 15) == 0) && (a.nx % 2 == 0);
   constexpr int kU = 8;  // loads in flight per thread (a loop of dependent load/store pairs paid a DRAM
                          // round trip per pair: ~7.6 us per band, slower than the wavefront)
-  for (int t = 0; t < a.n_tasks; ++t) {
+  // (a PE partition preps only its own bands, in its ticket order)
+  const int n_prep = a.my_tasks ? a.n_my_tasks : a.n_tasks;
+  for (int it = 0; it < n_prep; ++it) {
+    const int t = a.my_tasks ? a.my_tasks[it] : it;
     if (a.bflag) {  // streamed host solve: band t's b may still be on its way
       __shared__ int ok_s;
       if (tid == 0) {
@@ -1338,7 +1341,10 @@ cudaError_t launch_stencil_v(const StArgs& a, int blocks, cudaStream_t s) {
 // probe bits 12..15 select an ablation variant of the fast kernel (timing only)
 template <bool EXACT>
 cudaError_t launch_stencil(const StArgs& a, int blocks, cudaStream_t s) {
-  if (a.band_owner) return launch_stencil_v<EXACT, 0, true>(a, blocks, s);
+  if (a.band_owner) {
+    if (!EXACT && a.prep_tasks > 0) return launch_stencil_v<EXACT, 0, true, 1, false, true>(a, blocks, s);
+    return launch_stencil_v<EXACT, 0, true>(a, blocks, s);
+  }
   if (!EXACT) {
     switch ((a.probe >> 12) & 15) {
       case 1: return launch_stencil_v<EXACT, 1>(a, blocks, s);
@@ -1605,7 +1611,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   // write bd = b * (1/d) on the SMs the 64 bands leave idle; SPTRSV_NO_BD=1
   // keeps the multiply in the step, diagnostics)
   static const bool no_bd = std::getenv("SPTRSV_NO_BD") != nullptr;
-  const bool bd_mode = !stencil.exact && !many && !stencil.part && kStCluster == 1 && !no_bd;
+  const bool bd_mode = !stencil.exact && !many && kStCluster == 1 && !no_bd;
   if (bd_mode) {
     if (!stencil.bd) {
       if ((e = cudaMalloc((void**)&stencil.bd, sizeof(double) * (size_t)n)) != cudaSuccess ||
