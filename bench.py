@@ -231,7 +231,10 @@ def main():
     setup_s = time.perf_counter() - ts
     info = plan.info()
     if ws > 1:
-        info["executor"] = f"{info['executor']} (PE partition, peer {'mailboxes' if info['executor'] == 'stencil' else 'segments'})"
+        if solver.replicated:  # no per-PE mode for this executor: every rank solves the whole system
+            info["executor"] = f"{info['executor']} (replicated per rank: no per-PE mode)"
+        else:
+            info["executor"] = f"{info['executor']} (PE partition, peer {'mailboxes' if info['executor'] == 'stencil' else 'segments'})"
 
     db = torch.from_numpy(b).to(f"cuda:{dev}")
     dx = torch.zeros_like(db)

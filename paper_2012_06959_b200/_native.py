@@ -542,10 +542,22 @@ def pe_solver_for(l, partition, executor: str = "auto", **kw):
         plans = []
         for p in range(P):
             pl = build(devs[p])
+            ex0 = pl.info()["executor"]
             pl.set_partition(owner, P, p)
+            if ex0 != "rows" and pl.info()["executor"] != ex0:
+                # a structured executor without a per-PE mode (band blocks, 3D
+                # wavefront, lane chains, a band-splitting 2D owner map) would
+                # degrade to the component pool: one GPU runs the fast plan
+                for q in plans + [pl]:
+                    q.close()
+                plans = None
+                break
             plans.append(pl)
-        _wire(plans)
-        solver = PeGroup(plans, devs, "pe-per-gpu")
+        if plans is not None:
+            _wire(plans)
+            solver = PeGroup(plans, devs, "pe-per-gpu")
+        else:
+            solver = SharedSegment(plan_for(l, executor=executor, device=device, **kw))
     else:
         single = plan_for(l, executor=executor, device=device, **kw)
         ex = single.info()["executor"]

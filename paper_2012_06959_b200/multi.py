@@ -77,14 +77,28 @@ class DistributedSolver:
         self.world = plan.n_pes
         self.group = group
         # auto: a 2D five-point L with a band-aligned owner map runs the stencil
-        # executor partitioned (peer mailboxes); anything else the component pool
-        self.native = _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision,
-                                         executor=executor, device=device, timeout=timeout)
+        # executor partitioned (peer mailboxes); an unstructured L the component
+        # pool with per-PE segments. The structured executors without a per-PE
+        # mode (band blocks, 3D wavefront, lane chains, or a 2D wavefront whose
+        # owner map splits bands) would degrade to the pool (banded-8M: 3.6 ms
+        # -> 13 s), so there every rank solves the whole system on its own GPU
+        # and keeps its rows ("replicated": correct, no speed-up, no regression).
+        build = lambda: _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision,  # noqa: E731
+                                           executor=executor, device=device, timeout=timeout)
+        self.native = build()
+        ex0 = self.native.info()["executor"]
         self.native.set_partition(plan.owner_arr, plan.n_pes, rank)
-        handles = exchange_handles(self.native.export_segment(), group)
-        for pe, h in enumerate(handles):
-            if pe != rank:
-                self.native.import_segment(pe, h)
+        ex1 = self.native.info()["executor"]
+        # (every rank decides alike: same matrix, same partition law)
+        self.replicated = ex0 != "rows" and ex0 != ex1
+        if self.replicated:
+            self.native.close()
+            self.native = build()
+        else:
+            handles = exchange_handles(self.native.export_segment(), group)
+            for pe, h in enumerate(handles):
+                if pe != rank:
+                    self.native.import_segment(pe, h)
         self.rows = owned_rows(plan.owner_arr, rank)
 
     def barrier(self) -> None:
