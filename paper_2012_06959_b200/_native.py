@@ -513,6 +513,9 @@ def pe_solver_for(l, partition, executor: str = "auto", **kw):
       publishing its rows into its own HBM, peers read over NVLink (P2P);
     * one GPU, 2D five-point L with whole 64-row bands per PE: one stencil
       plan per PE, peers' mailboxes in the same HBM (``mode="stencil-pes"``);
+    * one GPU, banded L in fast mode with slabs on row-block boundaries: one
+      band-block plan per PE, the tail chain handed from PE to PE
+      (``mode="band-pes"``);
     * one GPU, unstructured L: the component pool with one segment per PE
       (``mode="pool-segments"``);
     * one GPU, any other structured L: the single fast plan
@@ -545,8 +548,9 @@ def pe_solver_for(l, partition, executor: str = "auto", **kw):
             ex0 = pl.info()["executor"]
             pl.set_partition(owner, P, p)
             if ex0 != "rows" and pl.info()["executor"] != ex0:
-                # a structured executor without a per-PE mode (band blocks, 3D
-                # wavefront, lane chains, a band-splitting 2D owner map) would
+                # a structured executor without a per-PE mode (3D wavefront,
+                # lane chains, band window (exact), a band-splitting 2D owner
+                # map, band slabs off the row-block boundaries) would
                 # degrade to the component pool: one GPU runs the fast plan
                 for q in plans + [pl]:
                     q.close()
@@ -562,17 +566,20 @@ def pe_solver_for(l, partition, executor: str = "auto", **kw):
         single = plan_for(l, executor=executor, device=device, **kw)
         ex = single.info()["executor"]
         solver = None
-        if ex == "stencil":
-            first = build(device, "stencil")
+        if ex in ("stencil", "band"):
+            # 2D: whole 64-row bands per PE (partitioned wavefront); band
+            # blocks (fast mode): slabs on row-block boundaries (each PE its
+            # blocks' sweeps and its stretch of the tail chain)
+            first = build(device, ex)
             first.set_partition(owner, P, 0)
-            if first.info()["executor"] == "stencil":  # whole bands per PE (2D): partitioned wavefront
+            if first.info()["executor"] == ex:
                 plans = [first]
                 for p in range(1, P):
-                    pl = build(device, "stencil")
+                    pl = build(device, ex)
                     pl.set_partition(owner, P, p)
                     plans.append(pl)
                 _wire(plans)
-                solver = PeGroup(plans, devs, "stencil-pes")
+                solver = PeGroup(plans, devs, ex + "-pes")
             else:
                 first.close()
         if solver is None and ex in ("rows", "push"):

@@ -136,13 +136,14 @@ struct SweepArgs {
   double* out;         // K1: c tails [nblk][64]; K3: x
   long long n;
   int S, nblk;
+  int k_begin, k_end;  // the blocks of this PE (all blocks without a partition)
 };
 
 template <bool COUPLED>
 __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constant__ SweepArgs a) {
   const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * kBBWarps + (threadIdx.x >> 5);
-  if (k >= a.nblk) return;
+  const int k = a.k_begin + blockIdx.x * kBBWarps + (threadIdx.x >> 5);
+  if (k >= a.k_end) return;
   const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
   // lane owns window rows 2 lane + s (s = 0, 1) of each 64-row window
   double acc[2];
@@ -256,6 +257,12 @@ struct TailArgs {
   const double* ct;   // [nblk][64] c tails (K1)
   double* tt;         // [nblk][64] t
   int nblk;
+  // PE partition: this PE's blocks [k_begin, k_end); t_{k_begin - 1} comes
+  // from the previous PE's slot (value-is-flag words), t_{k_end - 1} goes to
+  // this PE's slot for the next one (null: no such PE)
+  int k_begin, k_end;
+  const unsigned long long* prev_slot;
+  unsigned long long* my_slot;
   DeviceStatus* status;
   int* abort_flag;
   unsigned long long timeout_ns;
@@ -286,18 +293,41 @@ __global__ void __launch_bounds__(160, 1) k_bb_tail(const __grid_constant__ Tail
     ctl[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < kW) tb[tid] = a.ct[tid];  // t_0 = c_0 tail
-  __syncthreads();
-  if (tid < kW) a.tt[tid] = tb[tid];
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  // the chain enters at block kb with t_{kb - 1}
+  const int kb = a.k_begin == 0 ? 1 : a.k_begin;
+  const int klast = min(a.k_end, a.nblk - 1) - 1;  // the last block whose tail is needed
+  if (tid < kW) {
+    double t0;
+    if (a.k_begin == 0) {
+      t0 = a.ct[tid];  // t_0 = c_0 tail
+    } else {
+      // the previous PE's last tail: one-sided loads of its slot until the
+      // word is published (system scope: the slot may be a peer mapping)
+      unsigned long long u = ld_relaxed_sys_u64(a.prev_slot + tid);
+      int polls = 0;
+      while (u == kNotReady) {
+        if ((++polls & 1023) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag))) {
+          atomicExch(&a.status->code, 5);
+          atomicExch(a.abort_flag, 1);
+          break;
+        }
+        u = ld_relaxed_sys_u64(a.prev_slot + tid);
+      }
+      t0 = __longlong_as_double((long long)u);
+    }
+    tb[((kb - 1) & 1) * kW + tid] = t0;
+    a.tt[(size_t)(kb - 1) * kW + tid] = t0;
+  }
+  __syncthreads();
   if (tid >= 128) {
     if (tid != 128) return;
-    // producer: step k (1 .. nblk-2) uses slot (k - 1) % kTSlots
-    for (int k = 1; k < a.nblk - 1; ++k) {
-      const int q = (k - 1) % kTSlots;
-      if (k - 1 >= kTSlots) {
+    // producer: step k (kb .. klast) uses slot (k - kb) % kTSlots
+    for (int k = kb; k <= klast; ++k) {
+      const int q = (k - kb) % kTSlots;
+      if (k - kb >= kTSlots) {
         int polls = 0;
-        while (ld_acquire_cta(ctl) < k - kTSlots) {  // the slot's previous step is done
+        while (ld_acquire_cta(ctl) < k - kb + 1 - kTSlots) {  // the slot's previous step is done
           if ((++polls & 1023) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
             return;
         }
@@ -311,9 +341,9 @@ __global__ void __launch_bounds__(160, 1) k_bb_tail(const __grid_constant__ Tail
   }
   const int r = tid & (kW - 1), h = tid >> 6;
   unsigned phase = 0;
-  // t_k for blocks 1 .. nblk-2 (the last block's tail is not needed)
-  for (int k = 1; k < a.nblk - 1; ++k) {
-    const int q = (k - 1) % kTSlots;
+  // t_k for blocks kb .. klast (the last block's tail is not needed)
+  for (int k = kb; k <= klast; ++k) {
+    const int q = (k - kb) % kTSlots;
     int polls = 0;
     bool ok = true;
     while (!mbar_try_wait(&bars[q], (phase >> q) & 1u)) {
@@ -349,7 +379,12 @@ __global__ void __launch_bounds__(160, 1) k_bb_tail(const __grid_constant__ Tail
       a.tt[(size_t)k * kW + r] = t;
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (tid == 0) st_release_cta(ctl, k);
+    if (tid == 0) st_release_cta(ctl, k - kb + 1);
+  }
+  // hand this PE's last tail to the next PE (value-is-flag words)
+  if (a.my_slot && tid < kW && !ld_relaxed_s32(a.abort_flag)) {
+    const int kl = a.k_end - 1;
+    st_relaxed_sys_u64(a.my_slot + tid, (unsigned long long)__double_as_longlong(tb[(kl & 1) * kW + tid]));
   }
 }
 
@@ -399,10 +434,52 @@ int DevicePlan::build_band_blocks() {
   return SPTRSV_OK;
 }
 
+// PE partition: contiguous slabs in PE order whose boundaries fall on row
+// blocks (multiples of S). Returns 1 when installed, 0 when the owner map does
+// not fit (the caller falls back), -1 on a CUDA error.
+int DevicePlan::set_band_partition(const int32_t* owner, int pes, int my_pe) {
+  const long long S = bblk.S;
+  std::vector<long long> r0(pes, -1), r1(pes, -1);
+  for (long long i = 0; i < n; ++i) {
+    const int o = owner[i];
+    if (i > 0 && o < owner[i - 1]) return 0;  // not in PE order
+    if (r0[o] < 0) r0[o] = i;
+    else if (r1[o] != i) return 0;  // not contiguous
+    r1[o] = i + 1;
+  }
+  for (int p = 0; p < pes; ++p) {
+    if (r0[p] < 0) return 0;                  // every PE owns a slab
+    if (r0[p] % S || (r1[p] % S && r1[p] != n)) return 0;  // on block boundaries
+  }
+  bblk.release_part();
+  cudaError_t e;
+  if ((e = cudaMalloc((void**)&bblk.slot, 2 * kW * sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMemset(bblk.slot, 0xFF, 2 * kW * sizeof(unsigned long long))) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e)), -1;
+  bblk.k0 = (int)(r0[my_pe] / S);
+  bblk.k1 = (int)((r1[my_pe] + S - 1) / S);
+  bblk.my_pe = my_pe;
+  bblk.n_pes = pes;
+  bblk.part = true;
+  return 1;
+}
+
 int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s) {
   if (!bblk.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "band blocks were not built for this plan");
+  if (bblk.part && bblk.my_pe > 0 && !bblk.prev_slot)
+    return plan_fail(SPTRSV_E_INVALID_PE, "the previous PE's segment was never imported");
   cudaError_t e;
   if ((e = reset_control(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // partition: this solve publishes into / reads slot half `par` (reset by
+  // the previous solve) and resets the other half for the next one
+  // (consecutive solves are separated by a barrier across PEs)
+  const int par = (int)(bblk.solves & 1);
+  if (bblk.part) {
+    ++bblk.solves;
+    if ((e = cudaMemsetAsync(bblk.slot + (1 - par) * kW, 0xFF, kW * sizeof(unsigned long long), s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  const int kb = bblk.part ? bblk.k0 : 0, ke = bblk.part ? bblk.k1 : bblk.nblk;
   SweepArgs sa{};
   sa.coef = band.coef;
   sa.pk = bblk.pk;
@@ -413,7 +490,9 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   sa.n = n;
   sa.S = bblk.S;
   sa.nblk = bblk.nblk;
-  const int grid = (bblk.nblk + kBBWarps - 1) / kBBWarps;
+  sa.k_begin = kb;
+  sa.k_end = ke;
+  const int grid = (ke - kb + kBBWarps - 1) / kBBWarps;
   if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   // K1: c tails
   sa.out = bblk.ct;
@@ -425,6 +504,10 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   ta.ct = bblk.ct;
   ta.tt = bblk.tt;
   ta.nblk = bblk.nblk;
+  ta.k_begin = kb;
+  ta.k_end = ke;
+  ta.prev_slot = bblk.part && kb > 0 ? bblk.prev_slot + par * kW : nullptr;
+  ta.my_slot = bblk.part && ke < bblk.nblk ? bblk.slot + par * kW : nullptr;
   ta.status = status;
   ta.abort_flag = abort_flag;
   ta.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);

@@ -40,6 +40,7 @@ __global__ void k_gather_owned(unsigned long long* const* segs, const unsigned c
 
 void DevicePlan::release_partition() {
   stencil.release_part();
+  bblk.release_part();
   for (auto* s : local_segs) cudaFree(s);
   local_segs.clear();
   for (void* p : opened_peers) cudaIpcCloseMemHandle(p);
@@ -75,6 +76,13 @@ int DevicePlan::set_partition(const int32_t* owner, int pes, int my_pe) {
     // band-aligned block (or band round-robin) ownership: the stencil
     // executor runs partitioned; anything else falls back to the pool
     const int rc = set_stencil_partition(owner, pes, my_pe);
+    if (rc < 0) return SPTRSV_E_CUDA;
+    if (rc == 1) return SPTRSV_OK;
+  }
+  if (executor_used == SPTRSV_EXECUTOR_BAND && bblk.ready && my_pe >= 0) {
+    // contiguous slabs in PE order on row-block boundaries: the band-block
+    // executor runs partitioned; anything else falls back to the pool
+    const int rc = set_band_partition(owner, pes, my_pe);
     if (rc < 0) return SPTRSV_E_CUDA;
     if (rc == 1) return SPTRSV_OK;
   }
@@ -331,6 +339,14 @@ int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* handle_out) {
     std::memcpy(handle_out, &h, sizeof(h));
     return SPTRSV_OK;
   }
+  if (p->bblk.part) {  // the band chain's shared state is this PE's tail slot
+    cudaSetDevice(p->device);
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, p->bblk.slot);
+    if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return SPTRSV_OK;
+  }
   if (p->local_segs.size() != 1) return plan_fail(SPTRSV_E_ARGUMENT, "export needs a one-PE-per-process partition");
   cudaSetDevice(p->device);
   cudaIpcMemHandle_t h;
@@ -343,10 +359,12 @@ int sptrsv_plan_export_segment(const sptrsv_plan* plan, void* handle_out) {
 int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle) {
   auto* p = reinterpret_cast<DevicePlan*>(plan);
   if (!p || !handle) return plan_fail(SPTRSV_E_ARGUMENT, "null argument");
-  const bool st = p->stencil.part;
-  if (pe < 0 || pe >= (st ? p->stencil.n_pes : p->n_pes)) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
-  if (st ? pe == p->stencil.my_pe : (pe >= p->pe_base && pe < p->pe_base + p->n_pe_local))
+  const bool st = p->stencil.part, bb = p->bblk.part;
+  if (pe < 0 || pe >= (st ? p->stencil.n_pes : bb ? p->bblk.n_pes : p->n_pes))
+    return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+  if (st ? pe == p->stencil.my_pe : bb ? pe == p->bblk.my_pe : (pe >= p->pe_base && pe < p->pe_base + p->n_pe_local))
     return plan_fail(SPTRSV_E_ARGUMENT, "pe is local");
+  if (bb && pe != p->bblk.my_pe - 1) return SPTRSV_OK;  // the chain reads the previous PE's slot only
   cudaSetDevice(p->device);
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle, sizeof(h));
@@ -354,6 +372,10 @@ int sptrsv_plan_import_segment(sptrsv_plan* plan, int32_t pe, const void* handle
   cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   p->opened_peers.push_back(ptr);
+  if (bb) {
+    p->bblk.prev_slot = reinterpret_cast<const unsigned long long*>(ptr);
+    return SPTRSV_OK;
+  }
   if (st) {
     p->stencil.host_pe_mbox[pe] = reinterpret_cast<unsigned long long*>(ptr);
     return p->stencil_sync_peers();
@@ -372,6 +394,11 @@ int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr
     p->stencil.host_pe_mbox[pe] = reinterpret_cast<unsigned long long*>(device_ptr);
     return p->stencil_sync_peers();
   }
+  if (p->bblk.part) {
+    if (pe < 0 || pe >= p->bblk.n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
+    if (pe == p->bblk.my_pe - 1) p->bblk.prev_slot = reinterpret_cast<const unsigned long long*>(device_ptr);
+    return SPTRSV_OK;
+  }
   if (pe < 0 || pe >= p->n_pes) return plan_fail(SPTRSV_E_INVALID_PE, "pe out of range");
   cudaSetDevice(p->device);
   p->host_seg_table[pe] = reinterpret_cast<unsigned long long*>(device_ptr);
@@ -381,6 +408,7 @@ int sptrsv_plan_set_peer_segment(sptrsv_plan* plan, int32_t pe, void* device_ptr
 void* sptrsv_plan_segment(const sptrsv_plan* plan) {
   auto* p = reinterpret_cast<const DevicePlan*>(plan);
   if (p && p->stencil.part) return p->stencil.mbox;
+  if (p && p->bblk.part) return p->bblk.slot;
   if (!p || p->local_segs.empty()) return nullptr;
   return p->local_segs[0];
 }

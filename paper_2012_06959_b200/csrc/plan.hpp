@@ -120,7 +120,24 @@ struct DevicePlan {
     // the dense 64-wide band
     double* pk = nullptr;
     int* off = nullptr;  // [n_pad + 1]
+    // PE partition (set_partition with contiguous slabs on block boundaries):
+    // this PE sweeps blocks [k0, k1) and runs their part of the tail chain;
+    // the chain enters from the previous PE's last tail, read from its slot
+    // (one-sided loads), and leaves through this PE's own slot
+    bool part = false;
+    int k0 = 0, k1 = 0, my_pe = 0, n_pes = 1;
+    unsigned long long* slot = nullptr;             // own [2][64], value-is-flag, by solve parity
+    const unsigned long long* prev_slot = nullptr;  // PE my_pe - 1's slot (peer mapping)
+    long long solves = 0;
+    void release_part() {
+      if (slot) cudaFree(slot);
+      slot = nullptr;
+      prev_slot = nullptr;
+      part = false;
+      k0 = 0, k1 = nblk, my_pe = 0, n_pes = 1, solves = 0;
+    }
     void release() {
+      release_part();
       void* ptrs[] = {nt, ct, tt, pk, off};
       for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -128,6 +145,7 @@ struct DevicePlan {
     }
   } bblk;
   int build_band_blocks();
+  int set_band_partition(const int32_t* owner, int pes, int my_pe);
   int solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s);
   int solve_push(const double* d_b, double* d_x, cudaStream_t s);
 

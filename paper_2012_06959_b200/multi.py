@@ -77,12 +77,16 @@ class DistributedSolver:
         self.world = plan.n_pes
         self.group = group
         # auto: a 2D five-point L with a band-aligned owner map runs the stencil
-        # executor partitioned (peer mailboxes); an unstructured L the component
-        # pool with per-PE segments. The structured executors without a per-PE
-        # mode (band blocks, 3D wavefront, lane chains, or a 2D wavefront whose
-        # owner map splits bands) would degrade to the pool (banded-8M: 3.6 ms
-        # -> 13 s), so there every rank solves the whole system on its own GPU
-        # and keeps its rows ("replicated": correct, no speed-up, no regression).
+        # executor partitioned (peer mailboxes); a banded L in fast mode with
+        # slabs on row-block boundaries the band-block executor partitioned
+        # (each rank sweeps its blocks, the tail chain passes rank to rank
+        # through one 64-value slot); an unstructured L the component pool with
+        # per-PE segments. The structured executors without a per-PE mode (3D
+        # wavefront, lane chains, the exact band window, or owner maps that
+        # split bands / row blocks) would degrade to the pool (banded-8M:
+        # 3.6 ms -> 13 s), so there every rank solves the whole system on its
+        # own GPU and keeps its rows ("replicated": correct, no speed-up, no
+        # regression).
         build = lambda: _native.NativePlan(l.col_ptr, l.row_idx, l.values, l.n, precision=precision,  # noqa: E731
                                            executor=executor, device=device, timeout=timeout)
         self.native = build()

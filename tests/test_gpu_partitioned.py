@@ -83,15 +83,42 @@ def test_dropin_n_pes_keeps_the_wavefront(n_pes, precision):
         assert report.totals()["components_solved"] == l.n
 
 
+@pytest.mark.parametrize("n_pes", [2, 3, 4])
+@pytest.mark.parametrize("n", [7680, 7710])
+def test_dropin_n_pes_band_blocks_partitioned(n_pes, n):
+    """Fast mode, banded L, contiguous slabs on 64-row block boundaries: one
+    band-block plan per PE (its blocks' sweeps and its stretch of the tail
+    chain, the chain handed PE to PE through a 64-value slot); x within 1e-12
+    of the oracle over repeated solves (slot halves alternate by parity).
+    n = 7710: the last PE's last block is partial."""
+    l = synth.banded(n, 64, 0.5, 6)
+    plan = sp.nnz_block_partition(np.ones(n), n_pes, 64)
+    cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=n_pes, precision="fast")
+    for seed in range(3):
+        b = np.random.default_rng(seed).uniform(-1.0, 1.0, l.n)
+        x, report = sp.solve(l, b, plan, cfg)
+        assert report.device["executor"] == "band"
+        assert report.device["pe_mode"] in ("band-pes", "pe-per-gpu")
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        assert sp.compare_solutions(x, ref, 1e-12).within_tol
+        assert report.totals()["components_solved"] == l.n
+
+
 def test_dropin_n_pes_structured_executors_stay_fast():
     """Executors without a per-PE mode (band window, 3D wavefront) keep running
     on one device instead of falling back to the component pool."""
     for l, ex in ((synth.banded(20000, 64, 0.5, 1), "band"), (synth.lap3d(24), "stencil")):
         b = np.random.default_rng(2).uniform(-1.0, 1.0, l.n)
-        cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=4, precision="exact")
-        x, report = sp.solve(l, b, sp.block_partition(l.n, 4), cfg)
-        assert report.device["executor"] == ex
-        assert x.tobytes() == oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b).tobytes()
+        ref = oracle.solve_serial(l.col_ptr, l.row_idx, l.values, b)
+        for precision in ("exact", "fast"):
+            # (block_partition(20000, 4): 5000-row slabs, off the band blocks' 64-row grid)
+            cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=4, precision=precision)
+            x, report = sp.solve(l, b, sp.block_partition(l.n, 4), cfg)
+            assert report.device["executor"] == ex
+            if precision == "exact":
+                assert x.tobytes() == ref.tobytes()
+            else:
+                assert sp.compare_solutions(x, ref, 1e-12).within_tol
 
 
 @pytest.mark.parametrize("name", ["worked_3x3", "random_3", "bidiagonal1000", "blockdiag4096"])
