@@ -24,6 +24,7 @@
 // at ~250 cycles per step. Exact mode keeps the column-ordered window kernel
 // (the serial oracle's summation order).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 #include "plan.hpp"
 #include "kernels.cuh"
@@ -388,6 +389,146 @@ __global__ void __launch_bounds__(160, 1) k_bb_tail(const __grid_constant__ Tail
   }
 }
 
+// ---- K2 by superblocks (one PE) --------------------------------------------
+// The tail chain t_k = c_k + M_k t_{k-1} (M_k = N_k's tail) is an affine
+// recurrence, so it can be cut into superblocks g of G consecutive steps:
+//   d_g = g's steps run from t = 0                   (K2a, all g in parallel)
+//   T_g = P_g T_{g-1} + d_g,  P_g = M_last ... M_first   (K2b, nsb steps)
+//   t_k = g's steps run again from T_{g-1}            (K2c, all g in parallel)
+// P_g depends on L only and is built once per plan (k_bb_prod), so a solve
+// runs G + nsb + G sequential matvecs instead of nblk - 2 (2,046 for
+// banded-8M: ~0.8 ms of latency -> ~0.05 ms).
+__device__ __forceinline__ int k2_index(int r, int m) {  // K2 layout of element (r, m)
+  return (((m >> 5) * 16 + ((m & 31) >> 1)) * kW + r) * 2 + (m & 1);
+}
+
+constexpr int kProdSmem = 2 * kW * kW * 8;
+
+// setup: pp[g] = M_{s1-1} ... M_{s0} for superblock g's steps [s0, s1)
+__global__ void __launch_bounds__(256) k_bb_prod(const double* __restrict__ nt, int nsteps, int G,
+                                                 double* __restrict__ pp) {
+  extern __shared__ __align__(16) double ps_raw[];
+  double (*P)[kW] = reinterpret_cast<double (*)[kW]>(ps_raw);
+  double (*M)[kW] = reinterpret_cast<double (*)[kW]>(ps_raw + kW * kW);
+  const int g = blockIdx.x, tid = threadIdx.x;
+  const int s0 = g * G, s1 = min(nsteps, s0 + G);
+  for (int e = tid; e < kW * kW; e += 256) P[e >> 6][e & 63] = nt[(size_t)s0 * kW * kW + k2_index(e >> 6, e & 63)];
+  const int r = tid >> 2, m0 = (tid & 3) * 16;
+  for (int st = s0 + 1; st < s1; ++st) {
+    for (int e = tid; e < kW * kW; e += 256) M[e >> 6][e & 63] = nt[(size_t)st * kW * kW + k2_index(e >> 6, e & 63)];
+    __syncthreads();
+    double acc[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+    for (int q = 0; q < kW; ++q) {
+      const double mq = M[r][q];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc[u] = __fma_rn(mq, P[q][m0 + u], acc[u]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) P[r][m0 + u] = acc[u];
+  }
+  __syncthreads();
+  for (int e = tid; e < kW * kW; e += 256) pp[(size_t)g * kW * kW + k2_index(e >> 6, e & 63)] = P[e >> 6][e & 63];
+}
+
+struct TailChainArgs {
+  const double* mat;    // step s: 64 x 64 at mat + s * 4096 (K2 layout)
+  const double* cv;     // step s: cv + s * 64
+  const double* init0;  // CTA 0's incoming t (null: zero)
+  const double* init;   // CTA g > 0's incoming t: init + (g - 1) * 64 (null: zero)
+  double* out_all;      // t after step s -> out_all + s * 64 (null: not kept)
+  double* out_last;     // t after CTA g's last step -> out_last + g * 64 (null: not kept)
+  int nsteps, G;        // CTA g runs steps [g G, min(nsteps, (g + 1) G))
+  DeviceStatus* status;
+  int* abort_flag;
+  unsigned long long timeout_ns;
+};
+
+// One CTA per superblock, the same step as k_bb_tail: threads 0..127 sum,
+// thread 128 streams the step's matrix and constant into the ring by TMA.
+__global__ void __launch_bounds__(160, 1) k_bb_chain(const __grid_constant__ TailChainArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + TSmem::kBars);
+  int* ctl = reinterpret_cast<int*>(smem + TSmem::kCtl);
+  double* tb = reinterpret_cast<double*>(smem + TSmem::kT);
+  double* part = reinterpret_cast<double*>(smem + TSmem::kPart);
+  const int tid = threadIdx.x, g = blockIdx.x;
+  const int s0 = g * a.G, s1 = min(a.nsteps, s0 + a.G);
+  if (tid == 0) {
+    for (int q = 0; q < kTSlots; ++q) mbar_init(&bars[q], 1);
+    ctl[0] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
+  if (tid < kW) {
+    const double* in = g == 0 ? a.init0 : (a.init ? a.init + (size_t)(g - 1) * kW : nullptr);
+    tb[kW + tid] = in ? in[tid] : 0.0;  // step s reads buffer (s - s0 + 1) & 1
+  }
+  __syncthreads();
+  if (tid >= 128) {
+    if (tid != 128) return;
+    for (int st = s0; st < s1; ++st) {
+      const int q = (st - s0) % kTSlots;
+      if (st - s0 >= kTSlots) {
+        int polls = 0;
+        while (ld_acquire_cta(ctl) < st - s0 + 1 - kTSlots) {
+          if ((++polls & 1023) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag)))
+            return;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bars[q], kTailBytes + kW * 8);
+      bulk_g2s(smem + TSmem::kN + q * kTailBytes, a.mat + (size_t)st * (kTailBytes / 8), kTailBytes, &bars[q]);
+      bulk_g2s(smem + TSmem::kC + q * kW * 8, a.cv + (size_t)st * kW, kW * 8, &bars[q]);
+    }
+    return;
+  }
+  const int r = tid & (kW - 1), h = tid >> 6;
+  unsigned phase = 0;
+  for (int st = s0; st < s1; ++st) {
+    const int q = (st - s0) % kTSlots, cur = (st - s0) & 1;
+    int polls = 0;
+    bool ok = true;
+    while (!mbar_try_wait(&bars[q], (phase >> q) & 1u)) {
+      if ((++polls & 1023) == 0 && deadline && globaltimer_ns() > deadline) {
+        ok = false;
+        break;
+      }
+    }
+    if (!ok) {
+      if (tid == 0) {
+        atomicExch(&a.status->code, 5);
+        atomicExch(a.abort_flag, 1);
+      }
+      break;
+    }
+    phase ^= 1u << q;
+    const double2* nq = reinterpret_cast<const double2*>(smem + TSmem::kN + q * kTailBytes) + h * 16 * kW + r;
+    const double* tp = tb + (cur ^ 1) * kW + 32 * h;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const double2 w = nq[i * kW];
+      s4[i & 3] = __fma_rn(w.x, tp[2 * i], s4[i & 3]);
+      s4[i & 3] = __fma_rn(w.y, tp[2 * i + 1], s4[i & 3]);
+    }
+    const double sum = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
+    if (h == 1) part[r] = sum;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (h == 0) {
+      const double* cq = reinterpret_cast<const double*>(smem + TSmem::kC + q * kW * 8);
+      const double t = __dadd_rn(cq[r], __dadd_rn(sum, part[r]));
+      tb[cur * kW + r] = t;
+      if (a.out_all) a.out_all[(size_t)st * kW + r] = t;
+      if (a.out_last && st == s1 - 1) a.out_last[(size_t)g * kW + r] = t;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (tid == 0) st_release_cta(ctl, st - s0 + 1);
+  }
+}
+
 }  // namespace
 
 int DevicePlan::build_band_blocks() {
@@ -412,6 +553,29 @@ int DevicePlan::build_band_blocks() {
     k_bb_ntail<<<nblk - 2, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt);
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  // the tail chain by superblocks of G ~ sqrt(steps) steps (SPTRSV_BB_SUPER=0: one sequential chain)
+  static const bool super_on = [] {
+    const char* v = std::getenv("SPTRSV_BB_SUPER");
+    return !v || std::atoi(v) != 0;
+  }();
+  const int nsteps = nblk - 2;
+  if (super_on && nsteps >= 64) {
+    int G = 1;
+    while ((long long)G * G < nsteps) ++G;
+    const int nsb = (nsteps + G - 1) / G;
+    if ((e = al((void**)&bblk.pp, (size_t)nsb * kTailBytes)) != cudaSuccess ||
+        (e = al((void**)&bblk.dd, sizeof(double) * nsb * kW)) != cudaSuccess ||
+        (e = al((void**)&bblk.TT, sizeof(double) * nsb * kW)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    static std::atomic<unsigned long long> pattr{0};
+    if ((e = set_max_dyn_smem(k_bb_prod, kProdSmem, pattr)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    k_bb_prod<<<nsb, 256, kProdSmem, stream>>>(bblk.nt, nsteps, G, bblk.pp);
+    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    bblk.G = G;
+    bblk.nsb = nsb;
   }
   if (kBBPacked) {
     // off = exclusive scan of the per-column entry counts; pk in row order
@@ -511,18 +675,58 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   ta.status = status;
   ta.abort_flag = abort_flag;
   ta.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
-  static std::atomic<unsigned long long> attr{0};
-  if ((e = set_max_dyn_smem(k_bb_tail, TSmem::kTotal, attr)) != cudaSuccess)
-    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  k_bb_tail<<<1, 160, TSmem::kTotal, s>>>(ta);
-  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  int k2_launches = 1;
+  if (!bblk.part && bblk.G > 0) {
+    // K2a / K2b / K2c: the chain by superblocks (see k_bb_chain)
+    static std::atomic<unsigned long long> cattr{0};
+    if ((e = set_max_dyn_smem(k_bb_chain, TSmem::kTotal, cattr)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    const int nsteps = bblk.nblk - 2;
+    TailChainArgs ca{};
+    ca.status = status;
+    ca.abort_flag = abort_flag;
+    ca.timeout_ns = ta.timeout_ns;
+    ca.mat = bblk.nt;
+    ca.cv = bblk.ct + kW;
+    ca.out_last = bblk.dd;
+    ca.nsteps = nsteps;
+    ca.G = bblk.G;
+    k_bb_chain<<<bblk.nsb, 160, TSmem::kTotal, s>>>(ca);  // d_g
+    if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    TailChainArgs cb = ca;
+    cb.mat = bblk.pp;
+    cb.cv = bblk.dd;
+    cb.init0 = bblk.ct;  // t_0 = c_0
+    cb.out_last = nullptr;
+    cb.out_all = bblk.TT;
+    cb.nsteps = bblk.nsb;
+    cb.G = bblk.nsb;
+    k_bb_chain<<<1, 160, TSmem::kTotal, s>>>(cb);  // T_g
+    if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    TailChainArgs cc = ca;
+    cc.init0 = bblk.ct;
+    cc.init = bblk.TT;
+    cc.out_last = nullptr;
+    cc.out_all = bblk.tt + kW;
+    k_bb_chain<<<bblk.nsb, 160, TSmem::kTotal, s>>>(cc);  // every t_k
+    if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    if ((e = cudaMemcpyAsync(bblk.tt, bblk.ct, kW * sizeof(double), cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    k2_launches = 3;
+  } else {
+    static std::atomic<unsigned long long> attr{0};
+    if ((e = set_max_dyn_smem(k_bb_tail, TSmem::kTotal, attr)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+    k_bb_tail<<<1, 160, TSmem::kTotal, s>>>(ta);
+    if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
   // K3: x
   sa.tt = bblk.tt;
   sa.out = d_x;
   k_bb_sweep<true><<<grid, 32 * kBBWarps, 0, s>>>(sa);
   if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-  launches = 3;
+  launches = 2 + k2_launches;
   return SPTRSV_OK;
 }
 

@@ -266,6 +266,7 @@ int DevicePlan::solve_rows(const double* d_b, double* d_x, cudaStream_t s) {
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = coop_long;
   a.long_deps = kLongDeps;
+  a.lane_loop = rows_lane_loop();
   if (mode == kModeFast && split_rows.n_heavy) {
     CUDA_TRY(cudaMemsetAsync(split_rows.part_sum, 0, sizeof(double) * split_rows.n_heavy, s));
     CUDA_TRY(cudaMemsetAsync(split_rows.part_done, 0, sizeof(int) * split_rows.n_heavy, s));

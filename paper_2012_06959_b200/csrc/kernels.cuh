@@ -74,10 +74,12 @@ struct RowsArgs {
   int* part_done;
   long long* stamps;  // diagnostics (probe bit 512): globaltimer at each row's publish
   int debug;          // SPTRSV_PLAN_DEBUG: check owner-only, write-once publication
+  int lane_loop;      // 1: a ticket's short rows complete lane by lane (solve_rows_lanes)
 };
 
 cudaError_t launch_rows(int mode, const RowsArgs& a, int blocks, cudaStream_t s);
 int rows_blocks_per_sm(int mode);
+int rows_lane_loop();  // SPTRSV_ROWS_LANELOOP=0 selects the per-lane spin loops (A/B)
 
 // ---- solve_chains.cu: lane-chain lockstep executor ------------------------
 struct ChainArgs;

@@ -184,6 +184,7 @@ int DevicePlan::solve_partitioned_rows(const double* d_b, double* d_x, cudaStrea
   a.spin_max_ns = opt.spin_max_ns;
   a.coop_long = 0;
   a.long_deps = 1 << 30;
+  a.lane_loop = rows_lane_loop();
   int per_sm = rows_blocks_per_sm(mode);
   // grid_cap: this PE's share of the SMs when several PEs' kernels share the device
   int blocks = std::max(1, (grid_cap > 0 ? std::min(grid_cap, num_sms) : num_sms) * std::max(per_sm, 1));

@@ -115,6 +115,13 @@ struct DevicePlan {
     double* nt = nullptr;  // [nblk - 2] 64 x 64 coupling tails
     double* ct = nullptr;  // [nblk][64] tails of the uncoupled block solves
     double* tt = nullptr;  // [nblk][64] tails of x
+    // the tail chain cut into superblocks of G steps (one PE): pp[g] = the
+    // product of superblock g's coupling tails (built once per plan); per solve
+    // dd[g] = g's chain run from zero, TT[g] = t at the end of g
+    int G = 0, nsb = 0;
+    double* pp = nullptr;  // [nsb] 64 x 64, K2 layout
+    double* dd = nullptr;  // [nsb][64]
+    double* TT = nullptr;  // [nsb][64]
     // the band's stored entries packed per column in row order (pk[off[j] ..]),
     // located through the presence mask: the sweeps stream ~half the bytes of
     // the dense 64-wide band
@@ -138,7 +145,7 @@ struct DevicePlan {
     }
     void release() {
       release_part();
-      void* ptrs[] = {nt, ct, tt, pk, off};
+      void* ptrs[] = {nt, ct, tt, pk, off, pp, dd, TT};
       for (void* p : ptrs)
         if (p) cudaFree(p);
       *this = BandBlocks();

@@ -21,6 +21,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 #ifndef SPTRSV_LONG_UNROLL
 #define SPTRSV_LONG_UNROLL 8
 #endif
@@ -195,6 +197,109 @@ __device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
     }
   }
   publish_u64(a, i, acc.finish(a, i));
+  return true;
+}
+
+// The same rows, one per lane, but the warp polls them in lockstep rounds
+// instead of each lane spinning inside its own row loop. With per-lane spin
+// loops the lanes reconverge after every dependency group, so a row is only
+// published once its 31 ticket-mates are solved too: every hop of the level
+// chain then costs the slowest of ~250 dependencies plus one L2 round trip per
+// group of each row. Here, per round, every unfinished lane reloads the
+// not-yet-consumed part of its current window of kWin dependencies (all loads in
+// flight together), folds the ready prefix in column order (so x is bitwise
+// the same as the per-lane loop) and publishes its row the round its last
+// dependency arrives. The next window's indices and values are prefetched while
+// the current one is polled.
+template <int MODE>
+__device__ bool solve_rows_lanes(const RowsArgs& a, Poller& poll, int i, bool active, int lane) {
+  constexpr int kWin = 8;
+  Acc<MODE> acc;
+  int k = 0, end = 0, cnt = 0, c = 0;
+  int j[kWin], jn[kWin];
+  double v[kWin], vn[kWin];
+  if (active) {
+    acc.init(a, i);
+    k = a.rp[i];
+    end = a.rp[i + 1];
+    cnt = min(kWin, end - k);
+#pragma unroll
+    for (int q = 0; q < kWin; ++q) {
+      j[q] = q < cnt ? __ldg(a.ci + k + q) : 0;
+      v[q] = q < cnt ? __ldg(a.val + k + q) : 0.0;
+      const int kn = k + kWin + q;
+      jn[q] = kn < end ? __ldg(a.ci + kn) : 0;
+      vn[q] = kn < end ? __ldg(a.val + kn) : 0.0;
+    }
+    if (cnt == 0) {
+      publish_u64(a, i, acc.finish(a, i));
+      active = false;
+    }
+  }
+  int rounds = 0;
+  unsigned long long deadline = poll.deadline;
+  while (__any_sync(0xffffffffu, active)) {
+    bool progressed = false;
+    if (active) {
+      unsigned long long u[kWin];
+      bool rem[kWin];
+#pragma unroll
+      for (int q = 0; q < kWin; ++q) {
+        if (q >= c && q < cnt) {
+          const unsigned long long* p = slot_u64<MODE>(a, j[q], rem[q]);
+          u[q] = rem[q] ? ld_relaxed_sys_u64(p) : ld_relaxed_u64(p);
+        }
+      }
+      bool prefix = true;
+#pragma unroll
+      for (int q = 0; q < kWin; ++q) {
+        if (q >= c && q < cnt && prefix) {
+          if (u[q] == kNotReady) {
+            prefix = false;
+          } else {
+            acc.add(v[q], as_f64(u[q]));
+            if (rem[q]) ++poll.remote;  // one remote read per dependency, as the per-lane loop counts
+            ++c;
+            progressed = true;
+          }
+        }
+      }
+      if (c == cnt) {
+        k += kWin;
+        if (k >= end) {
+          publish_u64(a, i, acc.finish(a, i));
+          active = false;
+        } else {
+          cnt = min(kWin, end - k);
+          c = 0;
+#pragma unroll
+          for (int q = 0; q < kWin; ++q) {
+            j[q] = jn[q];
+            v[q] = vn[q];
+            const int kn = k + kWin + q;
+            jn[q] = kn < end ? __ldg(a.ci + kn) : 0;
+            vn[q] = kn < end ? __ldg(a.val + kn) : 0.0;
+          }
+        }
+      }
+      if (!progressed) ++poll.spins;
+    }
+    if (++rounds > a.spin_initial) {
+      if ((rounds & 63) == 0) {
+        int stop = 0;
+        if (lane == 0) {
+          stop = ld_relaxed_s32(a.abort_flag);
+          if (!stop && deadline && globaltimer_ns() > deadline) {
+            atomicExch(&a.status->code, 5);
+            atomicExch(a.abort_flag, 1);
+            stop = 1;
+          }
+        }
+        if (__shfl_sync(0xffffffffu, stop, 0)) return false;
+      }
+      if (!__any_sync(0xffffffffu, progressed)) __nanosleep(a.spin_max_ns);
+    }
+  }
   return true;
 }
 
@@ -480,9 +585,11 @@ __global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
     if (i >= a.n) is_long = true;  // a partial task of a split row (fast mode)
     else if (i >= 0 && a.coop_long) is_long = (a.rp[i + 1] - a.rp[i]) > a.long_deps;
     bool ok = true;
-    if (i >= 0 && !is_long) {
-      if constexpr (MODE == kModeLevel) ok = level_row_thread(a, poll, i);
-      else ok = solve_row_thread<MODE>(a, poll, i);
+    if constexpr (MODE != kModeLevel) {
+      if (a.lane_loop) ok = solve_rows_lanes<MODE>(a, poll, i, i >= 0 && !is_long, lane);
+      else if (i >= 0 && !is_long) ok = solve_row_thread<MODE>(a, poll, i);
+    } else if (i >= 0 && !is_long) {
+      ok = level_row_thread(a, poll, i);
     }
     unsigned longs = __ballot_sync(0xffffffffu, is_long);
     while (longs && __all_sync(0xffffffffu, ok)) {
@@ -511,6 +618,14 @@ __global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
 }
 
 }  // namespace
+
+int rows_lane_loop() {
+  static const int on = [] {
+    const char* e = std::getenv("SPTRSV_ROWS_LANELOOP");
+    return e ? std::atoi(e) : 1;
+  }();
+  return on;
+}
 
 int rows_blocks_per_sm(int mode) {
   int nb = 0;
