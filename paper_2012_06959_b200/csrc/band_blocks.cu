@@ -252,6 +252,118 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constan
   }
 }
 
+// ---- K1 / K3 with the band streamed by TMA ----------------------------------
+// The same sweep, but each warp's coefficient stream (its block's columns, one
+// contiguous 2 MB run for S = 4096) arrives in a shared-memory ring of kRing
+// chunks of kCw columns by bulk copies issued kRing chunks ahead, instead of
+// a register ring of kPf columns of 8-byte global loads (~1 us of HBM latency
+// against ~16 columns of sweep). Column j + 2's two entries per lane are read
+// from shared memory while column j is swept.
+constexpr int kCw = 8;                       // columns per chunk (4 KB)
+#ifndef SPTRSV_BB_RING
+#define SPTRSV_BB_RING 3
+#endif
+// chunks per warp ring: 3 (12 KB per warp) lets four CTAs share an SM, so the
+// 2,048 blocks of banded-8M run in one wave (16 warps per SM)
+constexpr int kRing = SPTRSV_BB_RING;
+constexpr int kChunkBytes = kCw * kW * 8;
+constexpr int kRingSmem = kBBWarps * (kRing * kChunkBytes + 8 * kRing);
+
+template <bool COUPLED>
+__global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_constant__ SweepArgs a) {
+  extern __shared__ __align__(128) unsigned char rsm[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int k = a.k_begin + blockIdx.x * kBBWarps + wq;
+  unsigned char* ring = rsm + wq * kRing * kChunkBytes;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(rsm + kBBWarps * kRing * kChunkBytes) + wq * kRing;
+  if (k >= a.k_end) return;
+  const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
+  const int ncol = (int)(s1 - s0), nch = (ncol + kCw - 1) / kCw;
+  auto issue = [&](int c) {  // lane 0: chunk c into its slot
+    if (c < nch) {
+      unsigned long long* bar = bars + c % kRing;
+      mbar_expect_tx(bar, kChunkBytes);
+      bulk_g2s(ring + (c % kRing) * kChunkBytes, a.coef + (size_t)(s0 + (long long)c * kCw) * kW, kChunkBytes, bar);
+    }
+  };
+  if (lane == 0) {
+    for (int q = 0; q < kRing; ++q) mbar_init(bars + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int c = 0; c < kRing; ++c) issue(c);
+  }
+  __syncwarp();
+  auto wait_chunk_ready = [&](int c) {
+    if (c < nch)
+      while (!mbar_try_wait(bars + c % kRing, (unsigned)(c / kRing) & 1u)) {
+      }
+  };
+  double acc[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const long long i = s0 + 2 * lane + s;
+    acc[s] = i < s1 ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
+    if (COUPLED && k > 0 && i < s1) {
+      const double* tp = a.tt + (size_t)(k - 1) * kW;
+      for (int q = 0; q < kW; ++q) {
+        const long long j = s0 - kW + q;
+        const long long d = i - j;
+        if (d >= 1 && d <= kW) acc[s] = __fma_rn(a.coef[(size_t)j * kW + d - 1], tp[q], acc[s]);
+      }
+    }
+  }
+  // column rel (relative to s0): the lane's two entries from the ring
+  auto sload = [&](int rel, double (&dst)[2]) {
+    const double* col = reinterpret_cast<const double*>(ring + ((rel / kCw) % kRing) * kChunkBytes) + (rel % kCw) * kW;
+    const int p = rel & (kW - 1);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) dst[s] = col[(2 * lane + s - p - 1) & (kW - 1)];
+  };
+  double nb[2];
+  double cf[4][2];  // column j at cf[j % 4] (4 divides the 64-column window), two columns ahead
+  wait_chunk_ready(0);
+  sload(0, cf[0]);
+  if (ncol > 1) sload(1, cf[1]);
+  for (int c0 = 0; c0 < ncol; c0 += kW) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const long long i = s0 + c0 + kW + 2 * lane + s;
+      nb[s] = i < s1 ? __dmul_rn(__ldg(a.b + i), __ldg(a.rdg + i)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const int rel = c0 + u;
+      const long long j = s0 + rel;
+      const int owner = u >> 1, os = u & 1;
+      if (u % kCw == 0 && rel > 0) {
+        // every read of the previous chunk has completed: refill its slot
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(rel / kCw - 1 + kRing);
+        }
+      }
+      if (u % kCw == kCw - 2) wait_chunk_ready(rel / kCw + 1);
+      if (rel + 2 < ncol) sload(rel + 2, cf[(u + 2) % 4]);
+      const double w0 = cf[u % 4][0], w1 = cf[u % 4][1];
+      const double xj = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
+      if (lane == owner && j < s1) {
+        if (COUPLED) {
+          a.out[j] = xj;
+        } else if (j >= s0 + a.S - kW) {
+          a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;
+        }
+      }
+      double v0 = acc[0], v1 = acc[1];
+      if (lane == owner) {
+        if (os) v1 = nb[1];
+        else v0 = nb[0];
+      }
+      acc[0] = __fma_rn(w0, xj, v0);
+      acc[1] = __fma_rn(w1, xj, v1);
+    }
+  }
+}
+
 // ---- K2: the tail recurrence (one CTA) -------------------------------------
 struct TailArgs {
   const double* nt;   // [nblk - 2] tails (blocks 1 .. nblk-2), K2 layout
@@ -658,10 +770,29 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   sa.k_end = ke;
   const int grid = (ke - kb + kBBWarps - 1) / kBBWarps;
   if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  static const bool tma_sweep = [] {
+    const char* v = std::getenv("SPTRSV_BB_TMA");
+    return !v || std::atoi(v) != 0;
+  }() && !kBBPacked;
+  if (tma_sweep) {
+    static std::atomic<unsigned long long> a1{0}, a3{0};
+    if ((e = set_max_dyn_smem(k_bb_sweep_tma<false>, kRingSmem, a1)) != cudaSuccess ||
+        (e = set_max_dyn_smem(k_bb_sweep_tma<true>, kRingSmem, a3)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
+  auto sweep = [&](bool coupled) {
+    if (tma_sweep) {
+      if (coupled) k_bb_sweep_tma<true><<<grid, 32 * kBBWarps, kRingSmem, s>>>(sa);
+      else k_bb_sweep_tma<false><<<grid, 32 * kBBWarps, kRingSmem, s>>>(sa);
+    } else {
+      if (coupled) k_bb_sweep<true><<<grid, 32 * kBBWarps, 0, s>>>(sa);
+      else k_bb_sweep<false><<<grid, 32 * kBBWarps, 0, s>>>(sa);
+    }
+    return cudaGetLastError();
+  };
   // K1: c tails
   sa.out = bblk.ct;
-  k_bb_sweep<false><<<grid, 32 * kBBWarps, 0, s>>>(sa);
-  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = sweep(false)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   // K2: tails
   TailArgs ta{};
   ta.nt = bblk.nt;
@@ -723,8 +854,7 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   // K3: x
   sa.tt = bblk.tt;
   sa.out = d_x;
-  k_bb_sweep<true><<<grid, 32 * kBBWarps, 0, s>>>(sa);
-  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  if ((e = sweep(true)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 2 + k2_launches;
   return SPTRSV_OK;
