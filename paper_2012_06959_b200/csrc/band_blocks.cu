@@ -364,6 +364,170 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
   }
 }
 
+// ---- K1 / K3 on the packed band, streamed by TMA -----------------------------
+// Only the stored entries (~32 of the 64 band positions per column on
+// banded-8M: 2.15 GB instead of 4.3 GB per sweep). A block's entries are one
+// contiguous run of `pk` (columns in order, rows ascending inside a column),
+// streamed through a ring of fixed 4 KB chunks that ignore column boundaries;
+// the presence masks and offsets of the current and next 64-column window sit
+// in shared memory (cp.async, a window ahead). A lane finds its entry of
+// column j by popcount of the mask below its bit. A chunk is refilled once
+// every entry in it lies below off[j] of the column being swept (read two
+// columns ago and already consumed).
+constexpr int kPkChunk = 256;  // doubles per chunk (2 KB)
+constexpr int kPkRing = 4;     // chunks per warp ring: entry r (relative to the block's base) at ring[r & 1023]
+constexpr int kPkRingMask = kPkRing * kPkChunk - 1;
+constexpr int kPkGroup = 8;    // columns per wait / refill point
+constexpr int kPkWarpBytes = kPkRing * kPkChunk * 8 + 2 * kW * 8 + 2 * kW * 4;
+constexpr int kPkSmem = kBBWarps * kPkWarpBytes + kBBWarps * kPkRing * 8;
+constexpr int kPkPad = 2 * kPkChunk;  // doubles allocated past the last entry (whole-chunk copies)
+
+template <bool COUPLED>
+__global__ void __launch_bounds__(32 * kBBWarps, 4) k_bb_sweep_pk(const __grid_constant__ SweepArgs a) {
+  extern __shared__ __align__(128) unsigned char psm[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int k = a.k_begin + blockIdx.x * kBBWarps + wq;
+  double* ring = reinterpret_cast<double*>(psm + wq * kPkWarpBytes);
+  unsigned long long* smask = reinterpret_cast<unsigned long long*>(ring + kPkRing * kPkChunk);  // [2][64]
+  int* soff = reinterpret_cast<int*>(smask + 2 * kW);                                          // [2][64]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(psm + kBBWarps * kPkWarpBytes) + wq * kPkRing;
+  if (k >= a.k_end) return;
+  const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
+  const int ncol = (int)(s1 - s0);
+  const int e1 = a.off[s1];
+  const int base = a.off[s0] & ~1;  // 16-byte aligned start of the block's entries
+  const int nq = (e1 - base + kPkChunk - 1) / kPkChunk;
+  auto issue = [&](int q) {  // lane 0
+    if (q < nq) {
+      unsigned long long* bar = bars + (q & (kPkRing - 1));
+      mbar_expect_tx(bar, kPkChunk * 8);
+      bulk_g2s(ring + (q & (kPkRing - 1)) * kPkChunk, a.pk + base + (long long)q * kPkChunk, kPkChunk * 8, bar);
+    }
+  };
+  // window w's masks and offsets into slot w & 1; columns past the block read
+  // as empty (mask 0, offset = the block's end)
+  auto stage = [&](int w) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = w * kW + h * 32 + lane, sl = (w & 1) * kW + h * 32 + lane;
+      if (c < ncol) {
+        cp_async8(&smask[sl], a.mask + s0 + c);
+        cp_async4(&soff[sl], a.off + s0 + c);
+      } else {
+        smask[sl] = 0ull;
+        soff[sl] = e1;
+      }
+    }
+    cp_async_commit();
+  };
+  if (lane == 0) {
+    for (int q = 0; q < kPkRing; ++q) mbar_init(bars + q, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int q = 0; q < kPkRing; ++q) issue(q);
+  }
+  stage(0);
+  stage(1);
+  cp_async_wait<0>();
+  __syncwarp();
+  int q_ready = -1, next_refill = kPkRing;
+  auto slot_of = [](int rel) { return ((rel >> 6) & 1) * kW + (rel & (kW - 1)); };
+  // make every chunk holding entries below off[rel_end] resident
+  auto ensure = [&](int rel_end) {
+    const int hi = soff[slot_of(rel_end)] - base;
+    if (hi > 0) {
+      const int qn = (hi - 1) / kPkChunk;
+      while (q_ready < qn) {
+        ++q_ready;
+        while (!mbar_try_wait(bars + (q_ready & (kPkRing - 1)), (unsigned)(q_ready / kPkRing) & 1u)) {
+        }
+      }
+    }
+  };
+  const int lb0 = 2 * lane - 1;  // bit of (row 2 lane + s, column at window position p) = (lb0 + s - p) & 63
+  auto load_col = [&](int rel, int p, double (&dst)[2]) {
+    const int sl = slot_of(rel);
+    const unsigned long long m = smask[sl];
+    const int o = soff[sl] - base;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int bit = (lb0 + s - p) & (kW - 1);
+      const int idx = o + __popcll(m & ((1ull << bit) - 1ull));
+      dst[s] = ((m >> bit) & 1ull) ? ring[idx & kPkRingMask] : 0.0;
+    }
+  };
+  double acc[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const long long i = s0 + 2 * lane + s;
+    acc[s] = i < s1 ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
+    if (COUPLED && k > 0 && i < s1) {
+      const double* tp = a.tt + (size_t)(k - 1) * kW;
+      for (int q = 0; q < kW; ++q) {
+        const long long j = s0 - kW + q;
+        const long long d = i - j;
+        if (d >= 1 && d <= kW) acc[s] = __fma_rn(a.coef[(size_t)j * kW + d - 1], tp[q], acc[s]);
+      }
+    }
+  }
+  double nb[2];
+  double cf[4][2];
+  ensure(2);
+  load_col(0, 0, cf[0]);
+  load_col(1, 1, cf[1]);
+  for (int c0 = 0; c0 < ncol; c0 += kW) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const long long i = s0 + c0 + kW + 2 * lane + s;
+      nb[s] = i < s1 ? __dmul_rn(__ldg(a.b + i), __ldg(a.rdg + i)) : 0.0;
+    }
+    if (c0 > 0) {
+      __syncwarp();
+      stage(c0 / kW + 1);  // into the previous window's slot
+    }
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const int rel = c0 + u;
+      const long long j = s0 + rel;
+      const int owner = u >> 1, os = u & 1;
+      if (u % kPkGroup == 0) {
+        if (u == kW - kPkGroup) {  // this group's lookahead reaches the next window
+          cp_async_wait<0>();
+          __syncwarp();
+        }
+        // refill the chunks wholly below off[rel] (read and consumed), then
+        // wait for those the group's lookahead (columns rel + 2 .. rel + 9) reads
+        const int qf = (soff[slot_of(rel)] - base) / kPkChunk;
+        if (next_refill - kPkRing < qf) {
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            for (int q = next_refill; q - kPkRing < qf; ++q) issue(q);
+          }
+          next_refill = qf + kPkRing;
+        }
+        ensure(rel + kPkGroup + 2);
+      }
+      load_col(rel + 2, (u + 2) & (kW - 1), cf[(u + 2) % 4]);
+      const double w0 = cf[u % 4][0], w1 = cf[u % 4][1];
+      const double xj = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
+      if (lane == owner && j < s1) {
+        if (COUPLED) {
+          a.out[j] = xj;
+        } else if (j >= s0 + a.S - kW) {
+          a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;
+        }
+      }
+      double v0 = acc[0], v1 = acc[1];
+      if (lane == owner) {
+        if (os) v1 = nb[1];
+        else v0 = nb[0];
+      }
+      acc[0] = __fma_rn(w0, xj, v0);
+      acc[1] = __fma_rn(w1, xj, v1);
+    }
+  }
+}
+
 // ---- K2: the tail recurrence (one CTA) -------------------------------------
 struct TailArgs {
   const double* nt;   // [nblk - 2] tails (blocks 1 .. nblk-2), K2 layout
@@ -689,12 +853,21 @@ int DevicePlan::build_band_blocks() {
     bblk.G = G;
     bblk.nsb = nsb;
   }
-  if (kBBPacked) {
+  // the packed band for the TMA sweeps (SPTRSV_BB_PK=1; measured slower than
+  // the dense band on banded-8M: 1.27 / 1.11 ms per sweep at 2.3 GB against
+  // 0.78 / 0.70 ms at 4.4 GB -- per column ~78 instructions and two dependent
+  // shared-memory loads per entry, so the sweep stops being HBM-bound)
+  static const bool pk_on = [] {
+    const char* v = std::getenv("SPTRSV_BB_PK");
+    return v && std::atoi(v) != 0;
+  }();
+  bblk.pk_tma = pk_on && !kBBPacked && noff + kPkPad < (1ll << 31);
+  if (kBBPacked || bblk.pk_tma) {
     // off = exclusive scan of the per-column entry counts; pk in row order
     int* cnt = nullptr;
     if ((e = al((void**)&cnt, sizeof(int) * (n + 1))) != cudaSuccess ||
         (e = al((void**)&bblk.off, sizeof(int) * (n + 1))) != cudaSuccess ||
-        (e = al((void**)&bblk.pk, sizeof(double) * std::max<long long>(noff, 1))) != cudaSuccess ||
+        (e = al((void**)&bblk.pk, sizeof(double) * (std::max<long long>(noff, 1) + kPkPad))) != cudaSuccess ||
         (e = cudaMemsetAsync(cnt, 0, sizeof(int) * (n + 1), stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
     const int g = (int)std::min<long long>((n + 255) / 256, 148 * 32);
@@ -774,14 +947,23 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
     const char* v = std::getenv("SPTRSV_BB_TMA");
     return !v || std::atoi(v) != 0;
   }() && !kBBPacked;
-  if (tma_sweep) {
+  const bool pk_sweep = bblk.pk_tma && bblk.pk && bblk.off;
+  if (pk_sweep) {
+    static std::atomic<unsigned long long> a1{0}, a3{0};
+    if ((e = set_max_dyn_smem(k_bb_sweep_pk<false>, kPkSmem, a1)) != cudaSuccess ||
+        (e = set_max_dyn_smem(k_bb_sweep_pk<true>, kPkSmem, a3)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  } else if (tma_sweep) {
     static std::atomic<unsigned long long> a1{0}, a3{0};
     if ((e = set_max_dyn_smem(k_bb_sweep_tma<false>, kRingSmem, a1)) != cudaSuccess ||
         (e = set_max_dyn_smem(k_bb_sweep_tma<true>, kRingSmem, a3)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
   auto sweep = [&](bool coupled) {
-    if (tma_sweep) {
+    if (pk_sweep) {
+      if (coupled) k_bb_sweep_pk<true><<<grid, 32 * kBBWarps, kPkSmem, s>>>(sa);
+      else k_bb_sweep_pk<false><<<grid, 32 * kBBWarps, kPkSmem, s>>>(sa);
+    } else if (tma_sweep) {
       if (coupled) k_bb_sweep_tma<true><<<grid, 32 * kBBWarps, kRingSmem, s>>>(sa);
       else k_bb_sweep_tma<false><<<grid, 32 * kBBWarps, kRingSmem, s>>>(sa);
     } else {

@@ -127,6 +127,7 @@ struct DevicePlan {
     // the dense 64-wide band
     double* pk = nullptr;
     int* off = nullptr;  // [n_pad + 1]
+    bool pk_tma = false;  // the sweeps stream pk (k_bb_sweep_pk)
     // PE partition (set_partition with contiguous slabs on block boundaries):
     // this PE sweeps blocks [k0, k1) and runs their part of the tail chain;
     // the chain enters from the previous PE's last tail, read from its slot
