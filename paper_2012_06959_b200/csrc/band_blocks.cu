@@ -679,6 +679,7 @@ __device__ __forceinline__ int k2_index(int r, int m) {  // K2 layout of element
 }
 
 constexpr int kProdSmem = 2 * kW * kW * 8;
+constexpr int kMinSuperSteps = 64;  // shorter chains run as one sequential chain
 
 // setup: pp[g] = M_{s1-1} ... M_{s0} for superblock g's steps [s0, s1)
 __global__ void __launch_bounds__(256) k_bb_prod(const double* __restrict__ nt, int nsteps, int G,
@@ -717,6 +718,12 @@ struct TailChainArgs {
   double* out_all;      // t after step s -> out_all + s * 64 (null: not kept)
   double* out_last;     // t after CTA g's last step -> out_last + g * 64 (null: not kept)
   int nsteps, G;        // CTA g runs steps [g G, min(nsteps, (g + 1) G))
+  // the superblock chain of a PE (K2b, one CTA): its incoming t is the previous
+  // PE's last tail, polled from that PE's slot (value-is-flag, system scope;
+  // null: init0), kept at init_out; its final t goes to this PE's slot
+  const unsigned long long* prev_slot;
+  unsigned long long* my_slot;
+  double* init_out;
   DeviceStatus* status;
   int* abort_flag;
   unsigned long long timeout_ns;
@@ -740,7 +747,22 @@ __global__ void __launch_bounds__(160, 1) k_bb_chain(const __grid_constant__ Tai
   const unsigned long long deadline = a.timeout_ns ? globaltimer_ns() + a.timeout_ns : 0;
   if (tid < kW) {
     const double* in = g == 0 ? a.init0 : (a.init ? a.init + (size_t)(g - 1) * kW : nullptr);
-    tb[kW + tid] = in ? in[tid] : 0.0;  // step s reads buffer (s - s0 + 1) & 1
+    double t0 = in ? in[tid] : 0.0;
+    if (g == 0 && a.prev_slot) {
+      unsigned long long u = ld_relaxed_sys_u64(a.prev_slot + tid);
+      int polls = 0;
+      while (u == kNotReady) {
+        if ((++polls & 1023) == 0 && ((deadline && globaltimer_ns() > deadline) || ld_relaxed_s32(a.abort_flag))) {
+          atomicExch(&a.status->code, 5);
+          atomicExch(a.abort_flag, 1);
+          break;
+        }
+        u = ld_relaxed_sys_u64(a.prev_slot + tid);
+      }
+      t0 = __longlong_as_double((long long)u);
+    }
+    if (g == 0 && a.init_out) a.init_out[tid] = t0;
+    tb[kW + tid] = t0;  // step s reads buffer (s - s0 + 1) & 1
   }
   __syncthreads();
   if (tid >= 128) {
@@ -799,6 +821,8 @@ __global__ void __launch_bounds__(160, 1) k_bb_chain(const __grid_constant__ Tai
       tb[cur * kW + r] = t;
       if (a.out_all) a.out_all[(size_t)st * kW + r] = t;
       if (a.out_last && st == s1 - 1) a.out_last[(size_t)g * kW + r] = t;
+      if (a.my_slot && st == s1 - 1 && !ld_relaxed_s32(a.abort_flag))
+        st_relaxed_sys_u64(a.my_slot + r, (unsigned long long)__double_as_longlong(t));
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (tid == 0) st_release_cta(ctl, st - s0 + 1);
@@ -806,6 +830,39 @@ __global__ void __launch_bounds__(160, 1) k_bb_chain(const __grid_constant__ Tai
 }
 
 }  // namespace
+
+// Superblocks over chain steps [s_first, s_first + nsteps) (step s computes
+// t_{s+1}): G ~ sqrt(nsteps) steps each, their coupling-tail products pp.
+// SPTRSV_BB_SUPER=0 keeps the single sequential chain (k_bb_tail).
+int DevicePlan::build_superblocks(int s_first, int nsteps, cudaStream_t st) {
+  static const bool super_on = [] {
+    const char* v = std::getenv("SPTRSV_BB_SUPER");
+    return !v || std::atoi(v) != 0;
+  }();
+  cudaError_t e;
+  for (double** p : {&bblk.pp, &bblk.dd, &bblk.TT})
+    if (*p) cudaFree(*p), *p = nullptr;
+  bblk.G = bblk.nsb = 0;
+  bblk.sb_first = s_first;
+  bblk.sb_steps = nsteps;
+  if (!super_on || nsteps < kMinSuperSteps) return SPTRSV_OK;
+  int G = 1;
+  while ((long long)G * G < nsteps) ++G;
+  const int nsb = (nsteps + G - 1) / G;
+  auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
+  if ((e = al((void**)&bblk.pp, (size_t)nsb * kTailBytes)) != cudaSuccess ||
+      (e = al((void**)&bblk.dd, sizeof(double) * nsb * kW)) != cudaSuccess ||
+      (e = al((void**)&bblk.TT, sizeof(double) * nsb * kW)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  static std::atomic<unsigned long long> pattr{0};
+  if ((e = set_max_dyn_smem(k_bb_prod, kProdSmem, pattr)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  k_bb_prod<<<nsb, 256, kProdSmem, st>>>(bblk.nt + (size_t)s_first * (kTailBytes / 8), nsteps, G, bblk.pp);
+  if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  bblk.G = G;
+  bblk.nsb = nsb;
+  return SPTRSV_OK;
+}
 
 int DevicePlan::build_band_blocks() {
   cudaError_t e;
@@ -830,28 +887,12 @@ int DevicePlan::build_band_blocks() {
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
-  // the tail chain by superblocks of G ~ sqrt(steps) steps (SPTRSV_BB_SUPER=0: one sequential chain)
-  static const bool super_on = [] {
-    const char* v = std::getenv("SPTRSV_BB_SUPER");
-    return !v || std::atoi(v) != 0;
-  }();
-  const int nsteps = nblk - 2;
-  if (super_on && nsteps >= 64) {
-    int G = 1;
-    while ((long long)G * G < nsteps) ++G;
-    const int nsb = (nsteps + G - 1) / G;
-    if ((e = al((void**)&bblk.pp, (size_t)nsb * kTailBytes)) != cudaSuccess ||
-        (e = al((void**)&bblk.dd, sizeof(double) * nsb * kW)) != cudaSuccess ||
-        (e = al((void**)&bblk.TT, sizeof(double) * nsb * kW)) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    static std::atomic<unsigned long long> pattr{0};
-    if ((e = set_max_dyn_smem(k_bb_prod, kProdSmem, pattr)) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    k_bb_prod<<<nsb, 256, kProdSmem, stream>>>(bblk.nt, nsteps, G, bblk.pp);
-    if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    bblk.G = G;
-    bblk.nsb = nsb;
+  // the tail chain by superblocks (one PE: every step; a PE of a partition
+  // rebuilds them over its own steps, see solve_band_blocks)
+  if (nblk - 2 >= kMinSuperSteps) {
+    const int rc = build_superblocks(0, nblk - 2, stream);
+    if (rc != SPTRSV_OK) return rc;
+    if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
   // the packed band for the TMA sweeps (SPTRSV_BB_PK=1; measured slower than
   // the dense band on banded-8M: 1.27 / 1.11 ms per sweep at 2.3 GB against
@@ -989,27 +1030,36 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   ta.abort_flag = abort_flag;
   ta.timeout_ns = (unsigned long long)(opt.timeout_s * 1e9);
   int k2_launches = 1;
-  if (!bblk.part && bblk.G > 0) {
+  // this PE's chain steps: t_k for k = kb2 .. klast from t_{kb2 - 1}
+  const int kb2 = kb == 0 ? 1 : kb, klast = std::min(ke, bblk.nblk - 1) - 1;
+  const int my_steps = klast - kb2 + 1;
+  if (my_steps >= kMinSuperSteps && (bblk.sb_first != kb2 - 1 || bblk.sb_steps != my_steps)) {
+    const int rc = build_superblocks(kb2 - 1, my_steps, s);  // a partition changed this PE's steps
+    if (rc != SPTRSV_OK) return rc;
+  }
+  if (my_steps >= kMinSuperSteps && bblk.G > 0) {
     // K2a / K2b / K2c: the chain by superblocks (see k_bb_chain)
     static std::atomic<unsigned long long> cattr{0};
     if ((e = set_max_dyn_smem(k_bb_chain, TSmem::kTotal, cattr)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    const int nsteps = bblk.nblk - 2;
     TailChainArgs ca{};
     ca.status = status;
     ca.abort_flag = abort_flag;
     ca.timeout_ns = ta.timeout_ns;
-    ca.mat = bblk.nt;
-    ca.cv = bblk.ct + kW;
+    ca.mat = bblk.nt + (size_t)(kb2 - 1) * (kTailBytes / 8);  // M_k at nt[k - 1]
+    ca.cv = bblk.ct + (size_t)kb2 * kW;                         // c_k
     ca.out_last = bblk.dd;
-    ca.nsteps = nsteps;
+    ca.nsteps = my_steps;
     ca.G = bblk.G;
     k_bb_chain<<<bblk.nsb, 160, TSmem::kTotal, s>>>(ca);  // d_g
     if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
     TailChainArgs cb = ca;
     cb.mat = bblk.pp;
     cb.cv = bblk.dd;
-    cb.init0 = bblk.ct;  // t_0 = c_0
+    cb.init0 = kb == 0 ? bblk.ct : nullptr;  // t_0 = c_0, or the previous PE's last tail
+    cb.prev_slot = ta.prev_slot;
+    cb.my_slot = ta.my_slot;
+    cb.init_out = bblk.tt + (size_t)(kb2 - 1) * kW;
     cb.out_last = nullptr;
     cb.out_all = bblk.TT;
     cb.nsteps = bblk.nsb;
@@ -1017,14 +1067,12 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
     k_bb_chain<<<1, 160, TSmem::kTotal, s>>>(cb);  // T_g
     if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
     TailChainArgs cc = ca;
-    cc.init0 = bblk.ct;
+    cc.init0 = bblk.tt + (size_t)(kb2 - 1) * kW;
     cc.init = bblk.TT;
     cc.out_last = nullptr;
-    cc.out_all = bblk.tt + kW;
+    cc.out_all = bblk.tt + (size_t)kb2 * kW;
     k_bb_chain<<<bblk.nsb, 160, TSmem::kTotal, s>>>(cc);  // every t_k
     if ((e = cudaGetLastError()) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    if ((e = cudaMemcpyAsync(bblk.tt, bblk.ct, kW * sizeof(double), cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
-      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
     k2_launches = 3;
   } else {
     static std::atomic<unsigned long long> attr{0};

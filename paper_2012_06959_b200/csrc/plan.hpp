@@ -119,6 +119,7 @@ struct DevicePlan {
     // product of superblock g's coupling tails (built once per plan); per solve
     // dd[g] = g's chain run from zero, TT[g] = t at the end of g
     int G = 0, nsb = 0;
+    int sb_first = -1, sb_steps = 0;  // the chain steps the superblocks cover
     double* pp = nullptr;  // [nsb] 64 x 64, K2 layout
     double* dd = nullptr;  // [nsb][64]
     double* TT = nullptr;  // [nsb][64]
@@ -153,6 +154,7 @@ struct DevicePlan {
     }
   } bblk;
   int build_band_blocks();
+  int build_superblocks(int s_first, int nsteps, cudaStream_t st);
   int set_band_partition(const int32_t* owner, int pes, int my_pe);
   int solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s);
   int solve_push(const double* d_b, double* d_x, cudaStream_t s);

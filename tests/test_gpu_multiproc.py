@@ -136,14 +136,15 @@ def _worker_band(rank, world, port, out_q, n):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [6400, 6000])
+@pytest.mark.parametrize("n", [6400, 6000, 25600])
 def test_two_processes_band_executor(n):
     """Band blocks over two processes. n = 6400: 3200-row slabs on the 64-row
     block grid, so each rank sweeps its blocks and rank 1's stretch of the
     tail chain starts from rank 0's last tail (read from rank 0's IPC-mapped
     slot). n = 6000: slabs off the grid, so the DistributedSolver keeps the
     band executor replicated (every rank solves the whole system and keeps
-    its rows) instead of degrading to the component pool."""
+    its rows) instead of degrading to the component pool. n = 25600: 200
+    blocks per rank, so rank 1's superblock chain polls rank 0's slot."""
     torch = pytest.importorskip("torch")
     import torch.multiprocessing as mp
 

@@ -84,13 +84,15 @@ def test_dropin_n_pes_keeps_the_wavefront(n_pes, precision):
 
 
 @pytest.mark.parametrize("n_pes", [2, 3, 4])
-@pytest.mark.parametrize("n", [7680, 7710])
+@pytest.mark.parametrize("n", [7680, 7710, 40000])
 def test_dropin_n_pes_band_blocks_partitioned(n_pes, n):
     """Fast mode, banded L, contiguous slabs on 64-row block boundaries: one
     band-block plan per PE (its blocks' sweeps and its stretch of the tail
     chain, the chain handed PE to PE through a 64-value slot); x within 1e-12
     of the oracle over repeated solves (slot halves alternate by parity).
-    n = 7710: the last PE's last block is partial."""
+    n = 7710: the last PE's last block is partial. n = 40000: every PE has
+    >= 64 chain steps, so each runs its stretch by superblocks (K2a/b/c) and
+    its superblock chain enters from the previous PE's slot."""
     l = synth.banded(n, 64, 0.5, 6)
     plan = sp.nnz_block_partition(np.ones(n), n_pes, 64)
     cfg = sp.SolverConfig(engine=sp.Engine.PARTITIONED_READ_ONLY, n_pes=n_pes, precision="fast")
