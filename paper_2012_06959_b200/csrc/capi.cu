@@ -232,6 +232,11 @@ int DevicePlan::run_levels(const int* grid, bool precomputed) {
 }
 
 int DevicePlan::rows_grid(int mode) const {
+  static const int forced = [] {  // SPTRSV_ROWS_GRID: fixed block count (A/B)
+    const char* v = std::getenv("SPTRSV_ROWS_GRID");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (forced > 0) return forced;
   int per_sm = rows_blocks_per_sm(mode);
   if (per_sm < 1) per_sm = 1;
   long long want = (order_len + 255) / 256;

@@ -24,7 +24,7 @@
 #include <cstdlib>
 
 #ifndef SPTRSV_LONG_UNROLL
-#define SPTRSV_LONG_UNROLL 8
+#define SPTRSV_LONG_UNROLL 4
 #endif
 
 namespace sptrsv {
@@ -213,7 +213,10 @@ __device__ bool solve_row_thread(const RowsArgs& a, Poller& poll, int i) {
 // the current one is polled.
 template <int MODE>
 __device__ bool solve_rows_lanes(const RowsArgs& a, Poller& poll, int i, bool active, int lane) {
-  constexpr int kWin = 8;
+#ifndef SPTRSV_ROWS_WIN
+#define SPTRSV_ROWS_WIN 4
+#endif
+  constexpr int kWin = SPTRSV_ROWS_WIN;
   Acc<MODE> acc;
   int k = 0, end = 0, cnt = 0, c = 0;
   int j[kWin], jn[kWin];
@@ -558,8 +561,18 @@ __device__ bool level_row_warp(const RowsArgs& a, Poller& poll, int i, int lane)
   return true;
 }
 
+// resident blocks per SM the register budget is sized for (SPTRSV_ROWS_MINB):
+// two blocks (2,368 warps in the pool) with 4-entry windows and 4 rounds of
+// long-row loads in flight measured best on rmat-4M (fast 3.33 -> 3.13 ms,
+// exact 10.4 -> 9.9 ms); one block with 8 / 8: 3.33 ms; three blocks: 3.46 ms;
+// four blocks (64 registers, spilling): 5.2 ms; fewer warps (SPTRSV_ROWS_GRID
+// 111 / 74 / 37 blocks of one per SM): 3.64 / 4.37 / 6.91 ms
+#ifndef SPTRSV_ROWS_MINB
+#define SPTRSV_ROWS_MINB 2
+#endif
+
 template <int MODE>
-__global__ void __launch_bounds__(256) k_rows(RowsArgs a_in) {
+__global__ void __launch_bounds__(256, SPTRSV_ROWS_MINB) k_rows(RowsArgs a_in) {
   const int lane = threadIdx.x & 31;
   // the PE this block works for: its slice of the order and its ticket pool
   RowsArgs a = a_in;
