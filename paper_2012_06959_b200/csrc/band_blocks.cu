@@ -84,8 +84,17 @@ __global__ void k_bb_pack(const double* __restrict__ coef, const unsigned long l
 // (m = 32h + 2i + e), r = tail row.
 constexpr int kNtSmem = 2 * kW * kW * 8;  // two 64-column chunks of the band
 
+// Coupling reach (fast mode): a row whose response to every coupling value
+// is <= kReachTau (2^-64) takes x = c, since the dropped N t is below
+// 64 * 2^-64 |t| (~3.5e-18 of the tail's magnitude, far under the sweep's own
+// rounding); reach[k] = 1 + the last row of block k above it, so K3 sweeps
+// rows [0, reach[k]) of the block (rounded up to whole 64-column windows:
+// the sweep writes every column of a window it enters) and K1's c stands
+// beyond.
+constexpr double kReachTau = 5.421010862427522e-20;  // 2^-64
+
 __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef, long long n, int S, int nblk,
-                                                 double* __restrict__ nt) {
+                                                 double* __restrict__ nt, int* __restrict__ reach) {
   extern __shared__ __align__(16) double cs_raw[];
   double (*cs)[kW][kW] = reinterpret_cast<double (*)[kW][kW]>(cs_raw);
   // blocks 1 .. nblk - 2: block 0 has no coupling and the last block's tail
@@ -105,6 +114,7 @@ __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef
   };
   stage(0, 0);
   __syncthreads();
+  int last = 0;  // 1 + the last row of the block whose response to coupling m exceeds kReachTau
   for (int c = 0; c < nchunk; ++c) {
     if (c + 1 < nchunk) stage(c + 1, (c + 1) & 1);
 #pragma unroll
@@ -112,6 +122,8 @@ __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef
       const long long j = s0 - kW + (long long)c * kW + u;
       // coupling column s0 - 64 + m has response 1 in lane m, 0 elsewhere
       const double nj = c == 0 ? (u == m ? 1.0 : 0.0) : acc[u];
+      // (NaN / inf responses compare false: keep the whole block then)
+      if (c > 0 && j < n && !(fabs(nj) <= kReachTau)) last = (int)(j - s0) + 1;
       if (c > 0 && j >= s0 + S - kW && j < n) {
         const int r = (int)(j - (s0 + S - kW)), i = (m & 31) >> 1, e = m & 1;
         nt[(size_t)(k - 1) * (kTailBytes / 8) + ((h * 16 + i) * kW + r) * 2 + e] = nj;
@@ -123,6 +135,7 @@ __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef
     }
     __syncthreads();
   }
+  if (reach) atomicMax(reach + k, last);
 }
 
 // ---- K1 / K3: one warp per block, the band window sweep --------------------
@@ -135,6 +148,8 @@ struct SweepArgs {
   const double* rdg;
   const double* tt;    // K3: t_k = x of block k's tail rows, [nblk][64] (null in K1)
   double* out;         // K1: c tails [nblk][64]; K3: x
+  double* x_all;       // K1: also c of every row into x (coupling reach in use), else null
+  const int* reach;    // K3: rows of block k the coupling reaches (null: all)
   long long n;
   int S, nblk;
   int k_begin, k_end;  // the blocks of this PE (all blocks without a partition)
@@ -165,7 +180,7 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constan
   }
   // next window's b * rd of the lane's rows (one iteration ahead)
   double nb[2];
-  const int ncol = (int)(s1 - s0);
+  const int ncol = (int)(COUPLED && a.reach ? std::min<long long>(s1 - s0, (a.reach[k] + kW - 1) / kW * kW) : s1 - s0);
   // coefficient register ring: column j's two entries of this lane, kPf columns ahead
   double cf[kPf][2];
   // packed: the presence masks and offsets of windows w .. w + 2 staged in
@@ -238,7 +253,9 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep(const __grid_constan
       if (lane == owner && j < s1) {
         if (COUPLED) {
           a.out[j] = xj;
-        } else if (j >= s0 + a.S - kW) {
+        } else {
+          if (a.x_all) a.x_all[j] = xj;
+          if (j >= s0 + a.S - kW)
           a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;  // c of the tail rows
         }
       }
@@ -278,7 +295,8 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(rsm + kBBWarps * kRing * kChunkBytes) + wq * kRing;
   if (k >= a.k_end) return;
   const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
-  const int ncol = (int)(s1 - s0), nch = (ncol + kCw - 1) / kCw;
+  const int ncol = (int)(COUPLED && a.reach ? std::min<long long>(s1 - s0, (a.reach[k] + kW - 1) / kW * kW) : s1 - s0);
+  const int nch = (ncol + kCw - 1) / kCw;
   auto issue = [&](int c) {  // lane 0: chunk c into its slot
     if (c < nch) {
       unsigned long long* bar = bars + c % kRing;
@@ -349,7 +367,9 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
       if (lane == owner && j < s1) {
         if (COUPLED) {
           a.out[j] = xj;
-        } else if (j >= s0 + a.S - kW) {
+        } else {
+          if (a.x_all) a.x_all[j] = xj;
+          if (j >= s0 + a.S - kW)
           a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;
         }
       }
@@ -393,8 +413,8 @@ __global__ void __launch_bounds__(32 * kBBWarps, 4) k_bb_sweep_pk(const __grid_c
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(psm + kBBWarps * kPkWarpBytes) + wq * kPkRing;
   if (k >= a.k_end) return;
   const long long s0 = (long long)k * a.S, s1 = std::min<long long>(s0 + a.S, a.n);
-  const int ncol = (int)(s1 - s0);
-  const int e1 = a.off[s1];
+  const int ncol = (int)(COUPLED && a.reach ? std::min<long long>(s1 - s0, (a.reach[k] + kW - 1) / kW * kW) : s1 - s0);
+  const int e1 = a.off[s0 + ncol];
   const int base = a.off[s0] & ~1;  // 16-byte aligned start of the block's entries
   const int nq = (e1 - base + kPkChunk - 1) / kPkChunk;
   auto issue = [&](int q) {  // lane 0
@@ -513,7 +533,9 @@ __global__ void __launch_bounds__(32 * kBBWarps, 4) k_bb_sweep_pk(const __grid_c
       if (lane == owner && j < s1) {
         if (COUPLED) {
           a.out[j] = xj;
-        } else if (j >= s0 + a.S - kW) {
+        } else {
+          if (a.x_all) a.x_all[j] = xj;
+          if (j >= s0 + a.S - kW)
           a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;
         }
       }
@@ -879,11 +901,25 @@ int DevicePlan::build_band_blocks() {
       (e = cudaMemsetAsync(bblk.ct, 0, sizeof(double) * nblk * kW, stream)) != cudaSuccess ||
       (e = cudaMemsetAsync(bblk.nt, 0, (size_t)std::max(nblk - 1, 1) * kTailBytes, stream)) != cudaSuccess)
     return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  // coupling reach per block (SPTRSV_BB_REACH=0: K3 sweeps every row): block 0
+  // has no coupling (x = c), the last block is swept whole, the others are
+  // raised by k_bb_ntail
+  static const bool reach_on = [] {
+    const char* v = std::getenv("SPTRSV_BB_REACH");
+    return !v || std::atoi(v) != 0;
+  }();
+  if (reach_on) {
+    std::vector<int> r0(nblk, 0);
+    r0[nblk - 1] = (int)S;
+    if ((e = al((void**)&bblk.reach, sizeof(int) * nblk)) != cudaSuccess ||
+        (e = cudaMemcpy(bblk.reach, r0.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  }
   if (nblk > 2) {
     static std::atomic<unsigned long long> attr{0};
     if ((e = set_max_dyn_smem(k_bb_ntail, kNtSmem, attr)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    k_bb_ntail<<<nblk - 2, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt);
+    k_bb_ntail<<<nblk - 2, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt, bblk.reach);
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
@@ -1013,8 +1049,9 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
     }
     return cudaGetLastError();
   };
-  // K1: c tails
+  // K1: c tails (and, with the coupling reach, c of every row into x)
   sa.out = bblk.ct;
+  sa.x_all = bblk.reach ? d_x : nullptr;
   if ((e = sweep(false)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   // K2: tails
   TailArgs ta{};
@@ -1084,6 +1121,8 @@ int DevicePlan::solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s
   // K3: x
   sa.tt = bblk.tt;
   sa.out = d_x;
+  sa.x_all = nullptr;
+  sa.reach = bblk.reach;
   if ((e = sweep(true)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   if ((e = cudaEventRecord(evk1, s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   launches = 2 + k2_launches;

@@ -129,6 +129,7 @@ struct DevicePlan {
     double* pk = nullptr;
     int* off = nullptr;  // [n_pad + 1]
     bool pk_tma = false;  // the sweeps stream pk (k_bb_sweep_pk)
+    int* reach = nullptr;  // [nblk] rows of each block the coupling reaches (K3 sweeps only those)
     // PE partition (set_partition with contiguous slabs on block boundaries):
     // this PE sweeps blocks [k0, k1) and runs their part of the tail chain;
     // the chain enters from the previous PE's last tail, read from its slot
@@ -147,13 +148,15 @@ struct DevicePlan {
     }
     void release() {
       release_part();
-      void* ptrs[] = {nt, ct, tt, pk, off, pp, dd, TT};
+      void* ptrs[] = {nt, ct, tt, pk, off, pp, dd, TT, reach};
       for (void* p : ptrs)
         if (p) cudaFree(p);
       *this = BandBlocks();
     }
   } bblk;
   int build_band_blocks();
+  int stencil_groups(cudaStream_t s);  // stencil.cu: 1 when the band groups are in use
+  int group_tasks_used = 0;            // tasks of the last stencil solve's band groups (0: none)
   int build_superblocks(int s_first, int nsteps, cudaStream_t st);
   int set_band_partition(const int32_t* owner, int pes, int my_pe);
   int solve_band_blocks(const double* d_b, double* d_x, cudaStream_t s);

@@ -181,10 +181,24 @@ struct alignas(64) StArgs {
   int* bd_done;
   unsigned bd_epoch;
   long long n_copy;  // elements of one right-hand side (rd index = i % n_copy)
+  // band groups (fast mode, one PE, one right-hand side; null otherwise):
+  // task t solves band tband[t] >= 0, or is the halo task of a group
+  // (tband[t] = -band - 1): that band solved from a zero row above it, its x
+  // discarded, only its bottom row handed to the group's first band
+  const int* tband;
+  int n_bands;  // bands of the grid (the host-copy flags' range)
 };
-// task t has a band below it in the same right-hand side
+__device__ __forceinline__ int st_band(const StArgs& a, int t) {
+  if (!a.tband) return t;
+  const int b = a.tband[t];
+  return b >= 0 ? b : -b - 1;
+}
+__device__ __forceinline__ bool st_halo(const StArgs& a, int t) { return a.tband && a.tband[t] < 0; }
+// task t starts from a zero row above (the first band of a right-hand side or a group's halo task)
+__device__ __forceinline__ bool st_no_above(const StArgs& a, int t) { return t % a.bands == 0 || st_halo(a, t); }
+// task t has a band below it in the same right-hand side / group
 __device__ __forceinline__ bool st_has_below(const StArgs& a, int t) {
-  return t + 1 < a.n_tasks && (t + 1) % a.bands != 0;
+  return t + 1 < a.n_tasks && !st_no_above(a, t + 1);
 }
 constexpr int kStProbeFirst = 64, kStProbeChunks = 64;
 template <bool DG>
@@ -371,7 +385,7 @@ struct StBlk {
 __device__ __forceinline__ int st_b_flag_band(const StArgs& a, int t) {
   if (a.b_chunk_max <= 0) return t;
   for (int t0b = 0, w = 1;; t0b += w, w = min(2 * w, a.b_chunk_max))
-    if (t < t0b + w) return min(a.n_tasks, t0b + w) - 1;
+    if (t < t0b + w) return min(a.n_bands, t0b + w) - 1;
 }
 
 template <bool EXACT, bool DG, bool BD = false>
@@ -381,9 +395,10 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   constexpr int NB = S::kSlots;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
-  const int y0 = t * kStBand + kStR * lane;
-  const unsigned char* tstream = a.stream + (size_t)(t % a.bands) * a.steps * S::kStep;
-  const bool b_tma = kStBTma && t < a.b_tma_bands;
+  const int band = st_band(a, t);
+  const int y0 = band * kStBand + kStR * lane;
+  const unsigned char* tstream = a.stream + (size_t)(band % a.bands) * a.steps * S::kStep;
+  const bool b_tma = kStBTma && band < a.b_tma_bands;
   bool ok = true;
   // chunk c: its coefficient block and, per lane and grid row, the b segment of
   // column blocks [c*G - lane, c*G - lane + G) clipped to the grid
@@ -410,7 +425,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
         bulk_g2s(smem + S::kCoef + slot * S::kCoefChunk, tstream + (size_t)c * S::kCoefChunk, S::kCoefChunk,
                  &bars[slot]);
       }
-      if (b_tma) tma_load_4d(smem + S::kB + slot * S::kBChunk, &a.bmap, c * kStG * kStC, 0, 0, t, &bars[slot]);
+      if (b_tma) tma_load_4d(smem + S::kB + slot * S::kBChunk, &a.bmap, c * kStG * kStC, 0, 0, band, &bars[slot]);
     }
     double2* dst = reinterpret_cast<double2*>(smem + S::kB + slot * S::kBChunk);
 #pragma unroll
@@ -450,7 +465,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // for the host copies of b)
   if (BD) {
     int polls = 0;
-    while ((int)(ld_acquire_gpu_u32(a.bdflag + t) - a.bd_epoch) < 0) {
+    while ((int)(ld_acquire_gpu_u32(a.bdflag + band) - a.bd_epoch) < 0) {
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
       if (!__all_sync(0xffffffffu, ok)) {
         abort_task(a, ctl, lane);
@@ -464,7 +479,7 @@ __device__ void loader(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // overlapped host solve: this band's b may still be on its way over PCIe
   if (a.bflag && !BD) {
     int polls = 0;
-    const int flag_band = st_b_flag_band(a, t);
+    const int flag_band = st_b_flag_band(a, band);
     while ((int)(ld_acquire_sys_u32(a.bflag + flag_band) - a.epoch) < 0) {
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) ok = false;
       if (!__all_sync(0xffffffffu, ok)) {
@@ -522,7 +537,7 @@ __device__ void poller(const StArgs& a, unsigned char* smem, int* ctl, int t, in
                        bool above_in_cluster) {
   using S = StSmem<EXACT>;
   if (above_in_cluster) return;  // the band above pushes into our inbox itself
-  if (t % a.bands == 0) {
+  if (st_no_above(a, t)) {
     // no band above: the top grid row's "row above" is zero, so the compute
     // warp's lane 0 reads zeros from the inbox like any other band (no
     // per-step has_above select)
@@ -680,7 +695,9 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   using S = StSmem<EXACT>;
   HandDown<EXACT, PART> hd(a, smem, ctl, t, crank, below_in_cluster);
   const int nchunks = a.steps / kStG, nblk = a.nx / kStC;
-  const int y0 = t * kStBand + kStR * lane;
+  const int band = st_band(a, t);
+  const bool halo = st_halo(a, t);  // a group's halo band: x is not stored
+  const int y0 = band * kStBand + kStR * lane;
   // this band's row of the other mailbox half (last read by the previous
   // solve, which is complete) is reset here for the next solve: no memset
   // node between solves
@@ -688,7 +705,7 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     ulonglong2* row = reinterpret_cast<ulonglong2*>(a.mbox_next + (size_t)t * a.nx);
     for (int w = lane; w < a.nx / 2; w += kStLanes) row[w] = make_ulonglong2(kStNotReady, kStNotReady);
   }
-  const bool x_tma = kStBTma && t < a.x_tma_bands;
+  const bool x_tma = kStBTma && band < a.x_tma_bands;
   // TMA stores stay in flight: after chunk c only the kStStoreDepth most recent
   // stores may still be reading their slots, so chunks <= c - kStStoreDepth
   // are handed back (edge chunks are stored synchronously and drain the rest)
@@ -719,6 +736,8 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
     if (true) {
     } else
 #endif
+    if (halo) {
+    } else
     // interior chunk (every lane's blocks inside the row): one TMA store of
     // the whole slot; edge chunks element by element (the skewed box would
     // write padding into neighbouring rows there)
@@ -726,7 +745,7 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
       async_store = true;
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the compute warp's STS -> async proxy
-        tma_store_4d(&a.xmap, c * kStG * kStC, 0, 0, t, slot);
+        tma_store_4d(&a.xmap, c * kStG * kStC, 0, 0, band, slot);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStStoreDepth) : "memory");
       }
@@ -768,15 +787,15 @@ __device__ void storer(const StArgs& a, unsigned char* smem, int* ctl, int t, in
   // overlapped host solve: band t's x may now be copied to the host. Flags
   // are raised in band order (after band t - 1's), so the copy stream waits
   // on the last band of each copy only
-  if (a.xflag && lane == 0) {
+  if (a.xflag && lane == 0 && !halo) {
     __threadfence_system();
     int polls = 0;
-    while (SPTRSV_ST_XFLAG_ORDER && t > 0 && (int)(ld_acquire_sys_u32(a.xflag + t - 1) - a.epoch) < 0) {
+    while (SPTRSV_ST_XFLAG_ORDER && band > 0 && (int)(ld_acquire_sys_u32(a.xflag + band - 1) - a.epoch) < 0) {
       if (ld_relaxed_s32(a.abort_flag)) break;  // the flags are released after the kernel anyway
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) break;
       __nanosleep(64);
     }
-    st_release_sys_u32(a.xflag + t, a.epoch);
+    st_release_sys_u32(a.xflag + band, a.epoch);
   }
 }
 
@@ -1549,6 +1568,77 @@ cudaError_t stencil_release_flags(unsigned* f, int n, unsigned v, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Error contraction per grid row of the fast recurrence x = bd + a x_left +
+// u x_up (a = -L[i,i-1]/L_ii, u = -L[i,i-nx]/L_ii): a solve started from a
+// zero row r0 - 1 instead of the true one errs by e with
+// |e_{r,c}| <= A |e_{r,c-1}| + U max|e_{r-1,.}|, e_{r,-1} = 0, so row r's
+// error is at most gamma = U / (1 - A) times row r - 1's (A, U: the largest
+// |a|, |u|). Device max-reduction over the pre-scaled entries.
+__global__ void k_st_decay(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ wv,
+                           long long n, unsigned long long* __restrict__ amax) {
+  unsigned long long ma = 0, mu = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(wv[k]));  // NaN sorts above
+      if (ci[k] == i - 1) ma = max(ma, bits);
+      else mu = max(mu, bits);
+    }
+  atomicMax(amax, ma);
+  atomicMax(amax + 1, mu);
+}
+
+int DevicePlan::stencil_groups(cudaStream_t s) {
+  // SPTRSV_ST_GROUP: bands per group (0: one chain of every band)
+  static const int want = [] {
+    const char* v = std::getenv("SPTRSV_ST_GROUP");
+    return v ? std::atoi(v) : kStGroupDefault;
+  }();
+  const int nb = stencil.n_tasks;
+  if (want <= 0 || nb <= want || !wv || !rp || !ci) return 0;
+  cudaError_t e;
+  if (stencil.decay < 0.0) {
+    unsigned long long* d = nullptr;
+    unsigned long long h[2] = {0, 0};
+    if ((e = cudaMalloc((void**)&d, 2 * sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e)), -1;
+    k_st_decay<<<num_sms * 4, 256, 0, s>>>(rp, ci, wv, n, d);
+    if ((e = cudaGetLastError()) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e)), -1;
+    cudaFree(d);
+    double A, U;
+    std::memcpy(&A, &h[0], 8);
+    std::memcpy(&U, &h[1], 8);
+    stencil.decay = (A < 1.0 && U == U) ? U / (1.0 - A) : 1e300;
+  }
+  // one halo band of 64 rows: the entering error is <= decay^64 |x|; groups
+  // only when that is <= 2^-64 (decay <= 1/2; lap2d: 1/3, i.e. 3e-31)
+  if (!(stencil.decay <= 0.5)) return 0;
+  if (stencil.grp != want) {
+    std::vector<int> tb;
+    for (int b0 = 0; b0 < nb; b0 += want) {
+      if (b0 > 0) tb.push_back(-(b0 - 1) - 1);  // halo: band b0 - 1 from a zero row above
+      for (int b = b0; b < std::min(nb, b0 + want); ++b) tb.push_back(b);
+    }
+    if (stencil.tband) cudaFree(stencil.tband);
+    if (stencil.mbox_grp) cudaFree(stencil.mbox_grp);
+    stencil.tband = nullptr;
+    stencil.mbox_grp = nullptr;
+    const long long words = 2ll * (long long)tb.size() * stencil.nx;
+    if ((e = cudaMalloc((void**)&stencil.tband, sizeof(int) * tb.size())) != cudaSuccess ||
+        (e = cudaMemcpy(stencil.tband, tb.data(), sizeof(int) * tb.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&stencil.mbox_grp, sizeof(unsigned long long) * words)) != cudaSuccess ||
+        (e = fill_not_ready(stencil.mbox_grp, words, s)) != cudaSuccess)
+      return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e)), -1;
+    stencil.grp = want;
+    stencil.grp_tasks = (int)tb.size();
+    stencil.grp_solves = 0;
+  }
+  return 1;
+}
+
 int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bool b_flags, bool x_flags,
                               int copies) {
   if (!stencil.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 2D five-point lower structured");
@@ -1577,11 +1667,18 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     stencil.many_last = copies;
     stencil.many_solves = 0;
   }
-  const int n_tasks = stencil.n_tasks * (many ? copies : 1);
-  unsigned long long* mbox = many ? stencil.mbox_many : stencil.mbox;
+  // fast mode, one right-hand side, one PE: bands in independent groups
+  int grouped = 0;
+  if (!stencil.exact && !many && !stencil.part && kStCluster == 1) {
+    grouped = stencil_groups(s);
+    if (grouped < 0) return SPTRSV_E_CUDA;
+  }
+  const int n_tasks = grouped ? stencil.grp_tasks : stencil.n_tasks * (many ? copies : 1);
+  unsigned long long* mbox = grouped ? stencil.mbox_grp : many ? stencil.mbox_many : stencil.mbox;
   // (the stacked mailboxes keep their halves at the allocated size)
-  const long long half = (long long)(many ? stencil.many_k * stencil.n_tasks : stencil.n_tasks) * stencil.nx;
-  const int par = (int)((many ? stencil.many_solves : stencil.solves) & 1);
+  const long long half =
+      (long long)(grouped ? stencil.grp_tasks : many ? stencil.many_k * stencil.n_tasks : stencil.n_tasks) * stencil.nx;
+  const int par = (int)((grouped ? stencil.grp_solves : many ? stencil.many_solves : stencil.solves) & 1);
   if (stencil.part) {
     for (int t : stencil.host_my_tasks)
       if (t > 0 && !stencil.host_pe_mbox[stencil.host_band_owner[t - 1]])
@@ -1611,7 +1708,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   // write bd = b * (1/d) on the SMs the 64 bands leave idle; SPTRSV_NO_BD=1
   // keeps the multiply in the step, diagnostics)
   static const bool no_bd = std::getenv("SPTRSV_NO_BD") != nullptr;
-  const bool bd_mode = !stencil.exact && !many && kStCluster == 1 && !no_bd;
+  const bool bd_mode = !stencil.exact && !many && kStCluster == 1 && !no_bd && !grouped;
   if (bd_mode) {
     if (!stencil.bd) {
       if ((e = cudaMalloc((void**)&stencil.bd, sizeof(double) * (size_t)n)) != cudaSuccess ||
@@ -1642,7 +1739,9 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.nx = stencil.nx;
   a.ny = stencil.ny * (many ? copies : 1);
   a.n_tasks = n_tasks;
-  a.bands = stencil.n_tasks;
+  a.bands = grouped ? n_tasks : stencil.n_tasks;
+  a.n_bands = stencil.n_tasks;
+  a.tband = grouped ? stencil.tband : nullptr;
   a.steps = stencil.steps_per_task;
   a.probe = opt.probe_flags;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
@@ -1667,7 +1766,8 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     a.prep_tasks = std::max(16, sms - std::min(a.n_my_tasks, sms));
     blocks = std::min(a.n_my_tasks + a.prep_tasks, std::max(sms, a.prep_tasks + 1));
   }
-  ++(many ? stencil.many_solves : stencil.solves);
+  ++(grouped ? stencil.grp_solves : many ? stencil.many_solves : stencil.solves);
+  group_tasks_used = grouped ? stencil.grp_tasks : 0;
   if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = stencil.exact ? launch_stencil<true>(a, blocks, s) : launch_stencil<false>(a, blocks, s);
   if (e != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));

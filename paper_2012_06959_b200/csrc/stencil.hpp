@@ -49,6 +49,13 @@ __host__ __device__ constexpr int st_step_bytes(bool exact) { return st_fields(e
 #endif
 __host__ __device__ constexpr int st_slots(bool exact) { return exact ? SPTRSV_ST_SLOTS_EXACT : SPTRSV_ST_SLOTS_FAST; }
 
+// bands per group of the fast single-right-hand-side 2D wavefront (stencil.cu
+// stencil_groups; SPTRSV_ST_GROUP overrides, 0 = one chain)
+#ifndef SPTRSV_ST_GROUP_DEFAULT
+#define SPTRSV_ST_GROUP_DEFAULT 2
+#endif
+constexpr int kStGroupDefault = SPTRSV_ST_GROUP_DEFAULT;
+
 struct StencilPlan {
   bool ready = false;
   bool exact = true;
@@ -76,6 +83,14 @@ struct StencilPlan {
   // several right-hand sides per launch (solve_many): mailboxes of k stacked
   // copies, [2][k * n_tasks][nx], grown on demand, with their own parity
   unsigned long long* mbox_many = nullptr;
+  // band groups (fast mode, one PE, one right-hand side): groups of `grp`
+  // bands run side by side, each entered through a halo task (stencil.cu);
+  // decay = the plan-time error contraction per grid row (-1: not computed)
+  int grp = 0, grp_tasks = 0;
+  int* tband = nullptr;                    // device [grp_tasks]
+  unsigned long long* mbox_grp = nullptr;  // [2][grp_tasks][nx]
+  long long grp_solves = 0;
+  double decay = -1.0;
   // fast mode, one right-hand side: b * (1/d) written by the kernel's prep
   // tasks (stencil.cu BD kernels) with per-band flags and prep counters
   double* bd = nullptr;
@@ -115,12 +130,17 @@ struct StencilPlan {
   }
   void release() {
     release_part();
-    void* ptrs[] = {stream, mbox, bflag, xflag, mbox_many, bd, bdflag, bd_done};
+    void* ptrs[] = {stream, mbox, bflag, xflag, mbox_many, bd, bdflag, bd_done, tband, mbox_grp};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     stream = nullptr;
     mbox = nullptr;
     mbox_many = nullptr;
+    tband = nullptr;
+    mbox_grp = nullptr;
+    grp = grp_tasks = 0;
+    grp_solves = 0;
+    decay = -1.0;
     bd = nullptr;
     bdflag = nullptr;
     bd_done = nullptr;
