@@ -337,6 +337,7 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
     for (int s = 0; s < 2; ++s) dst[s] = col[(2 * lane + s - p - 1) & (kW - 1)];
   };
   double nb[2];
+  double xs0 = 0.0, xs1 = 0.0;  // this lane's two columns of the current window
   double cf[4][2];  // column j at cf[j % 4] (4 divides the 64-column window), two columns ahead
   wait_chunk_ready(0);
   sload(0, cf[0]);
@@ -364,14 +365,10 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
       if (rel + 2 < ncol) sload(rel + 2, cf[(u + 2) % 4]);
       const double w0 = cf[u % 4][0], w1 = cf[u % 4][1];
       const double xj = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
-      if (lane == owner && j < s1) {
-        if (COUPLED) {
-          a.out[j] = xj;
-        } else {
-          if (a.x_all) a.x_all[j] = xj;
-          if (j >= s0 + a.S - kW)
-          a.out[(size_t)k * kW + (j - (s0 + a.S - kW))] = xj;
-        }
+      (void)j;
+      if (lane == owner) {  // x of the window's columns 2 lane, 2 lane + 1: stored once per window
+        if (os) xs1 = xj;
+        else xs0 = xj;
       }
       double v0 = acc[0], v1 = acc[1];
       if (lane == owner) {
@@ -380,6 +377,23 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
       }
       acc[0] = __fma_rn(w0, xj, v0);
       acc[1] = __fma_rn(w1, xj, v1);
+    }
+    // the window's x: one 16-byte store per lane (K3: x; K1: c into x when the
+    // coupling reach is in use, and c of the block's tail rows)
+    const long long j0 = s0 + c0 + 2 * lane;
+    double* dst = COUPLED ? a.out : a.x_all;
+    if (dst) {
+      if (j0 + 1 < s1 && ((reinterpret_cast<uintptr_t>(dst + j0) & 15) == 0)) {
+        *reinterpret_cast<double2*>(dst + j0) = make_double2(xs0, xs1);
+      } else {
+        if (j0 < s1) dst[j0] = xs0;
+        if (j0 + 1 < s1) dst[j0 + 1] = xs1;
+      }
+    }
+    if (!COUPLED) {
+      const long long t0 = s0 + a.S - kW;
+      if (j0 < s1 && j0 >= t0) a.out[(size_t)k * kW + (j0 - t0)] = xs0;
+      if (j0 + 1 < s1 && j0 + 1 >= t0) a.out[(size_t)k * kW + (j0 + 1 - t0)] = xs1;
     }
   }
 }

@@ -156,6 +156,7 @@ struct DevicePlan {
   } bblk;
   int build_band_blocks();
   int stencil_groups(cudaStream_t s);  // stencil.cu: 1 when the band groups are in use
+  int s3_zgroups(struct Stencil3Plan& P);  // stencil3d.cu: z-groups of the fast 3D wavefront
   int group_tasks_used = 0;            // tasks of the last stencil solve's band groups (0: none)
   int build_superblocks(int s_first, int nsteps, cudaStream_t st);
   int set_band_partition(const int32_t* owner, int pes, int my_pe);

@@ -52,7 +52,7 @@ __host__ __device__ constexpr int st_slots(bool exact) { return exact ? SPTRSV_S
 // bands per group of the fast single-right-hand-side 2D wavefront (stencil.cu
 // stencil_groups; SPTRSV_ST_GROUP overrides, 0 = one chain)
 #ifndef SPTRSV_ST_GROUP_DEFAULT
-#define SPTRSV_ST_GROUP_DEFAULT 2
+#define SPTRSV_ST_GROUP_DEFAULT 1
 #endif
 constexpr int kStGroupDefault = SPTRSV_ST_GROUP_DEFAULT;
 
@@ -178,8 +178,12 @@ struct Stencil3Plan {
   unsigned* xflag = nullptr;  // [n_tasks]
   unsigned epoch = 0;
   int b_chunk_max = 0;
+  // z-groups (fast mode, stencil3d.cu): virtual z-tiles, mailboxes sized by them
+  int nztv = 0, n_vtasks = 0, zgroup = 0, zhalo = 0;
+  int* zmap = nullptr;  // device [nztv]
+  double decay = -1.0;  // plan-time error contraction per z-plane
   void release() {
-    void* ptrs[] = {stream, ymail, zmail, bflag, xflag};
+    void* ptrs[] = {stream, ymail, zmail, bflag, xflag, zmap};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     *this = Stencil3Plan();

@@ -34,6 +34,8 @@
 // the serial oracle's ascending-column order with separate IEEE operations
 // (absent boundary terms contribute +0 and leave every partial sum unchanged),
 // Markstein division with a branch-free guard and an IEEE fallback.
+#include <cmath>
+#include <cstring>
 #include <vector>
 #include <chrono>
 #include <cstring>
@@ -84,7 +86,36 @@ struct S3Args {
   unsigned* xflag;
   unsigned epoch;
   int b_chunk_max;
+  // z-groups (fast mode; null: one z-chain): virtual z-tile zv is real slab
+  // zmap[zv] & 0xFFFFF, a halo tile when bit 20 is set (x discarded), the
+  // first tile of its group (no z-tile behind: a zero plane) when bit 21 is
+  const int* zmap;
+  int nztv;  // virtual z-tiles (tasks = nyt * nztv)
 };
+
+struct S3Tile {
+  int Y, Z, rt;  // tile row, real z-slab, real tile index (coefficient stream, x flags)
+  bool halo, zsrc, pubz;
+};
+__device__ __forceinline__ S3Tile s3_tile(const S3Args& a, int t) {
+  S3Tile q;
+  q.Y = t % a.nyt;
+  const int zv = t / a.nyt;
+  if (!a.zmap) {
+    q.Z = zv;
+    q.halo = false;
+    q.zsrc = zv > 0;
+    q.pubz = zv + 1 < a.nzt;
+  } else {
+    const int m = a.zmap[zv];
+    q.Z = m & 0xFFFFF;
+    q.halo = (m >> 20) & 1;
+    q.zsrc = !((m >> 21) & 1);
+    q.pubz = zv + 1 < a.nztv && !((a.zmap[zv + 1] >> 21) & 1);
+  }
+  q.rt = q.Z * a.nyt + q.Y;
+  return q;
+}
 
 template <bool EXACT>
 struct S3Smem {
@@ -133,9 +164,10 @@ __device__ void s3_loader(const S3Args& a, unsigned char* smem, int* ctl, int t,
   constexpr int NB = S::kSlots;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + S::kBars);
   const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
-  const int Y = t % a.nyt, Z = t / a.nyt;
+  const S3Tile tl = s3_tile(a, t);
+  const int Y = tl.Y, Z = tl.Z;
   const int y = Y * k3Lanes + lane;
-  const unsigned char* tstream = a.stream + (size_t)t * a.steps * S::kStep;
+  const unsigned char* tstream = a.stream + (size_t)tl.rt * a.steps * S::kStep;
   auto issue = [&](int c) {
     const int slot = c % NB;
     if (lane == 0) {
@@ -222,9 +254,10 @@ __device__ void s3_poller(const S3Args& a, unsigned char* smem, int* ctl, int t,
   using S = S3Smem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
-  const int Y = t % a.nyt, Z = t / a.nyt;
+  const S3Tile tl = s3_tile(a, t);
+  const int Y = tl.Y;
   // z-inbox: lane l's row-0 z-neighbours = plane z0 - 1, lane l, of the tile behind
-  const unsigned long long* zsrc = Z > 0 ? a.zmail + ((size_t)(t - a.nyt) * k3Lanes + lane) * a.nx : nullptr;
+  const unsigned long long* zsrc = tl.zsrc ? a.zmail + ((size_t)(t - a.nyt) * k3Lanes + lane) * a.nx : nullptr;
   // y-inbox: lane 0's y-neighbours = lane 31's rows of the tile above; value
   // (k, r, q) of the chunk is polled by lane k * R * C + r * C + q
   const int yk = lane / (k3R * k3C), yr = (lane / k3C) % k3R, yq = lane % k3C;
@@ -301,7 +334,8 @@ __device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t,
                           unsigned long long deadline) {
   using S = S3Smem<EXACT>;
   const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
-  const int Y = t % a.nyt, Z = t / a.nyt;
+  const S3Tile tl = s3_tile(a, t);
+  const int Y = tl.Y, Z = tl.Z;
   const int y = Y * k3Lanes + lane;
   {  // reset this tile's mailboxes in the other half for the next solve
     const ulonglong2 nr = make_ulonglong2(k3NotReady, k3NotReady);
@@ -316,7 +350,7 @@ __device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t,
 #pragma unroll
     for (int k = 0; k < k3G; ++k) {
       const int j = c * k3G + k - lane;
-      if (j < 0 || j >= nblk || y >= a.ny) continue;
+      if (tl.halo || j < 0 || j >= nblk || y >= a.ny) continue;  // a halo tile's x is discarded
 #pragma unroll
       for (int r = 0; r < k3R; ++r) {
         const int z = Z * k3R + r;
@@ -336,15 +370,15 @@ __device__ void s3_storer(const S3Args& a, unsigned char* smem, int* ctl, int t,
   }
   // streamed host solve: tile t's x may be copied once its flag is up; flags
   // go up in tile order so a copy of whole slabs waits on its last tile only
-  if (a.xflag && lane == 0) {
+  if (a.xflag && lane == 0 && !tl.halo) {
     __threadfence_system();
     int polls = 0;
-    while (t > 0 && (int)(ld_acquire_sys_u32(a.xflag + t - 1) - a.epoch) < 0) {
+    while (tl.rt > 0 && (int)(ld_acquire_sys_u32(a.xflag + tl.rt - 1) - a.epoch) < 0) {
       if (ld_relaxed_s32(a.abort_flag)) break;  // released after the kernel anyway
       if ((++polls & 255) == 0 && deadline && globaltimer_ns() > deadline) break;
       __nanosleep(64);
     }
-    st_release_sys_u32(a.xflag + t, a.epoch);
+    st_release_sys_u32(a.xflag + tl.rt, a.epoch);
   }
 }
 
@@ -415,13 +449,14 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
   using S = S3Smem<EXACT>;
   constexpr int NB = S::kSlots;
   const int nchunks = a.steps / k3G, nblk = a.nx / k3C;
-  const int Y = t % a.nyt, Z = t / a.nyt;
+  const S3Tile tl = s3_tile(a, t);
+  const int Y = tl.Y;
   // publish: lane 31's rows for the tile below in y, every lane's last plane
   // for the tile in front in z
   unsigned long long* ypub = a.ymail + (size_t)t * k3R * a.nx;
   unsigned long long* zpub = a.zmail + ((size_t)t * k3Lanes + lane) * a.nx;
   const bool pub_y = lane == k3Lanes - 1 && Y + 1 < a.nyt;
-  const bool pub_z = Z + 1 < a.nzt;
+  const bool pub_z = tl.pubz;
   constexpr bool k3Spec = EXACT && SPTRSV_S3_SPEC && k3C == 2;
   double xleft[k3R], prev[k3R][k3C];
 #pragma unroll
@@ -749,6 +784,76 @@ bool detect_stencil3d(long long n, const std::vector<int>& rp, const std::vector
   return true;
 }
 
+// Error contraction per z-plane of the fast 3D recurrence x = bd + a x_left +
+// u x_up + w x_back (pre-scaled, a / u / w the x / y / z neighbours): a
+// solve started from a zero plane errs by e with
+// |e| <= A |e_left| + U |e_up| + W max|e_{plane behind}| and zero x / y
+// boundaries, so each plane's error is at most gamma = W / (1 - A - U) times
+// the one behind (A, U, W: the largest |a|, |u|, |w|).
+__global__ void k_s3_decay(const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ wv,
+                           long long n, int nx, unsigned long long* __restrict__ amax) {
+  unsigned long long m[3] = {0, 0, 0};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(fabs(wv[k]));  // NaN sorts above
+      const long long d = i - ci[k];
+      const int f = d == 1 ? 0 : d == nx ? 1 : 2;
+      m[f] = max(m[f], bits);
+    }
+  for (int f = 0; f < 3; ++f) atomicMax(amax + f, m[f]);
+}
+
+// z-groups of G real z-tiles (SPTRSV_S3_ZGROUP, default 12; 0: one chain;
+// lap3d-128 fast: one chain 0.225 ms, G = 16: 0.191, G = 12: 0.182),
+// each after the first entered through H halo z-tiles solved from a zero
+// plane, H * k3R planes enough for gamma^(H k3R) <= 2^-64 (lap3d: gamma =
+// 1/4, 32 planes = 8 tiles). Returns 0 (or 1 when grouped), < 0 on error.
+int DevicePlan::s3_zgroups(Stencil3Plan& P) {
+  static const int want = [] {
+    const char* v = std::getenv("SPTRSV_S3_ZGROUP");
+    return v ? std::atoi(v) : 12;
+  }();
+  if (want <= 0 || !wv || !rp || !ci) return 0;
+  cudaError_t e;
+  unsigned long long* d = nullptr;
+  unsigned long long h[3] = {0, 0, 0};
+  if ((e = cudaMalloc((void**)&d, sizeof(h))) != cudaSuccess || (e = cudaMemset(d, 0, sizeof(h))) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  k_s3_decay<<<num_sms * 4, 256, 0, stream>>>(rp, ci, wv, n, P.nx, d);
+  if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess ||
+      (e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  cudaFree(d);
+  double A, U, W;
+  std::memcpy(&A, &h[0], 8);
+  std::memcpy(&U, &h[1], 8);
+  std::memcpy(&W, &h[2], 8);
+  P.decay = (A + U < 1.0 && W == W) ? W / (1.0 - A - U) : 1e300;
+  if (!(P.decay < 1.0) || P.decay <= 0.0) {
+    if (!(P.decay > 0.0) && P.decay == 0.0) {
+      // no z-coupling at all: every group needs no halo (not a 3D stencil in practice)
+    }
+    return 0;
+  }
+  const int planes = (int)std::ceil(64.0 / -std::log2(P.decay));
+  const int H = (planes + k3R - 1) / k3R;
+  if (H >= want || P.nzt <= want + H) return 0;  // the halo would cost more than the chain it cuts
+  std::vector<int> zm;
+  for (int z0 = 0; z0 < P.nzt; z0 += want) {
+    if (z0 > 0)
+      for (int h2 = 0; h2 < H && z0 - H + h2 >= 0; ++h2)
+        zm.push_back((z0 - H + h2) | (1 << 20) | (h2 == 0 || z0 - H + h2 == 0 ? (1 << 21) : 0));
+    for (int z = z0; z < std::min(P.nzt, z0 + want); ++z) zm.push_back(z | (z == 0 ? (1 << 21) : 0));
+  }
+  if ((e = cudaMalloc((void**)&P.zmap, sizeof(int) * zm.size())) != cudaSuccess ||
+      (e = cudaMemcpy(P.zmap, zm.data(), sizeof(int) * zm.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
+  P.nztv = (int)zm.size();
+  P.zgroup = want;
+  P.zhalo = H;
+  return 1;
+}
+
 int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<int>& h_ci) {
   auto t0 = std::chrono::steady_clock::now();
   stencil3.release();
@@ -770,7 +875,14 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
   (void)step_doubles;
   (void)NF;
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
-  const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
+  // fast mode: z-groups when the per-plane error contraction allows a halo
+  P.nztv = P.nzt;
+  if (!exact) {
+    const int rc = s3_zgroups(P);
+    if (rc < 0) return rc;
+  }
+  P.n_vtasks = P.nyt * P.nztv;
+  const long long yw = (long long)P.n_vtasks * k3R * P.nx, zw = (long long)P.n_vtasks * k3Lanes * P.nx;
   if ((e = al((void**)&P.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
       (e = al((void**)&P.zmail, 2 * sizeof(unsigned long long) * zw)) != cudaSuccess ||
@@ -801,7 +913,7 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
 int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, bool flags) {
   Stencil3Plan& P = stencil3;
   if (!P.ready) return plan_fail(SPTRSV_E_UNSUPPORTED, "matrix is not 3D seven-point lower structured");
-  const long long yw = (long long)P.n_tasks * k3R * P.nx, zw = (long long)P.n_tasks * k3Lanes * P.nx;
+  const long long yw = (long long)P.n_vtasks * k3R * P.nx, zw = (long long)P.n_vtasks * k3Lanes * P.nx;
   const int par = (int)(P.solves & 1);
   cudaError_t e;
   // this solve uses mailbox half `par`; reset the other half for the next one
@@ -829,7 +941,9 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, 
   a.spin_initial = opt.spin_initial;
   a.spin_max_ns = opt.spin_max_ns;
   a.nx = P.nx, a.ny = P.ny, a.nz = P.nz, a.nyt = P.nyt, a.nzt = P.nzt;
-  a.n_tasks = P.n_tasks;
+  a.n_tasks = P.n_vtasks;
+  a.zmap = P.zmap;
+  a.nztv = P.nztv;
   a.steps = P.steps;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
@@ -839,7 +953,7 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, 
     cudaMemsetAsync(probe_buf, 0, sizeof(long long) * kProbeWords, s);
     a.dbg = probe_buf;
   }
-  const int blocks = std::max(1, std::min(P.n_tasks, num_sms));
+  const int blocks = std::max(1, std::min(P.n_vtasks, num_sms));
   ++P.solves;
   if ((e = record_k0(s)) != cudaSuccess) return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   e = P.exact ? launch_s3<true>(a, blocks, s) : launch_s3<false>(a, blocks, s);
