@@ -321,11 +321,23 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
     const long long i = s0 + 2 * lane + s;
     acc[s] = i < s1 ? __dmul_rn(a.b[i], a.rdg[i]) : 0.0;
     if (COUPLED && k > 0 && i < s1) {
+      // coupling terms in ascending column order, 16 loads in flight per batch
+      // (one memory round trip per batch instead of one per column)
       const double* tp = a.tt + (size_t)(k - 1) * kW;
-      for (int q = 0; q < kW; ++q) {
-        const long long j = s0 - kW + q;
-        const long long d = i - j;
-        if (d >= 1 && d <= kW) acc[s] = __fma_rn(a.coef[(size_t)j * kW + d - 1], tp[q], acc[s]);
+#pragma unroll
+      for (int q0 = 0; q0 < kW; q0 += 16) {
+        double cw[16], tv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const long long j = s0 - kW + q0 + q, d = i - j;
+          cw[q] = (d >= 1 && d <= kW) ? __ldg(a.coef + (size_t)j * kW + d - 1) : 0.0;
+          tv[q] = __ldg(tp + q0 + q);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const long long d = i - (s0 - kW + q0 + q);
+          if (d >= 1 && d <= kW) acc[s] = __fma_rn(cw[q], tv[q], acc[s]);
+        }
       }
     }
   }
