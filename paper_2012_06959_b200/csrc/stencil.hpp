@@ -180,6 +180,7 @@ struct Stencil3Plan {
   int b_chunk_max = 0;
   // z-groups (fast mode, stencil3d.cu): virtual z-tiles, mailboxes sized by them
   int nztv = 0, n_vtasks = 0, zgroup = 0, zhalo = 0;
+  int nytv = 0, ygrp = 0;  // y-groups: virtual y-slots (2 nyt - 1 with halo rows)
   int* zmap = nullptr;  // device [nztv]
   double decay = -1.0;  // plan-time error contraction per z-plane
   void release() {

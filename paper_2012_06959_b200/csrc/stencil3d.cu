@@ -90,17 +90,31 @@ struct S3Args {
   // zmap[zv] & 0xFFFFF, a halo tile when bit 20 is set (x discarded), the
   // first tile of its group (no z-tile behind: a zero plane) when bit 21 is
   const int* zmap;
-  int nztv;  // virtual z-tiles (tasks = nyt * nztv)
+  int nztv;  // virtual z-tiles (tasks = nytv * nztv)
+  // y-groups (fast mode): every y-tile row Y >= 1 is entered through a halo
+  // copy of row Y - 1 solved from a zero row above (virtual y-slots: 0 = row
+  // 0, 2Y - 1 = halo of row Y - 1, 2Y = row Y); nytv = 2 nyt - 1, else nyt
+  int ygrp, nytv;
 };
 
 struct S3Tile {
   int Y, Z, rt;  // tile row, real z-slab, real tile index (coefficient stream, x flags)
-  bool halo, zsrc, pubz;
+  bool halo, zsrc, pubz, ysrc, puby;  // halo: x discarded; ysrc / puby: y hand-over from t - 1 / to t + 1
 };
 __device__ __forceinline__ S3Tile s3_tile(const S3Args& a, int t) {
   S3Tile q;
-  q.Y = t % a.nyt;
-  const int zv = t / a.nyt;
+  const int yv = t % a.nytv;
+  const int zv = t / a.nytv;
+  if (a.ygrp) {
+    q.Y = (yv + 1) >> 1;  // slot 2Y: row Y; slot 2Y - 1: the halo copy of row Y - 1
+    if (yv & 1) q.Y = (yv - 1) >> 1;
+    q.ysrc = yv > 0 && !(yv & 1);
+    q.puby = yv & 1;
+  } else {
+    q.Y = yv;
+    q.ysrc = yv > 0;
+    q.puby = yv + 1 < a.nyt;
+  }
   if (!a.zmap) {
     q.Z = zv;
     q.halo = false;
@@ -113,6 +127,7 @@ __device__ __forceinline__ S3Tile s3_tile(const S3Args& a, int t) {
     q.zsrc = !((m >> 21) & 1);
     q.pubz = zv + 1 < a.nztv && !((a.zmap[zv + 1] >> 21) & 1);
   }
+  if (a.ygrp && (yv & 1)) q.halo = true;
   q.rt = q.Z * a.nyt + q.Y;
   return q;
 }
@@ -257,11 +272,11 @@ __device__ void s3_poller(const S3Args& a, unsigned char* smem, int* ctl, int t,
   const S3Tile tl = s3_tile(a, t);
   const int Y = tl.Y;
   // z-inbox: lane l's row-0 z-neighbours = plane z0 - 1, lane l, of the tile behind
-  const unsigned long long* zsrc = tl.zsrc ? a.zmail + ((size_t)(t - a.nyt) * k3Lanes + lane) * a.nx : nullptr;
+  const unsigned long long* zsrc = tl.zsrc ? a.zmail + ((size_t)(t - a.nytv) * k3Lanes + lane) * a.nx : nullptr;
   // y-inbox: lane 0's y-neighbours = lane 31's rows of the tile above; value
   // (k, r, q) of the chunk is polled by lane k * R * C + r * C + q
   const int yk = lane / (k3R * k3C), yr = (lane / k3C) % k3R, yq = lane % k3C;
-  const unsigned long long* ysrc = Y > 0 ? a.ymail + ((size_t)(t - 1) * k3R + yr) * a.nx : nullptr;
+  const unsigned long long* ysrc = tl.ysrc ? a.ymail + ((size_t)(t - 1) * k3R + yr) * a.nx : nullptr;
   unsigned long long spins = 0;
   for (int c = 0; c < nchunks; ++c) {
     if (c >= NB && !s3_wait(ctl, kC3InDone, c - NB + 1, deadline, 64)) return s3_abort(a, ctl, lane);
@@ -455,7 +470,7 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
   // for the tile in front in z
   unsigned long long* ypub = a.ymail + (size_t)t * k3R * a.nx;
   unsigned long long* zpub = a.zmail + ((size_t)t * k3Lanes + lane) * a.nx;
-  const bool pub_y = lane == k3Lanes - 1 && Y + 1 < a.nyt;
+  const bool pub_y = lane == k3Lanes - 1 && tl.puby;
   const bool pub_z = tl.pubz;
   constexpr bool k3Spec = EXACT && SPTRSV_S3_SPEC && k3C == 2;
   double xleft[k3R], prev[k3R][k3C];
@@ -555,7 +570,7 @@ __device__ void s3_compute(const S3Args& a, unsigned char* smem, int* ctl, int t
   auto publish_chunk = [&](int c) {
     const double2* src = reinterpret_cast<const double2*>(smem + S::kOut + (c % k3OutSlots) * S::kOutChunk);
     // y: lane 31's rows, one (step, row) per lane
-    if (Y + 1 < a.nyt && lane < k3G * k3R) {
+    if (tl.puby && lane < k3G * k3R) {
       const int k = lane / k3R, r = lane % k3R, jj = c * k3G + k - (k3Lanes - 1);
       if (jj >= 0 && jj < nblk) {
         const double2 v = src[(k * k3Pairs + r) * k3Lanes + k3Lanes - 1];
@@ -829,12 +844,21 @@ int DevicePlan::s3_zgroups(Stencil3Plan& P) {
   std::memcpy(&U, &h[1], 8);
   std::memcpy(&W, &h[2], 8);
   P.decay = (A + U < 1.0 && W == W) ? W / (1.0 - A - U) : 1e300;
-  if (!(P.decay < 1.0) || P.decay <= 0.0) {
-    if (!(P.decay > 0.0) && P.decay == 0.0) {
-      // no z-coupling at all: every group needs no halo (not a 3D stencil in practice)
-    }
-    return 0;
+  // y-groups (SPTRSV_S3_YGROUP=1): the same bound per grid row, gamma_y =
+  // U / (1 - A - W); one 32-row halo tile suffices when gamma_y^32 <= 2^-64
+  // (lap3d: 1/4). Off by default: lap3d-128 0.200 ms with them against 0.181
+  // without (7 y-slots instead of 4: the extra tiles cost more than the two
+  // y-hops they remove)
+  static const int ywant = [] {
+    const char* v = std::getenv("SPTRSV_S3_YGROUP");
+    return v ? std::atoi(v) : 0;
+  }();
+  const double gy = (A + W < 1.0 && U == U) ? U / (1.0 - A - W) : 1e300;
+  if (ywant > 0 && P.nyt > 1 && gy <= 0.25) {
+    P.ygrp = 1;
+    P.nytv = 2 * P.nyt - 1;
   }
+  if (!(P.decay < 1.0) || P.decay <= 0.0) return 0;
   const int planes = (int)std::ceil(64.0 / -std::log2(P.decay));
   const int H = (planes + k3R - 1) / k3R;
   if (H >= want || P.nzt <= want + H) return 0;  // the halo would cost more than the chain it cuts
@@ -877,11 +901,13 @@ int DevicePlan::build_stencil3d(const std::vector<int>& h_rp, const std::vector<
   auto al = [](void** p, size_t b) { return cudaMalloc(p, b < 16 ? 16 : b); };
   // fast mode: z-groups when the per-plane error contraction allows a halo
   P.nztv = P.nzt;
+  P.nytv = P.nyt;
+  P.ygrp = 0;
   if (!exact) {
     const int rc = s3_zgroups(P);
     if (rc < 0) return rc;
   }
-  P.n_vtasks = P.nyt * P.nztv;
+  P.n_vtasks = P.nytv * P.nztv;
   const long long yw = (long long)P.n_vtasks * k3R * P.nx, zw = (long long)P.n_vtasks * k3Lanes * P.nx;
   if ((e = al((void**)&P.stream, bytes)) != cudaSuccess ||
       (e = al((void**)&P.ymail, 2 * sizeof(unsigned long long) * yw)) != cudaSuccess ||
@@ -944,6 +970,8 @@ int DevicePlan::solve_stencil3d(const double* d_b, double* d_x, cudaStream_t s, 
   a.n_tasks = P.n_vtasks;
   a.zmap = P.zmap;
   a.nztv = P.nztv;
+  a.ygrp = P.ygrp;
+  a.nytv = P.nytv;
   a.steps = P.steps;
   a.b_aligned = ((uintptr_t)d_b & 15) == 0;
   a.x_aligned = ((uintptr_t)d_x & 15) == 0;
