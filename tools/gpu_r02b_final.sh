@@ -4,7 +4,7 @@
 # command, and ncu --set full captures of the headline stencil kernel, the
 # band-block solve kernels (TMA sweeps + superblock chain) and the component
 # pool on rmat-4M (their DRAM bytes feed profiles/traffic.json).
-o=gpurun_out/final3
+o=gpurun_out/final4
 mkdir -p $o
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
@@ -24,8 +24,9 @@ cap() {  # name regex count run_one-args...
 }
 # fast single right-hand side: band groups (no prep tasks), one chain (SPTRSV_ST_GROUP=0: the BD kernel)
 cap stencil_fast 'k_stencil2dILb0ELi0ELb0ELi1ELb0ELb0' 1 --config lap2d-4096 --executor stencil --precision fast
-SPTRSV_ST_GROUP=1 cap stencil_fast_g1 'k_stencil2dILb0ELi0ELb0ELi1ELb0ELb0' 1 --config lap2d-4096 --executor stencil --precision fast
-for G in 0 1 4 8; do SPTRSV_ST_GROUP=$G timeout 300 python bench.py --no-cpu-baseline > $o/bench_group$G.json 2> $o/bench_group$G.err; done
+ncu -i $o/stencil_fast.ncu-rep --page source --csv --print-source cuda,sass > $o/stencil_fast_source.csv 2>&1
+for G in 0 2 4 8; do SPTRSV_ST_GROUP=$G timeout 300 python bench.py --no-cpu-baseline > $o/bench_group$G.json 2> $o/bench_group$G.err; done
+cap stencil3d_fast 'k_stencil3d' 1 --config lap3d-128 --executor stencil --precision fast
 cap band_fast 'k_bb_sweep_tma|k_bb_chain' 5 --config banded-8M --executor band --precision fast
 cap rows_rmat 'k_rowsILi1' 1 --config rmat-4M --executor rows --precision fast
 rm -f $o/*.ncu-rep.tmp
