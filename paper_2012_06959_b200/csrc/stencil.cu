@@ -1594,7 +1594,13 @@ int DevicePlan::stencil_groups(cudaStream_t s) {
     return v ? std::atoi(v) : kStGroupDefault;
   }();
   const int nb = stencil.n_tasks;
-  if (want <= 0 || nb <= want || !wv || !rp || !ci) return 0;
+  // the bands this plan solves: all of them, or this PE's under a partition
+  // (whose first band is then entered through a local halo instead of the
+  // peer's mailboxes: a fast PE solve reads nothing from other GPUs)
+  std::vector<int> bands;
+  if (stencil.part) bands = stencil.host_my_tasks;
+  else for (int b = 0; b < nb; ++b) bands.push_back(b);
+  if (want <= 0 || bands.empty() || (!stencil.part && nb <= want) || !wv || !rp || !ci) return 0;
   cudaError_t e;
   if (stencil.decay < 0.0) {
     unsigned long long* d = nullptr;
@@ -1616,11 +1622,15 @@ int DevicePlan::stencil_groups(cudaStream_t s) {
   // one halo band of 64 rows: the entering error is <= decay^64 |x|; groups
   // only when that is <= 2^-64 (decay <= 1/2; lap2d: 1/3, i.e. 3e-31)
   if (!(stencil.decay <= 0.5)) return 0;
-  if (stencil.grp != want) {
+  if (stencil.grp != want || stencil.grp_bands != bands) {
+    // groups of up to `want` consecutive bands; a group not starting at band 0
+    // is entered through a halo task (band b0 - 1 from a zero row above)
     std::vector<int> tb;
-    for (int b0 = 0; b0 < nb; b0 += want) {
-      if (b0 > 0) tb.push_back(-(b0 - 1) - 1);  // halo: band b0 - 1 from a zero row above
-      for (int b = b0; b < std::min(nb, b0 + want); ++b) tb.push_back(b);
+    for (size_t k = 0; k < bands.size();) {
+      const int b0 = bands[k];
+      if (b0 > 0) tb.push_back(-(b0 - 1) - 1);
+      int len = 0;
+      while (k < bands.size() && len < want && bands[k] == b0 + len) tb.push_back(bands[k++]), ++len;
     }
     if (stencil.tband) cudaFree(stencil.tband);
     if (stencil.mbox_grp) cudaFree(stencil.mbox_grp);
@@ -1633,6 +1643,7 @@ int DevicePlan::stencil_groups(cudaStream_t s) {
         (e = fill_not_ready(stencil.mbox_grp, words, s)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e)), -1;
     stencil.grp = want;
+    stencil.grp_bands = bands;
     stencil.grp_tasks = (int)tb.size();
     stencil.grp_solves = 0;
   }
@@ -1667,9 +1678,10 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
     stencil.many_last = copies;
     stencil.many_solves = 0;
   }
-  // fast mode, one right-hand side, one PE: bands in independent groups
+  // fast mode, one right-hand side: bands in independent groups (under a PE
+  // partition: this PE's bands, no peer reads)
   int grouped = 0;
-  if (!stencil.exact && !many && !stencil.part && kStCluster == 1) {
+  if (!stencil.exact && !many && kStCluster == 1) {
     grouped = stencil_groups(s);
     if (grouped < 0) return SPTRSV_E_CUDA;
   }
@@ -1679,7 +1691,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   const long long half =
       (long long)(grouped ? stencil.grp_tasks : many ? stencil.many_k * stencil.n_tasks : stencil.n_tasks) * stencil.nx;
   const int par = (int)((grouped ? stencil.grp_solves : many ? stencil.many_solves : stencil.solves) & 1);
-  if (stencil.part) {
+  if (stencil.part && !grouped) {
     for (int t : stencil.host_my_tasks)
       if (t > 0 && !stencil.host_pe_mbox[stencil.host_band_owner[t - 1]])
         return plan_fail(SPTRSV_E_INVALID_PE, "the mailboxes of a peer PE were never imported");
@@ -1697,7 +1709,7 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.ticket = ticket;
   a.n_my_tasks = n_tasks;
   a.my_pe = -1;
-  if (stencil.part) {
+  if (stencil.part && !grouped) {
     a.my_tasks = stencil.my_tasks;
     a.n_my_tasks = stencil.n_my_tasks;
     a.pe_mbox = stencil.pe_mbox;
@@ -1739,7 +1751,9 @@ int DevicePlan::solve_stencil(const double* d_b, double* d_x, cudaStream_t s, bo
   a.nx = stencil.nx;
   a.ny = stencil.ny * (many ? copies : 1);
   a.n_tasks = n_tasks;
-  a.bands = grouped ? n_tasks : stencil.n_tasks;
+  // (grouped: only task 0 may be "first of a right-hand side", and the
+  // coefficient stream index band % bands must not wrap for a PE's bands)
+  a.bands = grouped ? std::max(n_tasks, stencil.n_tasks) : stencil.n_tasks;
   a.n_bands = stencil.n_tasks;
   a.tband = grouped ? stencil.tband : nullptr;
   a.steps = stencil.steps_per_task;

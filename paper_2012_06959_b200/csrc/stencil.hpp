@@ -88,6 +88,7 @@ struct StencilPlan {
   // decay = the plan-time error contraction per grid row (-1: not computed)
   int grp = 0, grp_tasks = 0;
   int* tband = nullptr;                    // device [grp_tasks]
+  std::vector<int> grp_bands;              // the bands the groups were built for
   unsigned long long* mbox_grp = nullptr;  // [2][grp_tasks][nx]
   long long grp_solves = 0;
   double decay = -1.0;
@@ -139,6 +140,7 @@ struct StencilPlan {
     tband = nullptr;
     mbox_grp = nullptr;
     grp = grp_tasks = 0;
+    grp_bands.clear();
     grp_solves = 0;
     decay = -1.0;
     bd = nullptr;

@@ -65,7 +65,9 @@ def test_partitioned_pool_segments_bit_exact(n_pes, shape):
 def test_dropin_n_pes_keeps_the_wavefront(n_pes, precision):
     """SolverConfig.n_pes > 1 through the drop-in solve(): a 2D five-point L with
     whole 64-row bands per PE keeps the stencil executor (one plan per PE,
-    peers' mailboxes), and x equals the oracle bitwise in exact mode."""
+    peers' mailboxes), and x equals the oracle bitwise in exact mode. In fast
+    mode (lap2d: error contraction 1/3 per grid row) every PE enters its
+    bands through local halo bands, so it reads nothing from its peers."""
     l = synth.lap2d(256, 512)  # 8 bands: whole bands per PE for 2 and 4 PEs
     b = np.random.default_rng(5).uniform(-1.0, 1.0, l.n)
     plan = sp.block_partition(l.n, n_pes)
@@ -79,7 +81,10 @@ def test_dropin_n_pes_keeps_the_wavefront(n_pes, precision):
             assert x.tobytes() == ref.tobytes()
         else:
             assert sp.compare_solutions(x, ref, 1e-12).within_tol
-        assert report.device["remote_reads"] > 0
+        if precision == "exact":
+            assert report.device["remote_reads"] > 0
+        else:
+            assert report.device["remote_reads"] == 0
         assert report.totals()["components_solved"] == l.n
 
 
@@ -185,8 +190,9 @@ def _band_owner_map(l, nx, pes, kind):
 def test_stencil_partition_plans_on_one_device(pes, kind, precision):
     """One plan per PE (as one process per GPU would hold), wired by device
     pointer on one GPU: each solves its own bands concurrently, polling the
-    band above a PE boundary from the peer's mailboxes. Repeated solves
-    exercise the parity double-buffer of the mailboxes."""
+    band above a PE boundary from the peer's mailboxes (exact mode; fast mode
+    enters each band through a local halo band and reads nothing remote).
+    Repeated solves exercise the parity double-buffer of the mailboxes."""
     torch = pytest.importorskip("torch")
     nx, ny = 128, 64 * 6 - 17  # last band partial
     l = synth.lap2d(nx, ny)
@@ -223,7 +229,10 @@ def test_stencil_partition_plans_on_one_device(pes, kind, precision):
             assert x.tobytes() == ref.tobytes()
         else:
             assert np.max(np.abs(x - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-12
-        assert sum(st["remote_reads"] for st in stats) > 0
+        if precision == "exact":
+            assert sum(st["remote_reads"] for st in stats) > 0
+        else:  # diagonally dominant: every PE enters its bands through local halo bands
+            assert sum(st["remote_reads"] for st in stats) == 0
         assert all(st["executor"] == "stencil" for st in stats)
     for pl in plans:
         pl.close()
