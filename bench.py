@@ -234,7 +234,9 @@ def main():
         if solver.replicated:  # no per-PE mode for this executor: every rank solves the whole system
             info["executor"] = f"{info['executor']} (replicated per rank: no per-PE mode)"
         else:
-            info["executor"] = f"{info['executor']} (PE partition, peer {'mailboxes' if info['executor'] == 'stencil' else 'segments'})"
+            via = {"stencil": ("local halo bands" if args.precision == "fast" else "peer mailboxes"),
+                   "band": "superblock chain through peer slots"}.get(info["executor"], "peer segments")
+            info["executor"] = f"{info['executor']} (PE partition, {via})"
 
     db = torch.from_numpy(b).to(f"cuda:{dev}")
     dx = torch.zeros_like(db)

@@ -77,7 +77,9 @@ class DistributedSolver:
         self.world = plan.n_pes
         self.group = group
         # auto: a 2D five-point L with a band-aligned owner map runs the stencil
-        # executor partitioned (peer mailboxes); a banded L in fast mode with
+        # executor partitioned (exact: peer mailboxes; fast on a diagonally
+        # dominant L: each rank enters its bands through local halo bands and
+        # reads nothing remote); a banded L in fast mode with
         # slabs on row-block boundaries the band-block executor partitioned
         # (each rank sweeps its blocks, the tail chain passes rank to rank
         # through one 64-value slot); an unstructured L the component pool with
