@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(64) k_bb_ntail(const double* __restrict__ coef
   // blocks 1 .. nblk - 2: block 0 has no coupling and the last block's tail
   // feeds no further block (it is also the only block that may be partial)
   const int k = blockIdx.x + 1;
-  if (k >= nblk - 1) return;
+  // the last block (launched only when it is whole: reach) feeds no tail
+  if (k > nblk - 1 || (k == nblk - 1 && (long long)k * S + S > n)) return;
   const long long s0 = (long long)k * S;
   const int tid = threadIdx.x, h = tid >> 5, lane = tid & 31, m = 32 * h + lane;
   double acc[kW];
@@ -936,7 +937,8 @@ int DevicePlan::build_band_blocks() {
   }();
   if (reach_on) {
     std::vector<int> r0(nblk, 0);
-    r0[nblk - 1] = (int)S;
+    // (a whole last block gets its reach from k_bb_ntail too; a partial one is swept whole)
+    r0[nblk - 1] = (n % S == 0 && nblk > 2) ? 0 : (int)S;
     if ((e = al((void**)&bblk.reach, sizeof(int) * nblk)) != cudaSuccess ||
         (e = cudaMemcpy(bblk.reach, r0.data(), sizeof(int) * nblk, cudaMemcpyHostToDevice)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
@@ -945,7 +947,10 @@ int DevicePlan::build_band_blocks() {
     static std::atomic<unsigned long long> attr{0};
     if ((e = set_max_dyn_smem(k_bb_ntail, kNtSmem, attr)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
-    k_bb_ntail<<<nblk - 2, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt, bblk.reach);
+    // blocks 1 .. nblk - 2 (their tails feed the chain) and, when whole, the
+    // last block (its reach only; its tail slot nt[nblk - 2] is never read)
+    const int nt_blocks = (n % S == 0) ? nblk - 1 : nblk - 2;
+    k_bb_ntail<<<nt_blocks, 64, kNtSmem, stream>>>(band.coef, n, (int)S, nblk, bblk.nt, bblk.reach);
     if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(stream)) != cudaSuccess)
       return plan_fail(SPTRSV_E_CUDA, cudaGetErrorString(e));
   }
