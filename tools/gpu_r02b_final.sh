@@ -4,7 +4,7 @@
 # command, and ncu --set full captures of the headline stencil kernel, the
 # band-block solve kernels (TMA sweeps + superblock chain) and the component
 # pool on rmat-4M (their DRAM bytes feed profiles/traffic.json).
-o=gpurun_out/final4
+o=gpurun_out/final5
 mkdir -p $o
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $o/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
