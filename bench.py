@@ -55,6 +55,23 @@ METRIC = "SpTRSV µs/solve and GFLOP/s (2·nnz/t) at 1/2/4/8 B200; % of HBM roof
 UNIT = "GFLOP/s"
 
 
+def _method(config: str, precision: str, executor: str) -> str:
+    """How the executor solved this config, for the bench line."""
+    ex = executor.split(" ")[0]
+    fast = precision == "fast"
+    if ex == "stencil" and config.startswith("lap2d"):
+        return ("2D wavefront, bands entered through halo bands when the plan-time error contraction allows "
+                "(lap2d: <= 3e-31 |x|; SPTRSV_ST_GROUP=0: one chain)") if fast else "2D wavefront, one band chain (bitwise)"
+    if ex == "stencil":
+        return ("3D wavefront, z-groups entered through halo z-tiles (<= 2^-64 |x|; SPTRSV_S3_ZGROUP=0: one chain)"
+                if fast else "3D wavefront, one chain (bitwise)")
+    if ex == "band":
+        return ("row blocks: TMA-streamed sweeps, tail chain by superblocks, coupling reach (terms <= 2^-64 dropped)"
+                if fast else "band window kernel (bitwise)")
+    if ex == "rows":
+        return "component pool (level-ordered tickets, value-is-flag polling)"
+    return ex
+
 def algorithmic_bytes(n: int, nnz: int) -> int:
     """int32 indices/pointers, f64 values, b and x."""
     return 12 * nnz + 4 * (n + 1) + 8 * n + 8 * n
@@ -411,6 +428,7 @@ def main():
             "rhs": "ones",
             "precision": args.precision,
             "executor": info["executor"],
+            "method": _method(args.config, args.precision, info["executor"]),
             "parallelism": (f"column-block x{ws} ({partition.kind} partition), IPC peer segments" if ws > 1
                             else "single GPU"),
             "l2": (f"flushed: 256 MB scratch write between timed solves (solve inputs {alg / 1e6:.0f} MB vs "
