@@ -40,7 +40,10 @@ struct DevicePlan {
   int* order = nullptr;
   long long order_len = 0;
   int coop_long = 0;
-  static constexpr int kLongDeps = 32;    // rows with more dependencies are solved warp-wide
+#ifndef SPTRSV_LONG_DEPS
+#define SPTRSV_LONG_DEPS 32
+#endif
+  static constexpr int kLongDeps = SPTRSV_LONG_DEPS;  // rows with more dependencies are solved warp-wide
   static constexpr int kSplitDeps = 256;  // fast mode: rows with more are split into partial tasks
   struct SplitRows {
     int n_heavy = 0;
