@@ -364,7 +364,6 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
 #pragma unroll
     for (int u = 0; u < kW; ++u) {
       const int rel = c0 + u;
-      const long long j = s0 + rel;
       const int owner = u >> 1, os = u & 1;
       if (u % kCw == 0 && rel > 0) {
         // every read of the previous chunk has completed: refill its slot
@@ -378,7 +377,6 @@ __global__ void __launch_bounds__(32 * kBBWarps) k_bb_sweep_tma(const __grid_con
       if (rel + 2 < ncol) sload(rel + 2, cf[(u + 2) % 4]);
       const double w0 = cf[u % 4][0], w1 = cf[u % 4][1];
       const double xj = __shfl_sync(0xffffffffu, os ? acc[1] : acc[0], owner);
-      (void)j;
       if (lane == owner) {  // x of the window's columns 2 lane, 2 lane + 1: stored once per window
         if (os) xs1 = xj;
         else xs0 = xj;
